@@ -1,0 +1,166 @@
+/* clothsim_b200 - C ABI of the sm_100a cloth pipeline.
+ *
+ * Drop-in boundary for the reference's hot path, Simulation.step()
+ * (pkg/src/clothsim/stepper.py:454-624) and the stage functions it calls.
+ * Plain pointers and sizes only (no torch types).  "device" pointers are CUDA
+ * device memory; "host" pointers are ordinary CPU memory.  Every entry point
+ * returns 0 on success or a status code:
+ *
+ *   CS_PENETRATION  (1)  impact at t <= 0      -> clothsim.PenetrationError   (stepper.py:450-451)
+ *   CS_NONFINITE    (2)  non-finite target     -> FloatingPointError          (mesh.py:194-195)
+ *   CS_DIVERGENCE   (3)  smoother blew up      -> clothsim.SmootherDivergence (smoothing.py:55-62)
+ *   CS_BAD_DIAGONAL (4)  nonpositive diagonal  -> ValueError                  (smoothing.py:39-40)
+ *   CS_BAD_ARGUMENT (5)  invalid size/argument -> ValueError
+ *   >= 1000              CUDA runtime error (1000 + cudaError_t)
+ *
+ * Which reference interface each entry point replaces is cited per function;
+ * INTEGRATION.md shows the ctypes binding.
+ */
+#ifndef CLOTHSIM_B200_H
+#define CLOTHSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_OK 0
+#define CS_PENETRATION 1
+#define CS_NONFINITE 2
+#define CS_DIVERGENCE 3
+#define CS_BAD_DIAGONAL 4
+#define CS_BAD_ARGUMENT 5
+
+typedef struct cs_scene cs_scene;
+
+/* Static scene description; all pointers are HOST memory, copied at creation.
+ * Produced by paper_2403_19272_b200/device.py from the reference-compatible
+ * setup objects (ClothMesh, ElasticConstraints, GlobalSystem, Subspace). */
+typedef struct {
+    int n_cloth, n_free, n_pinned, n_obstacle, n_world;
+    int n_edges, n_stencils;
+    int n_world_tris, n_world_edges;
+    int r_bar, r;
+    /* cloth */
+    const int *free_ids;        /* (n_free) */
+    const int *free_index;      /* (n_cloth) -1 if pinned */
+    const int *pin_ids;         /* (n_pinned) */
+    const double *mass;         /* (n_cloth) */
+    const double *fext;         /* (n_cloth*3) gravity force m g */
+    const double *mass_over_h2; /* (n_free) */
+    const int *edge_v;          /* (n_edges*2) */
+    const double *edge_rest, *edge_w;
+    const int *rhs_inc_ptr, *rhs_inc;   /* (n_cloth+1), (2 n_edges) codes e*2+endpoint, np.add.at order */
+    const int *grad_inc_ptr, *grad_inc; /* same, endpoint-1 block first (energy gradient order) */
+    const int *stencils;        /* (n_stencils*4) */
+    const double *bend_k, *bend_w;
+    const int *bend_inc_ptr, *bend_inc; /* codes s*4+j */
+    /* global matrix H (free x free), SELL-32 */
+    int sell_nslices;
+    const int *sell_slice_ptr, *sell_col;
+    const double *sell_val, *diag;
+    const int *hfp_ptr, *hfp_col;       /* pinned columns, hfp_col = cloth vertex id */
+    const double *hfp_val;
+    /* rest-shape eigenbasis */
+    const double *U;            /* (n_free*r_bar) row-major */
+    const double *eigenvalues;  /* (r_bar) */
+    /* collision world (cloth vertices first, then obstacles) */
+    const int *world_tris, *world_edges;
+    const uint8_t *tri_static, *vert_static, *vert_used, *edge_static;
+    const int *edge_tris, *edge_slot;   /* (n_world_edges*2) */
+    const int *patch, *patch_slot;      /* (n_world_tris) reference build_patches partition */
+    /* static-topology trees (Morton order of rest pose) */
+    const int *tri_left, *tri_right, *tri_parent, *tri_leaf_parent, *tri_prim;
+    const int *edge_left, *edge_right, *edge_parent, *edge_leaf_parent, *edge_prim;
+    /* initial state */
+    const double *x0;           /* (n_cloth*3) */
+    const double *obstacle_x0;  /* (n_obstacle*3) */
+} cs_scene_desc;
+
+/* Mirrors reference StepConfig (stepper.py:43-79); NDB barrier mode. */
+typedef struct {
+    double h, eps_initial, eps_inner, eps_outer, eps_toi, alpha;
+    double ndb_k, ndb_base, d_hat, omega, rf_tolerance, delta_f_cap;
+    int iteration_cap, samples, smoothing_iterations;
+    int warm_start_cap, inner_cap, outer_cap, rf_iterations;
+} cs_step_config;
+
+/* Mirrors reference StepReport (stepper.py:81-92) + device-side diagnostics. */
+typedef struct {
+    int lg_iterations, outer_loops, full_ccd_calls, partial_ccd_calls;
+    int active_pairs, rf_triggered, cap_hit, warm_start_iterations;
+    double toi_exit;
+    /* stage times in ms (CUDA events), reference timing keys */
+    double t_warm_start, t_local, t_global, t_smoothing, t_broad, t_narrow_partial, t_narrow_full, t_rf;
+    int n_outer_deltas;
+    double outer_deltas[64];
+    long long pairs_last_site, pairs_max_site;
+    int reduced_fallbacks;
+    long long gpu_launches;
+} cs_step_report;
+
+/* ---- scene lifetime ---------------------------------------------------- */
+/* replaces Simulation.__init__'s device-side state (stepper.py:127-173) */
+cs_scene *cs_scene_create(const cs_scene_desc *desc, const cs_step_config *cfg, int *status);
+void cs_scene_destroy(cs_scene *scene);
+int cs_scene_set_config(cs_scene *scene, const cs_step_config *cfg);
+
+/* ---- the hot path ------------------------------------------------------- */
+/* Simulation.step() (stepper.py:454-624): pin_next (n_pinned*3) and obstacle_next
+ * (n_obstacle*3) are HOST arrays (prescribed positions at t+h; may be NULL =
+ * stay put).  stream: cudaStream_t (NULL = legacy default stream). */
+int cs_step(cs_scene *scene, const double *pin_next, const double *obstacle_next, cs_step_report *report,
+            void *stream);
+
+/* SimState access (mesh.py:55-73), HOST arrays (n_cloth*3 each; obstacle n_obstacle*3). */
+int cs_get_state(cs_scene *scene, double *x, double *x_dot, double *x_prev, double *delta_f, double *obstacle_x,
+                 int *step_index, void *stream);
+int cs_set_state(cs_scene *scene, const double *x, const double *x_dot, const double *x_prev, const double *delta_f,
+                 const double *obstacle_x, int step_index, void *stream);
+/* device pointers of the resident state (n_cloth*3 doubles each) */
+int cs_state_device(cs_scene *scene, double **x, double **x_dot, double **delta_f, double **obstacle_x);
+
+/* ---- per-stage entry points (DEVICE pointers) ---------------------------- */
+/* full_ccd (collision/ccd.py:138-196): toi (P) nan = miss */
+int cs_full_ccd(const int8_t *kind, const int *idx4, const double *x_start, const double *x_end, long long P,
+                double tol, double *toi, void *stream);
+/* distance_toi (collision/ccd.py:221-266) */
+int cs_distance_toi(const int8_t *kind, const int *idx4, const double *x_start, const double *x_end, long long P,
+                    double floor_frac, int max_iterations, double *toi, void *stream);
+/* partial_ccd (collision/partial.py:149-204): active (P) 0/1; samples in {1,3,6} */
+int cs_partial_ccd(const int8_t *kind, const int *idx4, const double *x_start, const double *x_end, long long P,
+                   int samples, uint8_t *active, void *stream);
+/* pair_witness (collision/geometry.py:115-148) + Simulation._witness normal (stepper.py:194-216);
+ * p1/p2 may be NULL */
+int cs_pair_witness(const int8_t *kind, const int *idx4, const double *x, long long P, double *p1, double *p2,
+                    double *bary, double *dist, double *normal, void *stream);
+/* broad_phase (collision/bvh.py:207-292) over the scene's world topology.  Runs the
+ * query into the scene's pair buffer and returns the pair count; cs_scene_pairs
+ * copies kind/idx (DEVICE pointers, capacity >= count) out. */
+int cs_broad_phase(cs_scene *scene, const double *x_start_w, const double *x_end_w, double margin,
+                   long long *count, void *stream);
+int cs_scene_pairs(cs_scene *scene, int8_t *kind, int *idx4, void *stream);
+/* assemble_rhs (constraints.py:229-256); coll_* (n_coll) are the flat
+ * (ids, weights, targets) of Simulation._collision_terms in order; ids are cloth ids. */
+int cs_assemble_rhs(cs_scene *scene, const double *z, const double *x, const int *coll_ids, const double *coll_w,
+                    const double *coll_t, int n_coll, double *b, double *delta, void *stream);
+/* ajacobi_smooth (smoothing.py:23-66), x (n_free*3) updated in place; delta may be NULL */
+int cs_ajacobi_smooth(cs_scene *scene, const double *b, double *x, int iterations, double omega,
+                      const double *delta, void *stream);
+/* reduced_correction (subspace.py:165-186); reuse != 0 keeps the last reduced system */
+int cs_reduced_correction(cs_scene *scene, const double *b, double *x, const double *delta, int reuse,
+                          void *stream);
+/* warmstart_correction (subspace.py:189-192) */
+int cs_warmstart_correction(cs_scene *scene, const double *b, double *x, void *stream);
+/* Simulation.energy gradient (stepper.py:309-380, "quad" form); grad (n_cloth*3) */
+int cs_energy_gradient(cs_scene *scene, const double *x, const double *z, const int *q_ids, const double *q_w,
+                       const double *q_t, int n_q, double *grad, void *stream);
+
+const char *cs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CLOTHSIM_B200_H */

@@ -1,0 +1,393 @@
+"""Collision API surface of the drop-in (mirrors ``clothsim.collision``).
+
+Per-pair narrow-phase stages run on the GPU through the C ABI
+(``cs_full_ccd``, ``cs_distance_toi``, ``cs_partial_ccd``, ``cs_pair_witness``);
+the numpy-signature wrappers below copy inputs to the device, launch, and copy
+results back, so reference callers and tests can be re-pointed unchanged.
+
+Static setup pieces live here too: the reference's patch partition
+(``build_patches``, reference bvh.py:20-51 - needed to reproduce the
+reference's edge-edge row orientation) and the world topology + static
+Morton-order trees the device broad phase refits each query.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from collections import deque
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+VT = 0
+EE = 1
+LIFE_SPAN_CAP = 64                 # reference pairs.py:21
+PATCH_TARGET = 8                   # reference bvh.py:17
+
+
+# ------------------------------------------------------------------ pair records
+@dataclass
+class PairSet:
+    """Batched pairs + life spans/weights/witness (reference pairs.py:24-62)."""
+
+    kind: np.ndarray
+    idx: np.ndarray
+    life_span: np.ndarray
+    weight: np.ndarray
+    bary: np.ndarray = field(default=None)
+    distance: np.ndarray = field(default=None)
+    normal: np.ndarray = field(default=None)
+
+    @classmethod
+    def empty(cls) -> "PairSet":
+        return cls(np.zeros(0, np.int8), np.zeros((0, 4), np.int64), np.zeros(0, np.int64), np.zeros(0),
+                   np.zeros((0, 2)), np.zeros(0), np.zeros((0, 3)))
+
+    def __len__(self) -> int:
+        return len(self.kind)
+
+    def keys(self) -> np.ndarray:
+        """Canonical carry-over keys (reference pairs.py:51-62)."""
+        c = self.idx.copy()
+        vt = self.kind == VT
+        ee = self.kind == EE
+        c[vt, 1:] = np.sort(c[vt, 1:], axis=1)
+        c[ee, :2] = np.sort(c[ee, :2], axis=1)
+        c[ee, 2:] = np.sort(c[ee, 2:], axis=1)
+        flip = ee & (c[:, 0] > c[:, 2])
+        c[flip] = c[flip][:, [2, 3, 0, 1]]
+        return np.concatenate([self.kind[:, None].astype(np.int64), c], axis=1)
+
+
+def ndb_weights(life_span, k: float, base: float) -> np.ndarray:
+    """k * base**min(span, 64) (reference pairs.py:65-70); device twin in narrow.cu."""
+    if k <= 0 or base <= 1:
+        raise ValueError("need k > 0 and base > 1")
+    return k * np.power(base, np.minimum(life_span, LIFE_SPAN_CAP).astype(np.float64))
+
+
+def update_ndb_weights(pairs: PairSet, active, k: float, base: float) -> PairSet:
+    """reference pairs.py:73-80."""
+    pairs.life_span = np.where(active, np.minimum(pairs.life_span + 1, LIFE_SPAN_CAP), 0)
+    pairs.weight = ndb_weights(pairs.life_span, k, base)
+    return pairs
+
+
+# ------------------------------------------------------------------ sample patterns
+_TRI = {1: [[1 / 3, 1 / 3]], 3: [[1 / 6, 1 / 6], [2 / 3, 1 / 6], [1 / 6, 2 / 3]],
+        6: [[1 / 6, 1 / 6], [2 / 3, 1 / 6], [1 / 6, 2 / 3], [0.5, 0.25], [0.25, 0.5], [1 / 3, 1 / 3]]}
+_BOX = {1: [[0.5, 0.5]], 3: [[0.25, 0.25], [0.5, 0.5], [0.75, 0.75]],
+        6: [[0.25, 0.25], [0.5, 0.5], [0.75, 0.75], [0.25, 0.75], [0.75, 0.25], [0.5, 0.25]]}
+
+
+@dataclass
+class SampleSet:
+    """Partial-CCD sample points (reference partial.py:53-65)."""
+
+    vt_points: np.ndarray
+    ee_points: np.ndarray
+    interval: float
+    includes_projection: bool = True
+
+    @property
+    def count(self) -> int:
+        return len(self.vt_points)
+
+
+def _covering(points: np.ndarray, tri: bool, grid: int = 64) -> float:
+    g = np.linspace(0.0, 1.0, grid)
+    gx, gy = np.meshgrid(g, g)
+    probe = np.stack([gx.ravel(), gy.ravel()], axis=1)
+    if tri:
+        probe = probe[probe.sum(axis=1) <= 1.0]
+    return float(np.linalg.norm(probe[:, None, :] - points[None], axis=2).min(axis=1).max())
+
+
+def default_samples(count: int = 3) -> SampleSet:
+    """Built-in patterns (reference partial.py:79-85)."""
+    if count not in _TRI:
+        raise ValueError(f"no built-in pattern with {count} samples (choose 1, 3 or 6)")
+    vt = np.asarray(_TRI[count], dtype=np.float64)
+    ee = np.asarray(_BOX[count], dtype=np.float64)
+    return SampleSet(vt, ee, max(_covering(vt, True), _covering(ee, False)))
+
+
+def sample_bound(h0: float, h1: float, edge_bound: float, alpha: float) -> float:
+    """Eq. 14 sampling interval (reference partial.py:105-114)."""
+    if not (h0 > 0 and h1 >= h0 and edge_bound > 0 and 0 < alpha < 1):
+        raise ValueError("need h0 > 0, h1 >= h0, edge_bound > 0, 0 < alpha < 1")
+    return (1.0 / alpha - 1.0) * h0 * h0 / (2.0 * np.sqrt(2.0) * edge_bound * (h1 + 2.0 * edge_bound))
+
+
+# ------------------------------------------------------------------ GPU per-stage wrappers
+def _dev(a, dtype):
+    import torch
+
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def _pair_inputs(kind, idx, *xs):
+    import torch
+
+    k = _dev(np.asarray(kind, dtype=np.int8), torch.int8)
+    i = _dev(np.asarray(idx, dtype=np.int32).reshape(-1, 4), torch.int32)
+    return k, i, [_dev(np.asarray(x, dtype=np.float64), torch.float64) for x in xs]
+
+
+def full_ccd(kind, idx, x_start, x_end, tol: float = 1e-6) -> np.ndarray:
+    """GPU twin of reference full_ccd (ccd.py:138-196): TOI per pair, nan = miss."""
+    import torch
+
+    lib = _lib.load()
+    m = len(kind)
+    if m == 0:
+        return np.full(0, np.nan)
+    k, i, (a, b) = _pair_inputs(kind, idx, x_start, x_end)
+    out = torch.empty(m, dtype=torch.float64, device="cuda")
+    _lib.check(lib.cs_full_ccd(k.data_ptr(), i.data_ptr(), a.data_ptr(), b.data_ptr(), m, tol, out.data_ptr(),
+                               _lib.stream_handle()), "cs_full_ccd")
+    return out.cpu().numpy()
+
+
+def distance_toi(kind, idx, x_start, x_end, floor_frac: float = 0.2, max_iterations: int = 64) -> np.ndarray:
+    """GPU twin of reference distance_toi (ccd.py:221-266)."""
+    import torch
+
+    lib = _lib.load()
+    m = len(kind)
+    if m == 0:
+        return np.full(0, np.nan)
+    k, i, (a, b) = _pair_inputs(kind, idx, x_start, x_end)
+    out = torch.empty(m, dtype=torch.float64, device="cuda")
+    _lib.check(lib.cs_distance_toi(k.data_ptr(), i.data_ptr(), a.data_ptr(), b.data_ptr(), m, floor_frac,
+                                   max_iterations, out.data_ptr(), _lib.stream_handle()), "cs_distance_toi")
+    return out.cpu().numpy()
+
+
+def global_toi(kind, idx, x_start, x_end, alpha: float = 0.8) -> float:
+    """Step scale from the minimum impact time (reference ccd.py:269-285)."""
+    toi = full_ccd(kind, idx, x_start, x_end)
+    hits = toi[~np.isnan(toi)]
+    if hits.size == 0:
+        return 1.0
+    t = float(hits.min())
+    if t <= 0.0:
+        raise RuntimeError(f"nonpositive impact time {t}: start state was not collision-free "
+                           f"(pair {int(np.nanargmin(toi))})")
+    return alpha * t
+
+
+def partial_ccd(kind, idx, x_start, x_end, samples: SampleSet) -> np.ndarray:
+    """GPU twin of reference partial_ccd (partial.py:149-204)."""
+    import torch
+
+    lib = _lib.load()
+    m = len(kind)
+    if m == 0:
+        return np.zeros(0, dtype=bool)
+    k, i, (a, b) = _pair_inputs(kind, idx, x_start, x_end)
+    out = torch.empty(m, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.cs_partial_ccd(k.data_ptr(), i.data_ptr(), a.data_ptr(), b.data_ptr(), m, samples.count,
+                                  out.data_ptr(), _lib.stream_handle()), "cs_partial_ccd")
+    return out.cpu().numpy().astype(bool)
+
+
+def pair_witness(kind, idx, x):
+    """GPU twin of reference pair_witness (geometry.py:115-148): (p1, p2, bary, dist)."""
+    import torch
+
+    lib = _lib.load()
+    m = len(kind)
+    if m == 0:
+        z = np.zeros((0, 3))
+        return z, z.copy(), np.zeros((0, 2)), np.zeros(0)
+    k, i, (xx,) = _pair_inputs(kind, idx, x)
+    p1 = torch.empty((m, 3), dtype=torch.float64, device="cuda")
+    p2 = torch.empty_like(p1)
+    bary = torch.empty((m, 2), dtype=torch.float64, device="cuda")
+    dist = torch.empty(m, dtype=torch.float64, device="cuda")
+    _lib.check(lib.cs_pair_witness(k.data_ptr(), i.data_ptr(), xx.data_ptr(), m, p1.data_ptr(), p2.data_ptr(),
+                                   bary.data_ptr(), dist.data_ptr(), None, _lib.stream_handle()), "cs_pair_witness")
+    return p1.cpu().numpy(), p2.cpu().numpy(), bary.cpu().numpy(), dist.cpu().numpy()
+
+
+def witness_normals(kind, idx, x):
+    """bary, distance and separating normal as Simulation._witness sets them (stepper.py:194-216)."""
+    import torch
+
+    lib = _lib.load()
+    m = len(kind)
+    if m == 0:
+        return np.zeros((0, 2)), np.zeros(0), np.zeros((0, 3))
+    k, i, (xx,) = _pair_inputs(kind, idx, x)
+    bary = torch.empty((m, 2), dtype=torch.float64, device="cuda")
+    dist = torch.empty(m, dtype=torch.float64, device="cuda")
+    nrm = torch.empty((m, 3), dtype=torch.float64, device="cuda")
+    _lib.check(lib.cs_pair_witness(k.data_ptr(), i.data_ptr(), xx.data_ptr(), m, None, None, bary.data_ptr(),
+                                   dist.data_ptr(), nrm.data_ptr(), _lib.stream_handle()), "cs_pair_witness")
+    return bary.cpu().numpy(), dist.cpu().numpy(), nrm.cpu().numpy()
+
+
+# ------------------------------------------------------------------ static world topology
+def build_patches(triangles: np.ndarray, n_vertices: int = 0) -> list:
+    """Greedy BFS grouping of edge-connected triangles into patches of <= 8.
+
+    Same partition as reference bvh.py:20-51 (its order decides which edge of
+    an edge-edge pair the reference lists first).
+    """
+    tris = np.asarray(triangles, dtype=np.int64)
+    m = len(tris)
+    pending: dict = {}
+    adj = [[] for _ in range(m)]
+    for t, (a, b, c) in enumerate(tris.tolist()):
+        for u, w in ((a, b), (b, c), (c, a)):
+            key = (u, w) if u < w else (w, u)
+            o = pending.pop(key, None)
+            if o is None:
+                pending[key] = t
+            else:
+                adj[t].append(o)
+                adj[o].append(t)
+    owner = [-1] * m
+    groups = []
+    for seed in range(m):
+        if owner[seed] >= 0:
+            continue
+        pid = len(groups)
+        grp = [seed]
+        owner[seed] = pid
+        q = deque([seed])
+        while q and len(grp) < PATCH_TARGET:
+            t = q.popleft()
+            for u in adj[t]:
+                if owner[u] < 0 and len(grp) < PATCH_TARGET:
+                    owner[u] = pid
+                    grp.append(u)
+                    q.append(u)
+        groups.append(np.asarray(grp, dtype=np.int64))
+    return groups
+
+
+def _spread_bits(v: np.ndarray) -> np.ndarray:
+    v = v.astype(np.uint64) & np.uint64(0x3FF)
+    v = (v | (v << np.uint64(16))) & np.uint64(0x030000FF)
+    v = (v | (v << np.uint64(8))) & np.uint64(0x0300F00F)
+    v = (v | (v << np.uint64(4))) & np.uint64(0x030C30C3)
+    v = (v | (v << np.uint64(2))) & np.uint64(0x09249249)
+    return v
+
+
+def morton_tree(centroids: np.ndarray):
+    """Balanced binary tree over Morton-sorted primitives (built once, refit per query).
+
+    Returns int32 arrays (left, right, parent, leaf_parent, prim); child codes
+    >= 0 are internal nodes, < 0 encode leaf position ~pos.
+    """
+    L = len(centroids)
+    lo = centroids.min(axis=0)
+    span = np.maximum(centroids.max(axis=0) - lo, 1e-30)
+    q = np.clip(((centroids - lo) / span * 1023.0).astype(np.int64), 0, 1023)
+    code = (_spread_bits(q[:, 0]) << np.uint64(2)) | (_spread_bits(q[:, 1]) << np.uint64(1)) | _spread_bits(q[:, 2])
+    prim = np.lexsort((np.arange(L), code)).astype(np.int32)
+    ni = max(L - 1, 1)
+    left = np.full(ni, -1, np.int32)
+    right = np.full(ni, -1, np.int32)
+    parent = np.full(ni, -1, np.int32)
+    leaf_parent = np.full(L, -1, np.int32)
+    if L == 1:
+        return left, right, parent, leaf_parent, prim
+    ids, lo_r, hi_r = np.array([0]), np.array([0]), np.array([L])
+    nxt = 1
+    while ids.size:
+        mid = (lo_r + hi_r) // 2
+        child_ids = []
+        new_ids, new_lo, new_hi = [], [], []
+        for side, (a, b) in enumerate(((lo_r, mid), (mid, hi_r))):
+            size = b - a
+            leaf = size == 1
+            code_arr = np.empty(ids.size, np.int64)
+            code_arr[leaf] = ~a[leaf]
+            leaf_parent[a[leaf]] = ids[leaf]
+            k = int((~leaf).sum())
+            fresh = np.arange(nxt, nxt + k)
+            nxt += k
+            code_arr[~leaf] = fresh
+            parent[fresh] = ids[~leaf]
+            new_ids.append(fresh)
+            new_lo.append(a[~leaf])
+            new_hi.append(b[~leaf])
+            child_ids.append(code_arr)
+        left[ids] = child_ids[0]
+        right[ids] = child_ids[1]
+        ids = np.concatenate(new_ids)
+        lo_r = np.concatenate(new_lo)
+        hi_r = np.concatenate(new_hi)
+    return left, right, parent, leaf_parent, prim
+
+
+@dataclass
+class CollisionWorld:
+    """Static world topology (cloth first, then obstacles) for the device broad phase.
+
+    Plays the role of the reference's PatchBVH (bvh.py:54-137): fixed topology
+    from the rest pose, boxes refit per query.  ``triangles``/``tri_static``
+    keep the reference attribute names.
+    """
+
+    triangles: np.ndarray
+    tri_static: np.ndarray
+    edges: np.ndarray
+    tri_edges: np.ndarray
+    patches: list
+    patch_of_tri: np.ndarray
+    slot_of_tri: np.ndarray
+    edge_tris: np.ndarray
+    edge_slot: np.ndarray
+    vert_static: np.ndarray
+    vert_used: np.ndarray
+    edge_static: np.ndarray
+    tri_tree: tuple
+    edge_tree: tuple
+
+    @classmethod
+    def build(cls, triangles, rest_positions, tri_static=None) -> "CollisionWorld":
+        tris = np.asarray(triangles, dtype=np.int64)
+        m = len(tris)
+        nw = len(rest_positions)
+        stat = np.zeros(m, bool) if tri_static is None else np.asarray(tri_static, dtype=bool)
+        stack = np.concatenate([tris[:, [0, 1]], tris[:, [1, 2]], tris[:, [2, 0]]])
+        stack.sort(axis=1)
+        edges, inv = np.unique(stack, axis=0, return_inverse=True)
+        inv = inv.reshape(-1)
+        tri_edges = inv.reshape(3, m).T.copy()
+        owner = np.tile(np.arange(m), 3)
+        slot = np.repeat(np.arange(3), m)
+        order = np.argsort(inv, kind="stable")
+        cnt = np.bincount(inv, minlength=len(edges))
+        start = np.concatenate([[0], np.cumsum(cnt)[:-1]])
+        edge_tris = np.full((len(edges), 2), -1, np.int64)
+        edge_slot = np.zeros((len(edges), 2), np.int64)
+        edge_tris[:, 0] = owner[order[start]]
+        edge_slot[:, 0] = slot[order[start]]
+        two = cnt >= 2
+        edge_tris[two, 1] = owner[order[start[two] + 1]]
+        edge_slot[two, 1] = slot[order[start[two] + 1]]
+        patches = build_patches(tris, nw)
+        patch_of = np.zeros(m, np.int64)
+        slot_of = np.zeros(m, np.int64)
+        for p, g in enumerate(patches):
+            patch_of[g] = p
+            slot_of[g] = np.arange(len(g))
+        used = np.zeros(nw, bool)
+        used[tris.ravel()] = True
+        vstat = np.ones(nw, bool)
+        vstat[tris[~stat].ravel()] = False
+        estat = np.zeros(len(edges), bool)
+        estat[tri_edges[stat].ravel()] = True
+        rest = np.asarray(rest_positions, dtype=np.float64)
+        tri_tree = morton_tree(rest[tris].mean(axis=1))
+        edge_tree = morton_tree(rest[edges].mean(axis=1))
+        return cls(tris, stat, edges, tri_edges, patches, patch_of, slot_of, edge_tris, edge_slot, vstat, used,
+                   estat, tri_tree, edge_tree)

@@ -1,0 +1,1242 @@
+// C ABI + native step driver for the sm_100a cloth pipeline.
+//
+// cs_step() is reference Simulation.step() (pkg/src/clothsim/stepper.py:454-624)
+// in the NDB barrier mode: warm start -> CCD site -> outer/inner local-global
+// loops (collision stamps, rhs, reduced correction, A-Jacobi smoothing, partial
+// CCD + life-span update) -> CCD site per outer loop -> exit line search ->
+// residual forwarding (:626-672).  All arithmetic runs in the kernels of
+// narrow.cu / solver.cu / broad.cu / pairs.cu; the host only sequences launches
+// and reads back one small scalar block at each data-dependent branch (the
+// reference's own sync points: RMS exits, TOI clamps, pair counts).
+//
+// Single translation unit (unity build) so kernels stay in one module.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "narrow.cu"
+#include "solver.cu"
+#include "broad.cu"
+#include "pairs.cu"
+#include "../../include/clothsim_b200.h"
+
+using namespace cs;
+
+#define CS_TRY(expr)                                   \
+    do {                                               \
+        cudaError_t e_ = (expr);                       \
+        if (e_ != cudaSuccess) return 1000 + (int)e_;  \
+    } while (0)
+#define CS_RET(expr)               \
+    do {                           \
+        int rc_ = (expr);          \
+        if (rc_ != 0) return rc_;  \
+    } while (0)
+
+namespace {
+
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    int ensure(size_t m) {
+        if (m <= n && p) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        size_t want = std::max<size_t>(m, 1);
+        if (n) want = std::max(want, n + n / 2);
+        cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+        if (e != cudaSuccess) {
+            n = 0;
+            p = nullptr;
+            return 1000 + (int)e;
+        }
+        n = want;
+        return 0;
+    }
+    int upload(const T* host, size_t m) {
+        CS_RET(ensure(m));
+        if (m && host) {
+            cudaError_t e = cudaMemcpy(p, host, m * sizeof(T), cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return 1000 + (int)e;
+        }
+        return 0;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct TreeBuf {
+    int nleaf = 0;
+    DBuf<int> left, right, parent, leaf_parent, prim, flags;
+    DBuf<double> node_lo, node_hi, leaf_lo, leaf_hi;
+    int create(int nl, const int* l, const int* r, const int* par, const int* lpar, const int* pr) {
+        nleaf = nl;
+        const int ni = std::max(nl - 1, 1);
+        CS_RET(left.upload(l, nl - 1));
+        CS_RET(right.upload(r, nl - 1));
+        CS_RET(parent.upload(par, nl - 1));
+        CS_RET(leaf_parent.upload(lpar, nl));
+        CS_RET(prim.upload(pr, nl));
+        CS_RET(flags.ensure(ni));
+        CS_RET(node_lo.ensure(3 * (size_t)ni));
+        CS_RET(node_hi.ensure(3 * (size_t)ni));
+        CS_RET(leaf_lo.ensure(3 * (size_t)nl));
+        CS_RET(leaf_hi.ensure(3 * (size_t)nl));
+        return 0;
+    }
+    Tree view() {
+        Tree t;
+        t.nleaf = nleaf;
+        t.left = left.p;
+        t.right = right.p;
+        t.parent = parent.p;
+        t.leaf_parent = leaf_parent.p;
+        t.prim = prim.p;
+        t.node_lo = node_lo.p;
+        t.node_hi = node_hi.p;
+        t.leaf_lo = leaf_lo.p;
+        t.leaf_hi = leaf_hi.p;
+        t.flags = flags.p;
+        return t;
+    }
+};
+
+struct PairBuf {
+    long long P = 0;
+    DBuf<int8_t> kind;
+    DBuf<int4> idx;
+    DBuf<unsigned long long> keys;
+    DBuf<double> toi, filt, bary, dist, normal, weight;
+    DBuf<int> life;
+    DBuf<uint8_t> engaged;
+    int reserve(long long m) {
+        CS_RET(kind.ensure(m));
+        CS_RET(idx.ensure(m));
+        CS_RET(keys.ensure(m));
+        CS_RET(toi.ensure(m));
+        CS_RET(filt.ensure(m));
+        CS_RET(bary.ensure(2 * m));
+        CS_RET(dist.ensure(m));
+        CS_RET(normal.ensure(3 * m));
+        CS_RET(weight.ensure(m));
+        CS_RET(life.ensure(m));
+        CS_RET(engaged.ensure(m));
+        return 0;
+    }
+    void release() {
+        kind.release(); idx.release(); keys.release(); toi.release(); filt.release(); bary.release();
+        dist.release(); normal.release(); weight.release(); life.release(); engaged.release();
+    }
+};
+
+// scalar slots (doubles) read back in one D2H copy
+enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_NORM1 = 5, S_NORM_F = 6,
+       S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_COUNT = 16 };
+enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_COUNT = 8 };
+
+const int kStages = 8;
+enum { T_WARM = 0, T_LOCAL, T_GLOBAL, T_SMOOTH, T_BROAD, T_PARTIAL, T_FULL, T_RF };
+
+}  // namespace
+
+struct cs_scene {
+    // sizes
+    int n = 0, nf = 0, npin = 0, nobs = 0, nw = 0, ne = 0, ns = 0, ntw = 0, new_ = 0, rb = 0, r = 0;
+    cs_step_config cfg{};
+    SamplePattern pat{};
+    // static cloth data
+    DBuf<int> free_ids, free_index, pin_ids, pin_slot;
+    DBuf<double> mass, fext, mh2;
+    DBuf<int> e0, e1, rinc_ptr, rinc, ginc_ptr, ginc, st, binc_ptr, binc;
+    DBuf<double> erest, ew, bk, bw;
+    DBuf<int> sell_ptr, sell_col, hfp_ptr, hfp_col;
+    DBuf<double> sell_val, diag, hfp_val;
+    int nslices = 0;
+    bool has_fp = false;
+    DBuf<double> U, V, lam;
+    // world topology
+    DBuf<int> wtris, wedges, edge_tris, edge_slot, patch, pslot;
+    DBuf<uint8_t> tri_static, vert_static, vert_used, edge_static;
+    TreeBuf ttree, etree;
+    // state
+    DBuf<double> x, v, xprev, df, obs;
+    int step_index = 0;
+    // work arrays
+    DBuf<double> z, xs_w, xc_w, anchor_w, tmp_w, xf, xf0, b, t, delta, prev_outer, grad, fr;
+    DBuf<double> pins_next_d, obs_next_d;
+    DBuf<double> vlo, vhi;
+    DBuf<int> counts, offsets;
+    PairBuf pa, pb;  // current and next pair sets
+    PairBuf* cur = &pa;
+    PairBuf* nxt = &pb;
+    DBuf<int> sel, skey, ssrc, skey_s, ssrc_s, seg_beg, seg_end, rowflag, rows_act;
+    DBuf<double> sw, stt;
+    DBuf<unsigned long long> hkeys;
+    DBuf<int> hvals;
+    DBuf<double> part, part2, rhs_red, gram_red, q, Xred, beta_red, norms;
+    int pending_checks = 0;
+    DBuf<int> counts2, offsets2;
+    DBuf<int> fallback;
+    DBuf<char> cub_tmp;
+    DBuf<double> d_scal;
+    DBuf<int> d_iscal;
+    double* h_scal = nullptr;
+    int* h_iscal = nullptr;
+    cudaStream_t s = 0;
+    long long launches = 0;
+    // timing
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> spans;
+    int active_stage = -1;
+    cudaEvent_t stage_start{};
+    int sm_count = 148;
+    bool stamps_valid = false;   // seg_beg/seg_end hold stamps for the current rhs
+    int n_stamp_rows = 0;
+
+    // ------------------------------------------------------------ utilities
+    cudaEvent_t ev() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+    void stage(int k) {  // switch the timed stage (-1 = none)
+        if (active_stage == k) return;
+        cudaEvent_t e = ev();
+        cudaEventRecord(e, s);
+        if (active_stage >= 0) spans.push_back({active_stage, {stage_start, e}});
+        active_stage = k;
+        stage_start = e;
+    }
+    int sync_scalars() {
+        CS_TRY(cudaMemcpyAsync(h_scal, d_scal.p, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(h_iscal, d_iscal.p, I_COUNT * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        return check_divergence();
+    }
+    int grid(long long m, int bs = 256) { return (int)std::max<long long>(1, (m + bs - 1) / bs); }
+
+    Sell sell() { return Sell{nf, nslices, sell_ptr.p, sell_col.p, sell_val.p}; }
+    EdgeSet edges() { return EdgeSet{e0.p, e1.p, erest.p, ew.p}; }
+
+    // ------------------------------------------------------------ reductions
+    // slot = sqrt(sum (a[ids] - b)^2) over n rows (b may be null)
+    int sqnorm(const double* a, const double* bb, int rows, const int* ids, int slot) {
+        int g = std::min(grid(rows), 2 * sm_count);
+        CS_RET(part.ensure(g));
+        k_sqdiff_partial<<<g, 256, 0, s>>>(a, bb, rows, ids, part.p);
+        k_norm_final<<<1, 256, 0, s>>>(part.p, g, d_scal.p + slot);
+        launches += 2;
+        CS_CHECK_LAUNCH();
+        return 0;
+    }
+
+    // ------------------------------------------------------------ solver stages
+    // b, delta for cloth positions xcl (n,3) (pinned rows carry the pin targets)
+    int assemble_rhs(const double* zc, const double* xcl, bool with_stamps) {
+        const int* sb = with_stamps ? seg_beg.p : nullptr;
+        k_assemble_rhs<<<grid(nf), 256, 0, s>>>(nf, free_ids.p, xcl, zc, mh2.p, edges(), rinc_ptr.p, rinc.p,
+                                                has_fp ? hfp_ptr.p : nullptr, hfp_col.p, hfp_val.p, xcl, sb,
+                                                seg_end.p, ssrc_s.p, sw.p, stt.p, b.p, delta.p);
+        ++launches;
+        CS_CHECK_LAUNCH();
+        return 0;
+    }
+
+    // rank-2 A-Jacobi on x (nf,3) in place (smoothing.py:23-66).  The residual
+    // norms at k = 0, 10, 20, ... are kept on device and compared at the next
+    // host sync (check_divergence): a diverging step is discarded either way.
+    int smooth(const double* bb, double* xx, int iterations, double omega, const double* dl) {
+        const int steps = (iterations + 1) / 2;
+        const double c = 1.0 - omega;
+        const int g = grid(nf);
+        CS_RET(part.ensure(g));
+        const int nchk = (steps + 9) / 10;
+        CS_RET(norms.ensure(std::max(nchk, 1)));
+        for (int k = 0; k < steps; ++k) {
+            const bool chk = (k % 10) == 0;
+            k_jacobi_a<<<g, 256, 0, s>>>(sell(), diag.p, dl, bb, xx, t.p, chk ? part.p : nullptr);
+            if (chk) {
+                k_norm_final<<<1, 256, 0, s>>>(part.p, g, norms.p + k / 10);
+                ++launches;
+            }
+            k_jacobi_b<<<g, 256, 0, s>>>(sell(), diag.p, dl, t.p, c, xx);
+            launches += 2;
+            CS_CHECK_LAUNCH();
+        }
+        pending_checks = nchk;
+        return 0;
+    }
+
+    int check_divergence() {
+        if (pending_checks < 2) {
+            pending_checks = 0;
+            return 0;
+        }
+        std::vector<double> hn(pending_checks);
+        CS_TRY(cudaMemcpyAsync(hn.data(), norms.p, sizeof(double) * pending_checks, cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        const int m = pending_checks;
+        pending_checks = 0;
+        for (int i = 1; i < m; ++i)
+            if (hn[i] > 10.0 * hn[i - 1]) return CS_DIVERGENCE;
+        return 0;
+    }
+
+    // reduced correction in the reuse basis (subspace.py:165-186); x (nf,3) in place
+    int reduced(const double* bb, double* xx, const double* dl, bool refactor, int n_rows_act_known) {
+        const int g = std::min(cs_div_up(nf, PROJ_TILE), 2 * sm_count);
+        CS_RET(part.ensure((size_t)g * 3 * r));
+        k_project_partial<<<g, 256, 0, s>>>(sell(), bb, xx, dl, V.p, r, part.p);
+        k_reduce_partials<<<cs_div_up(3 * r, 32), 256, 0, s>>>(part.p, g, 3 * r, rhs_red.p);
+        launches += 2;
+        const double* gram = nullptr;
+        if (refactor && n_rows_act_known > 0) {
+            const int gg = std::min(cs_div_up(n_rows_act_known, 8), sm_count);
+            CS_RET(part2.ensure((size_t)gg * r * r));
+            k_gram_partial<<<gg, 256, 0, s>>>(rows_act.p, d_iscal.p + I_ROWS, dl, V.p, r, part2.p);
+            k_reduce_partials<<<cs_div_up(r * r, 32), 256, 0, s>>>(part2.p, gg, r * r, gram_red.p);
+            launches += 2;
+            gram = gram_red.p;
+        }
+        ReducedState rs{Xred.p, beta_red.p, fallback.p};
+        k_reduced_solve<<<1, 256, 0, s>>>(rhs_red.p, gram, lam.p, r, 0, refactor ? 1 : 0, rs, q.p);
+        k_prolong<<<cs_div_up((long long)nf * 32, 256), 256, 0, s>>>(V.p, r, q.p, nf, xx);
+        launches += 2;
+        CS_CHECK_LAUNCH();
+        return 0;
+    }
+
+    // warm-start correction in the wide basis (subspace.py:189-192)
+    int warm_correction(const double* bb, double* xx) {
+        const int g = std::min(cs_div_up(nf, PROJ_TILE), 2 * sm_count);
+        CS_RET(part.ensure((size_t)g * 3 * rb));
+        k_project_partial<<<g, 256, 0, s>>>(sell(), bb, xx, nullptr, U.p, rb, part.p);
+        k_reduce_partials<<<cs_div_up(3 * rb, 32), 256, 0, s>>>(part.p, g, 3 * rb, rhs_red.p);
+        ReducedState rs{Xred.p, beta_red.p, fallback.p};
+        k_reduced_solve<<<1, 256, 0, s>>>(rhs_red.p, nullptr, lam.p, rb, 1, 0, rs, q.p);
+        k_prolong<<<cs_div_up((long long)nf * 32, 256), 256, 0, s>>>(U.p, rb, q.p, nf, xx);
+        launches += 4;
+        CS_CHECK_LAUNCH();
+        return 0;
+    }
+
+    // ------------------------------------------------------------ collision stages
+    WorldTopo world() {
+        WorldTopo w;
+        w.nw = nw;
+        w.tris = wtris.p;
+        w.edges = wedges.p;
+        w.tri_static = tri_static.p;
+        w.vert_static = vert_static.p;
+        w.vert_used = vert_used.p;
+        w.edge_static = edge_static.p;
+        w.edge_tris = edge_tris.p;
+        w.edge_slot = edge_slot.p;
+        w.patch = patch.p;
+        w.pslot = pslot.p;
+        return w;
+    }
+
+    int scan(const int* in, int* out, int m) {
+        size_t bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, m, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp.p, bytes, in, out, m, s));
+        return 0;
+    }
+
+    // broad phase into pr (bvh.py:207-292): count -> scan -> write, one host sync
+    int broad_phase(const double* xa, const double* xb, double margin, PairBuf& pr) {
+        k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(xa, xb, nw, margin, vlo.p, vhi.p);
+        CS_TRY(cudaMemsetAsync(ttree.flags.p, 0, sizeof(int) * std::max(ttree.nleaf - 1, 1), s));
+        CS_TRY(cudaMemsetAsync(etree.flags.p, 0, sizeof(int) * std::max(etree.nleaf - 1, 1), s));
+        k_refit<<<grid(ttree.nleaf), 256, 0, s>>>(ttree.view(), wtris.p, 3, vlo.p, vhi.p);
+        k_refit<<<grid(etree.nleaf), 256, 0, s>>>(etree.view(), wedges.p, 2, vlo.p, vhi.p);
+        CS_TRY(cudaMemsetAsync(counts.p + nw, 0, sizeof(int), s));
+        CS_TRY(cudaMemsetAsync(counts2.p + new_, 0, sizeof(int), s));
+        k_query_vt<0><<<grid(nw, 128), 128, 0, s>>>(ttree.view(), world(), vlo.p, vhi.p, counts.p, nullptr,
+                                                      nullptr, nullptr, nullptr);
+        k_query_ee<0><<<grid(new_, 128), 128, 0, s>>>(etree.view(), world(), new_, vlo.p, vhi.p, counts2.p,
+                                                        nullptr, nullptr, nullptr, nullptr);
+        launches += 5;
+        CS_CHECK_LAUNCH();
+        CS_RET(scan(counts.p, offsets.p, nw + 1));
+        CS_RET(scan(counts2.p, offsets2.p, new_ + 1));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_VT], offsets.p + nw, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_EE], offsets2.p + new_, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        const long long n_vt = h_iscal[I_VT], n_ee = h_iscal[I_EE];
+        const long long P = n_vt + n_ee;
+        CS_RET(pr.reserve(std::max<long long>(P, 1)));
+        k_query_vt<1><<<grid(nw, 128), 128, 0, s>>>(ttree.view(), world(), vlo.p, vhi.p, nullptr, offsets.p,
+                                                      pr.kind.p, pr.idx.p, pr.keys.p);
+        k_query_ee<1><<<grid(new_, 128), 128, 0, s>>>(etree.view(), world(), new_, vlo.p, vhi.p, nullptr,
+                                                        offsets2.p, pr.kind.p + n_vt, pr.idx.p + n_vt,
+                                                        pr.keys.p + n_vt);
+        launches += 2;
+        CS_CHECK_LAUNCH();
+        pr.P = P;
+        return 0;
+    }
+
+    // broad -> full CCD -> distance march -> clamp factor (stepper.py:426-452)
+    int ccd_site(const double* xa, const double* xb, PairBuf& pr, cs_step_report* rep, double& clamp) {
+        stage(T_BROAD);
+        CS_RET(broad_phase(xa, xb, cfg.d_hat, pr));
+        stage(T_FULL);
+        const long long P = pr.P;
+        if (P > 0) {
+            k_full_ccd<<<grid(P, 128), 128, 0, s>>>(pr.kind.p, pr.idx.p, xa, xb, P, P == 1 ? 1 : 0, 1e-6, pr.toi.p);
+            k_distance_toi<<<grid(P, 128), 128, 0, s>>>(pr.kind.p, pr.idx.p, xa, xb, P, 1.0 - cfg.alpha, 64,
+                                                        pr.filt.p);
+            launches += 2;
+            const int g = std::min(grid(P), 2 * sm_count);
+            CS_RET(part.ensure(g));
+            k_min_toi_partial<<<g, 256, 0, s>>>(pr.filt.p, P, part.p);
+            k_min_toi_final<<<1, 256, 0, s>>>(part.p, g, cfg.alpha, d_scal.p + S_CLAMP_MIN);
+            launches += 2;
+            CS_CHECK_LAUNCH();
+            CS_RET(sync_scalars());
+            if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;
+            clamp = h_scal[S_CLAMP];
+        } else {
+            clamp = 1.0;
+        }
+        if (rep) {
+            rep->full_ccd_calls += 1;
+            rep->pairs_last_site = P;
+            rep->pairs_max_site = std::max(rep->pairs_max_site, P);
+        }
+        return 0;
+    }
+
+    int witness(PairBuf& pr, const double* xw) {
+        if (pr.P == 0) return 0;
+        k_witness<<<grid(pr.P, 128), 128, 0, s>>>(pr.kind.p, pr.idx.p, xw, pr.P, pr.bary.p, pr.dist.p,
+                                                  pr.normal.p, nullptr, nullptr);
+        ++launches;
+        CS_CHECK_LAUNCH();
+        return 0;
+    }
+
+    // engaged set + weights after a site; count lands in I_ENG
+    int engage(PairBuf& pr) {
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
+        if (pr.P == 0) return 0;
+        k_engage_init<<<grid(pr.P), 256, 0, s>>>(pr.toi.p, pr.dist.p, pr.life.p, pr.P, cfg.d_hat, cfg.ndb_k,
+                                                 cfg.ndb_base, pr.engaged.p, pr.weight.p, d_iscal.p + I_ENG);
+        ++launches;
+        CS_CHECK_LAUNCH();
+        return 0;
+    }
+
+    // life-span carry old -> new (stepper.py:300-305)
+    int carry(PairBuf& old, PairBuf& nw_) {
+        if (nw_.P == 0) return 0;
+        CS_TRY(cudaMemsetAsync(nw_.life.p, 0, sizeof(int) * nw_.P, s));
+        if (old.P == 0) return 0;
+        unsigned long long cap = 1;
+        while (cap < 2ull * (unsigned long long)old.P) cap <<= 1;
+        CS_RET(hkeys.ensure(cap));
+        CS_RET(hvals.ensure(cap));
+        k_fill_u64<<<grid(cap), 256, 0, s>>>(hkeys.p, cap, CS_EMPTY_KEY);
+        k_hash_insert<<<grid(old.P), 256, 0, s>>>(old.keys.p, old.life.p, old.P, hkeys.p, hvals.p, cap - 1);
+        k_hash_lookup<<<grid(nw_.P), 256, 0, s>>>(nw_.keys.p, nw_.P, hkeys.p, hvals.p, cap - 1, nw_.life.p);
+        launches += 3;
+        CS_CHECK_LAUNCH();
+        return 0;
+    }
+
+    // collision stamps from engaged pairs at world positions xw (stepper.py:238-285);
+    // A = number of engaged pairs (known on host).  Fills seg_beg/seg_end, rows_act.
+    int stamps(PairBuf& pr, long long A, const double* xw) {
+        stamps_valid = false;
+        n_stamp_rows = 0;
+        CS_TRY(cudaMemsetAsync(seg_beg.p, 0, sizeof(int) * nf, s));
+        CS_TRY(cudaMemsetAsync(seg_end.p, 0, sizeof(int) * nf, s));
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_ROWS, 0, sizeof(int), s));
+        if (A <= 0 || pr.P == 0) return 0;
+        CS_RET(sel.ensure(A));
+        const long long m = 4 * A;
+        CS_RET(skey.ensure(m));
+        CS_RET(ssrc.ensure(m));
+        CS_RET(skey_s.ensure(m));
+        CS_RET(ssrc_s.ensure(m));
+        CS_RET(sw.ensure(m));
+        CS_RET(stt.ensure(3 * m));
+        CS_RET(rowflag.ensure(m));
+        CS_RET(rows_act.ensure(m));
+        // compact engaged pair ids in pair order
+        size_t bytes = 0;
+        cub::CountingInputIterator<int> it(0);
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, pr.engaged.p, sel.p, d_iscal.p + I_BAD, (int)pr.P, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, pr.engaged.p, sel.p, d_iscal.p + I_BAD, (int)pr.P, s));
+        k_collision_terms<<<grid(A), 256, 0, s>>>(sel.p, A, pr.kind.p, pr.idx.p, xw, pr.bary.p, pr.normal.p,
+                                                  pr.weight.p, cfg.d_hat, n, free_index.p, 0, skey.p, sw.p, stt.p);
+        k_iota<<<grid(m), 256, 0, s>>>(ssrc.p, m);
+        launches += 2;
+        // stable sort of the 4A entries by free row keeps np.add.at's per-vertex order
+        bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey.p, skey_s.p, ssrc.p, ssrc_s.p, (int)m, 0, 31, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, skey.p, skey_s.p, ssrc.p, ssrc_s.p, (int)m, 0, 31, s));
+        CS_TRY(cudaMemsetAsync(rowflag.p, 0, sizeof(int) * m, s));
+        k_mark_segments<<<grid(m), 256, 0, s>>>(skey_s.p, (int)m, seg_beg.p, seg_end.p, rowflag.p);
+        ++launches;
+        bytes = 0;
+        cub::DeviceSelect::Flagged(nullptr, bytes, skey_s.p, rowflag.p, rows_act.p, d_iscal.p + I_ROWS, (int)m, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, skey_s.p, rowflag.p, rows_act.p, d_iscal.p + I_ROWS,
+                                          (int)m, s));
+        CS_CHECK_LAUNCH();
+        stamps_valid = true;
+        n_stamp_rows = (int)std::min<long long>(m, nf);  // upper bound; exact count read on device
+        return 0;
+    }
+
+    // one local-global cycle (stepper.py:402-424) on the candidate cloth rows xc_w[:n]
+    int inner_solve(long long A) {
+        stage(T_LOCAL);
+        CS_RET(stamps(*cur, A, xc_w.p));
+        CS_RET(assemble_rhs(z.p, xc_w.p, stamps_valid));
+        k_gather_rows<<<grid(nf), 256, 0, s>>>(xc_w.p, free_ids.p, nf, xf0.p);
+        CS_TRY(cudaMemcpyAsync(xf.p, xf0.p, sizeof(double) * 3 * nf, cudaMemcpyDeviceToDevice, s));
+        ++launches;
+        stage(T_GLOBAL);
+        CS_RET(reduced(b.p, xf.p, delta.p, true, stamps_valid ? n_stamp_rows : 0));
+        stage(T_SMOOTH);
+        CS_RET(smooth(b.p, xf.p, cfg.smoothing_iterations, cfg.omega, delta.p));
+        return 0;
+    }
+
+    int lerp_world(const double* a, const double* bb, const double* tptr, double* out) {
+        k_lerp<<<grid(3LL * nw), 256, 0, s>>>(a, bb, tptr, 3LL * nw, out);
+        ++launches;
+        CS_CHECK_LAUNCH();
+        return 0;
+    }
+
+    int set_clamp_value(double tval) {
+        h_scal[S_CLAMP] = tval;
+        CS_TRY(cudaMemcpyAsync(d_scal.p + S_CLAMP, &h_scal[S_CLAMP], sizeof(double), cudaMemcpyHostToDevice, s));
+        return 0;
+    }
+
+    // ------------------------------------------------------------ step
+    int step(const double* pin_next_h, const double* obs_next_h, cs_step_report* rep);
+    int residual_forward(const double* x_final_w, cs_step_report* rep);
+    int create(const cs_scene_desc* d, const cs_step_config* c);
+    void set_pattern();
+    void release();
+};
+
+void cs_scene::set_pattern() {
+    static const double tri1[1][2] = {{1.0 / 3.0, 1.0 / 3.0}};
+    static const double tri3[3][2] = {{1.0 / 6.0, 1.0 / 6.0}, {2.0 / 3.0, 1.0 / 6.0}, {1.0 / 6.0, 2.0 / 3.0}};
+    static const double tri6[6][2] = {{1.0 / 6.0, 1.0 / 6.0}, {2.0 / 3.0, 1.0 / 6.0}, {1.0 / 6.0, 2.0 / 3.0},
+                                      {0.5, 0.25}, {0.25, 0.5}, {1.0 / 3.0, 1.0 / 3.0}};
+    static const double box1[1][2] = {{0.5, 0.5}};
+    static const double box3[3][2] = {{0.25, 0.25}, {0.5, 0.5}, {0.75, 0.75}};
+    static const double box6[6][2] = {{0.25, 0.25}, {0.5, 0.5}, {0.75, 0.75}, {0.25, 0.75}, {0.75, 0.25}, {0.5, 0.25}};
+    const int cnt = cfg.samples == 1 ? 1 : (cfg.samples == 6 ? 6 : 3);
+    const double(*tp)[2] = cnt == 1 ? tri1 : (cnt == 6 ? tri6 : tri3);
+    const double(*bp)[2] = cnt == 1 ? box1 : (cnt == 6 ? box6 : box3);
+    pat.width = cnt;
+    for (int k = 0; k < cnt; ++k) {
+        pat.vt[k][0] = tp[k][0];
+        pat.vt[k][1] = tp[k][1];
+        pat.ee[k][0] = bp[k][0];
+        pat.ee[k][1] = bp[k][1];
+    }
+}
+
+int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
+    cfg = *c;
+    n = d->n_cloth;
+    nf = d->n_free;
+    npin = d->n_pinned;
+    nobs = d->n_obstacle;
+    nw = d->n_world;
+    ne = d->n_edges;
+    ns = d->n_stencils;
+    ntw = d->n_world_tris;
+    new_ = d->n_world_edges;
+    rb = d->r_bar;
+    r = d->r;
+    if (n <= 0 || nf <= 0 || nw != n + nobs || rb <= 0 || r <= 0 || r > rb || rb > 128 || r > 32 || ntw <= 0 ||
+        new_ <= 0)
+        return CS_BAD_ARGUMENT;
+    set_pattern();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+    CS_RET(free_ids.upload(d->free_ids, nf));
+    CS_RET(free_index.upload(d->free_index, n));
+    CS_RET(pin_ids.upload(d->pin_ids, npin));
+    CS_RET(mass.upload(d->mass, n));
+    CS_RET(fext.upload(d->fext, 3LL * n));
+    CS_RET(mh2.upload(d->mass_over_h2, nf));
+    {
+        std::vector<int> a(ne), bb(ne), slot(n, -1);
+        for (int i = 0; i < ne; ++i) {
+            a[i] = d->edge_v[2 * i];
+            bb[i] = d->edge_v[2 * i + 1];
+        }
+        for (int i = 0; i < npin; ++i) slot[d->pin_ids[i]] = i;
+        CS_RET(e0.upload(a.data(), ne));
+        CS_RET(e1.upload(bb.data(), ne));
+        CS_RET(pin_slot.upload(slot.data(), n));
+    }
+    CS_RET(erest.upload(d->edge_rest, ne));
+    CS_RET(ew.upload(d->edge_w, ne));
+    CS_RET(rinc_ptr.upload(d->rhs_inc_ptr, n + 1));
+    CS_RET(rinc.upload(d->rhs_inc, d->rhs_inc_ptr[n]));
+    CS_RET(ginc_ptr.upload(d->grad_inc_ptr, n + 1));
+    CS_RET(ginc.upload(d->grad_inc, d->grad_inc_ptr[n]));
+    CS_RET(st.upload(d->stencils, 4LL * ns));
+    CS_RET(bk.upload(d->bend_k, 4LL * ns));
+    CS_RET(bw.upload(d->bend_w, ns));
+    CS_RET(binc_ptr.upload(d->bend_inc_ptr, n + 1));
+    CS_RET(binc.upload(d->bend_inc, d->bend_inc_ptr[n]));
+    nslices = d->sell_nslices;
+    CS_RET(sell_ptr.upload(d->sell_slice_ptr, nslices + 1));
+    CS_RET(sell_col.upload(d->sell_col, d->sell_slice_ptr[nslices]));
+    CS_RET(sell_val.upload(d->sell_val, d->sell_slice_ptr[nslices]));
+    CS_RET(diag.upload(d->diag, nf));
+    has_fp = npin > 0 && d->hfp_ptr != nullptr && d->hfp_ptr[nf] > 0;
+    CS_RET(hfp_ptr.upload(d->hfp_ptr, nf + 1));
+    CS_RET(hfp_col.upload(d->hfp_col, std::max(d->hfp_ptr[nf], 1)));
+    CS_RET(hfp_val.upload(d->hfp_val, std::max(d->hfp_ptr[nf], 1)));
+    CS_RET(U.upload(d->U, (size_t)nf * rb));
+    {
+        std::vector<double> vv((size_t)nf * r);
+        for (long long i = 0; i < nf; ++i)
+            for (int j = 0; j < r; ++j) vv[i * r + j] = d->U[i * rb + j];
+        CS_RET(V.upload(vv.data(), vv.size()));
+    }
+    CS_RET(lam.upload(d->eigenvalues, rb));
+    CS_RET(wtris.upload(d->world_tris, 3LL * ntw));
+    CS_RET(wedges.upload(d->world_edges, 2LL * new_));
+    CS_RET(tri_static.upload(d->tri_static, ntw));
+    CS_RET(vert_static.upload(d->vert_static, nw));
+    CS_RET(vert_used.upload(d->vert_used, nw));
+    CS_RET(edge_static.upload(d->edge_static, new_));
+    CS_RET(edge_tris.upload(d->edge_tris, 2LL * new_));
+    CS_RET(edge_slot.upload(d->edge_slot, 2LL * new_));
+    CS_RET(patch.upload(d->patch, ntw));
+    CS_RET(pslot.upload(d->patch_slot, ntw));
+    CS_RET(ttree.create(ntw, d->tri_left, d->tri_right, d->tri_parent, d->tri_leaf_parent, d->tri_prim));
+    CS_RET(etree.create(new_, d->edge_left, d->edge_right, d->edge_parent, d->edge_leaf_parent, d->edge_prim));
+    // state
+    CS_RET(x.upload(d->x0, 3LL * n));
+    CS_RET(xprev.upload(d->x0, 3LL * n));
+    CS_RET(v.ensure(3LL * n));
+    CS_RET(df.ensure(3LL * n));
+    CS_TRY(cudaMemset(v.p, 0, sizeof(double) * 3 * n));
+    CS_TRY(cudaMemset(df.p, 0, sizeof(double) * 3 * n));
+    CS_RET(obs.upload(d->obstacle_x0, 3LL * std::max(nobs, 0)));
+    CS_RET(obs.ensure(std::max(3LL * nobs, 1LL)));
+    // work
+    for (DBuf<double>* w : {&xs_w, &xc_w, &anchor_w, &tmp_w}) CS_RET(w->ensure(3LL * nw));
+    for (DBuf<double>* w : {&z, &prev_outer, &grad}) CS_RET(w->ensure(3LL * n));
+    for (DBuf<double>* w : {&xf, &xf0, &b, &t, &fr}) CS_RET(w->ensure(3LL * nf));
+    CS_RET(delta.ensure(nf));
+    CS_RET(pins_next_d.ensure(std::max(3 * npin, 1)));
+    CS_RET(obs_next_d.ensure(std::max(3 * nobs, 1)));
+    CS_RET(vlo.ensure(3LL * nw));
+    CS_RET(vhi.ensure(3LL * nw));
+    CS_RET(counts.ensure(nw + 1));
+    CS_RET(offsets.ensure(nw + 1));
+    CS_RET(counts2.ensure(new_ + 1));
+    CS_RET(offsets2.ensure(new_ + 1));
+    CS_RET(seg_beg.ensure(nf));
+    CS_RET(seg_end.ensure(nf));
+    CS_RET(rhs_red.ensure(3 * 128));
+    CS_RET(gram_red.ensure(32 * 32));
+    CS_RET(q.ensure(3 * 128));
+    CS_RET(Xred.ensure(32 * 32));
+    CS_RET(beta_red.ensure(1));
+    CS_RET(fallback.ensure(1));
+    CS_RET(d_scal.ensure(S_COUNT));
+    CS_RET(d_iscal.ensure(I_COUNT));
+    CS_TRY(cudaMemset(d_scal.p, 0, sizeof(double) * S_COUNT));
+    CS_TRY(cudaMemset(d_iscal.p, 0, sizeof(int) * I_COUNT));
+    CS_TRY(cudaMallocHost(&h_scal, sizeof(double) * S_COUNT));
+    CS_TRY(cudaMallocHost(&h_iscal, sizeof(int) * I_COUNT));
+    CS_RET(pa.reserve(1024));
+    CS_RET(pb.reserve(1024));
+    CS_TRY(cudaDeviceSynchronize());
+    return 0;
+}
+
+void cs_scene::release() {
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    ev_pool.clear();
+    if (h_scal) cudaFreeHost(h_scal);
+    if (h_iscal) cudaFreeHost(h_iscal);
+    h_scal = nullptr;
+    h_iscal = nullptr;
+    // DBuf members release through their owners
+    DBuf<int>* ints[] = {&free_ids, &free_index, &pin_ids, &pin_slot, &e0, &e1, &rinc_ptr, &rinc, &ginc_ptr, &ginc,
+                         &st, &binc_ptr, &binc, &sell_ptr, &sell_col, &hfp_ptr, &hfp_col, &wtris, &wedges,
+                         &edge_tris, &edge_slot, &patch, &pslot, &counts, &offsets, &sel, &skey, &ssrc, &skey_s,
+                         &ssrc_s, &seg_beg, &seg_end, &rowflag, &rows_act, &hvals, &fallback, &d_iscal, &counts2, &offsets2};
+    for (auto* p : ints) p->release();
+    DBuf<double>* dbl[] = {&mass, &fext, &mh2, &erest, &ew, &bk, &bw, &sell_val, &diag, &hfp_val, &U, &V, &lam,
+                           &x, &v, &xprev, &df, &obs, &z, &xs_w, &xc_w, &anchor_w, &tmp_w, &xf, &xf0, &b, &t,
+                           &delta, &prev_outer, &grad, &fr, &pins_next_d, &obs_next_d, &vlo, &vhi, &sw, &stt,
+                           &part, &part2, &rhs_red, &gram_red, &q, &Xred, &beta_red, &d_scal, &norms};
+    for (auto* p : dbl) p->release();
+    tri_static.release();
+    vert_static.release();
+    vert_used.release();
+    edge_static.release();
+    hkeys.release();
+    cub_tmp.release();
+    pa.release();
+    pb.release();
+}
+
+int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_report* rep) {
+    launches = 0;
+    ev_used = 0;
+    spans.clear();
+    active_stage = -1;
+    const double h = cfg.h;
+    // prescribed geometry at t + h (stepper.py:461-463): host callbacks evaluated by the caller
+    if (npin) {
+        if (pin_next_h)
+            CS_TRY(cudaMemcpyAsync(pins_next_d.p, pin_next_h, sizeof(double) * 3 * npin, cudaMemcpyHostToDevice, s));
+        else {
+            k_gather_rows<<<grid(npin), 256, 0, s>>>(x.p, pin_ids.p, npin, pins_next_d.p);
+            ++launches;
+        }
+    }
+    const double* obs_next = obs.p;
+    if (nobs && obs_next_h) {
+        CS_TRY(cudaMemcpyAsync(obs_next_d.p, obs_next_h, sizeof(double) * 3 * nobs, cudaMemcpyHostToDevice, s));
+        obs_next = obs_next_d.p;
+    }
+    stage(T_WARM);
+    // z = inertia target (mesh.py:174-196)
+    CS_TRY(cudaMemsetAsync(d_iscal.p + I_BAD, 0, sizeof(int), s));
+    k_inertia_target<<<grid(n), 256, 0, s>>>(x.p, v.p, fext.p, df.p, mass.p, n, h, pin_slot.p, pins_next_d.p, z.p,
+                                            d_iscal.p + I_BAD);
+    ++launches;
+    CS_CHECK_LAUNCH();
+    // ---- warm start (stepper.py:384-400): x = z (pins already at pin_next)
+    double* xcl = xc_w.p;  // cloth rows of the candidate world array
+    CS_TRY(cudaMemcpyAsync(xcl, z.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    CS_RET(sync_scalars());
+    if (h_iscal[I_BAD]) return CS_NONFINITE;
+    int ws_iters = 0;
+    for (int it = 0; it < cfg.warm_start_cap; ++it) {
+        CS_RET(assemble_rhs(z.p, xcl, false));
+        k_gather_rows<<<grid(nf), 256, 0, s>>>(xcl, free_ids.p, nf, xf0.p);
+        CS_TRY(cudaMemcpyAsync(xf.p, xf0.p, sizeof(double) * 3 * nf, cudaMemcpyDeviceToDevice, s));
+        ++launches;
+        CS_RET(warm_correction(b.p, xf.p));
+        CS_RET(sqnorm(xf.p, xf0.p, nf, nullptr, S_SQ));
+        k_scatter_rows<<<grid(nf), 256, 0, s>>>(xf.p, free_ids.p, nf, xcl);
+        ++launches;
+        CS_RET(sync_scalars());
+        ++ws_iters;
+        const double dx = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
+        if (dx < cfg.eps_initial) break;
+    }
+    if (rep) rep->warm_start_iterations = ws_iters;
+
+    // ---- world arrays: start = [x; obstacle_x], candidate = [x_cand; obs_next]
+    CS_TRY(cudaMemcpyAsync(xs_w.p, x.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    if (nobs) {
+        CS_TRY(cudaMemcpyAsync(xs_w.p + 3LL * n, obs.p, sizeof(double) * 3 * nobs, cudaMemcpyDeviceToDevice, s));
+        CS_TRY(cudaMemcpyAsync(xc_w.p + 3LL * n, obs_next, sizeof(double) * 3 * nobs, cudaMemcpyDeviceToDevice, s));
+    }
+    double tc = 1.0;
+    CS_RET(ccd_site(xs_w.p, xc_w.p, *cur, rep, tc));
+    // x_acc = clamp; anchor = x_acc (stepper.py:475-480)
+    CS_RET(set_clamp_value(tc));
+    CS_RET(lerp_world(xs_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));
+    CS_TRY(cudaMemcpyAsync(xc_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
+    CS_TRY(cudaMemcpyAsync(anchor_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
+    stage(T_FULL);
+    CS_RET(witness(*cur, anchor_w.p));
+    if (cur->P) CS_TRY(cudaMemsetAsync(cur->life.p, 0, sizeof(int) * cur->P, s));
+    CS_RET(engage(*cur));
+    CS_TRY(cudaMemcpyAsync(prev_outer.p, xcl, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    CS_RET(sync_scalars());
+    long long A = h_iscal[I_ENG];
+
+    double dx_last = INFINITY;
+    bool cap_hit = false;
+    double toi_exit = 1.0;
+    int lg = 0, outer_loops = 0, partial_calls = 0;
+    int n_deltas = 0;
+    for (int outer = 0; outer < cfg.outer_cap; ++outer) {
+        for (int inner = 0; inner < cfg.inner_cap; ++inner) {
+            CS_RET(inner_solve(A));
+            // dx = rms(x_new[free] - x_cand[free]); write back (stepper.py:506-509)
+            CS_RET(sqnorm(xf.p, xf0.p, nf, nullptr, S_SQ));
+            k_scatter_rows<<<grid(nf), 256, 0, s>>>(xf.p, free_ids.p, nf, xcl);
+            ++launches;
+            ++lg;
+            // partial CCD + NDB life-span update (stepper.py:511-523)
+            stage(T_PARTIAL);
+            CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
+            if (cur->P) {
+                k_partial_ndb<<<grid(cur->P, 128), 128, 0, s>>>(cur->kind.p, cur->idx.p, anchor_w.p, xc_w.p, cur->P,
+                                                                pat, cur->bary.p, cur->normal.p, cfg.d_hat, cfg.ndb_k,
+                                                                cfg.ndb_base, cur->life.p, cur->weight.p,
+                                                                cur->engaged.p, 0, nullptr, d_iscal.p + I_ENG);
+                ++launches;
+                CS_CHECK_LAUNCH();
+            }
+            ++partial_calls;
+            CS_RET(sync_scalars());
+            dx_last = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
+            A = h_iscal[I_ENG];
+            if (cfg.iteration_cap && lg >= cfg.iteration_cap) {
+                cap_hit = true;
+                break;
+            }
+            if (dx_last <= cfg.eps_inner) break;
+        }
+        ++outer_loops;
+        // fresh pair set + line-search filter at the end of every outer loop (stepper.py:547-570)
+        double tout = 1.0;
+        CS_RET(ccd_site(anchor_w.p, xc_w.p, *nxt, rep, tout));
+        if (tout < 1.0) {
+            CS_RET(set_clamp_value(tout));
+            CS_RET(lerp_world(anchor_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));
+            CS_TRY(cudaMemcpyAsync(xc_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
+            toi_exit = std::min(toi_exit, tout);
+        }
+        CS_TRY(cudaMemcpyAsync(anchor_w.p, xc_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
+        stage(T_FULL);
+        CS_RET(witness(*nxt, anchor_w.p));
+        CS_RET(carry(*cur, *nxt));
+        CS_RET(engage(*nxt));
+        std::swap(cur, nxt);
+        // outer progress (stepper.py:574-578)
+        CS_RET(sqnorm(xcl, prev_outer.p, nf, free_ids.p, S_SQ));
+        // prev_outer holds cloth rows; compare over free rows only
+        CS_TRY(cudaMemcpyAsync(prev_outer.p, xcl, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+        CS_RET(sync_scalars());
+        A = h_iscal[I_ENG];
+        const double d_out = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
+        if (rep && n_deltas < 64) rep->outer_deltas[n_deltas++] = d_out;
+        if (cap_hit || d_out <= cfg.eps_outer) break;
+    }
+    // ---- exit line search (stepper.py:580-592)
+    const long long active_pairs = cur->P ? A : 0;
+    double tfin = 1.0;
+    CS_RET(ccd_site(anchor_w.p, xc_w.p, *nxt, rep, tfin));
+    CS_RET(set_clamp_value(tfin));
+    CS_RET(lerp_world(anchor_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));  // tmp_w = x_final_w
+    toi_exit = std::min(toi_exit, tfin);
+    stage(-1);
+    // ---- new state (stepper.py:594-602)
+    CS_TRY(cudaMemcpyAsync(xprev.p, x.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    k_velocity_update<<<grid(3LL * n), 256, 0, s>>>(tmp_w.p, x.p, v.p, 3LL * n, h);
+    ++launches;
+    CS_TRY(cudaMemcpyAsync(x.p, tmp_w.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    CS_TRY(cudaMemsetAsync(df.p, 0, sizeof(double) * 3 * n, s));
+    if (nobs) CS_TRY(cudaMemcpyAsync(obs.p, tmp_w.p + 3LL * n, sizeof(double) * 3 * nobs, cudaMemcpyDeviceToDevice, s));
+    CS_CHECK_LAUNCH();
+    // ---- residual forwarding (stepper.py:604-610)
+    const bool needs_rf = toi_exit < cfg.eps_toi || (cap_hit && dx_last > cfg.eps_outer);
+    if (needs_rf) {
+        stage(T_RF);
+        CS_RET(residual_forward(tmp_w.p, rep));
+        stage(-1);
+    }
+    ++step_index;
+    if (rep) {
+        rep->lg_iterations = lg;
+        rep->outer_loops = outer_loops;
+        rep->partial_ccd_calls = partial_calls;
+        rep->toi_exit = toi_exit;
+        rep->cap_hit = cap_hit ? 1 : 0;
+        rep->rf_triggered = needs_rf ? 1 : 0;
+        rep->active_pairs = (int)active_pairs;
+        rep->n_outer_deltas = n_deltas;
+        rep->gpu_launches = launches;
+        CS_TRY(cudaStreamSynchronize(s));
+        double acc[kStages] = {0};
+        for (auto& sp : spans) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, sp.second.first, sp.second.second);
+            acc[sp.first] += ms;
+        }
+        rep->t_warm_start = acc[T_WARM];
+        rep->t_local = acc[T_LOCAL];
+        rep->t_global = acc[T_GLOBAL];
+        rep->t_smoothing = acc[T_SMOOTH];
+        rep->t_broad = acc[T_BROAD];
+        rep->t_narrow_partial = acc[T_PARTIAL];
+        rep->t_narrow_full = acc[T_FULL];
+        rep->t_rf = acc[T_RF];
+    }
+    return 0;
+}
+
+int cs_scene::residual_forward(const double* xfw, cs_step_report* rep) {
+    // exit pairs live in *nxt: witness at x_final_w, frozen weights (stepper.py:626-642)
+    PairBuf& ex = *nxt;
+    long long A = 0;
+    CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
+    if (ex.P) {
+        CS_RET(witness(ex, xfw));
+        k_rf_weights<<<grid(ex.P), 256, 0, s>>>(ex.dist.p, ex.P, cfg.d_hat, cfg.ndb_k, ex.engaged.p, ex.weight.p);
+        k_count_true<<<grid(ex.P), 256, 0, s>>>(ex.engaged.p, ex.P, d_iscal.p + I_ENG);
+        launches += 2;
+        CS_RET(sync_scalars());
+        A = h_iscal[I_ENG];
+    }
+    CS_RET(stamps(ex, A, xfw));
+    // f_r = -grad E at x_final (quad collision form), delta from stamps
+    k_energy_grad<<<grid(n), 256, 0, s>>>(n, x.p, z.p, mass.p, cfg.h, edges(), ginc_ptr.p, ginc.p,
+                                          BendSet{st.p, bk.p, bw.p}, binc_ptr.p, binc.p, free_index.p,
+                                          stamps_valid ? seg_beg.p : nullptr, seg_end.p, ssrc_s.p, sw.p, stt.p,
+                                          grad.p);
+    k_neg_gather<<<grid(nf), 256, 0, s>>>(grad.p, free_ids.p, nf, fr.p);
+    k_stamp_delta<<<grid(nf), 256, 0, s>>>(nf, stamps_valid ? seg_beg.p : nullptr, seg_end.p, ssrc_s.p, sw.p,
+                                           delta.p);
+    launches += 3;
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaMemsetAsync(xf.p, 0, sizeof(double) * 3 * nf, s));
+    CS_RET(sqnorm(fr.p, nullptr, nf, nullptr, S_NORM_F));
+    for (int it = 0; it < cfg.rf_iterations; ++it) {
+        CS_RET(reduced(fr.p, xf.p, delta.p, it == 0, stamps_valid ? n_stamp_rows : 0));
+        CS_RET(smooth(fr.p, xf.p, cfg.smoothing_iterations, cfg.omega, delta.p));
+        // resid = f_r - H dx - delta dx ; ||resid|| <= tol * max(||f_r||, 1e-30)
+        k_residual<<<grid(nf), 256, 0, s>>>(sell(), fr.p, xf.p, delta.p, t.p);
+        ++launches;
+        CS_RET(sqnorm(t.p, nullptr, nf, nullptr, S_RES));
+        CS_RET(sync_scalars());
+        if (h_scal[S_RES] <= cfg.rf_tolerance * std::max(h_scal[S_NORM_F], 1e-30)) break;
+    }
+    CS_TRY(cudaMemsetAsync(df.p, 0, sizeof(double) * 3 * n, s));
+    k_forward_force<<<grid(nf), 256, 0, s>>>(xf.p, free_ids.p, nf, mass.p, cfg.h, df.p);
+    ++launches;
+    CS_RET(sqnorm(df.p, nullptr, n, nullptr, S_DFNORM));
+    CS_RET(sync_scalars());
+    const double nrm = h_scal[S_DFNORM];
+    if (nrm > cfg.delta_f_cap) {
+        h_scal[S_DFSCALE] = cfg.delta_f_cap / nrm;
+        CS_TRY(cudaMemcpyAsync(d_scal.p + S_DFSCALE, &h_scal[S_DFSCALE], sizeof(double), cudaMemcpyHostToDevice, s));
+        k_scale<<<grid(3LL * n), 256, 0, s>>>(df.p, 3LL * n, d_scal.p + S_DFSCALE);
+        ++launches;
+    }
+    CS_CHECK_LAUNCH();
+    if (rep) {
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_FALLBACK], fallback.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        rep->reduced_fallbacks += h_iscal[I_FALLBACK];
+    }
+    return 0;
+}
+
+// ============================================================ C ABI
+extern "C" {
+
+const char* cs_version(void) { return "clothsim_b200 0.1 sm_100a fp64"; }
+
+cs_scene* cs_scene_create(const cs_scene_desc* desc, const cs_step_config* cfg, int* status) {
+    cs_scene* sc = new cs_scene();
+    int rc = sc->create(desc, cfg);
+    if (status) *status = rc;
+    if (rc != 0) {
+        sc->release();
+        delete sc;
+        return nullptr;
+    }
+    return sc;
+}
+
+void cs_scene_destroy(cs_scene* scene) {
+    if (!scene) return;
+    cudaDeviceSynchronize();
+    scene->release();
+    delete scene;
+}
+
+int cs_scene_set_config(cs_scene* scene, const cs_step_config* cfg) {
+    if (!scene || !cfg) return CS_BAD_ARGUMENT;
+    scene->cfg = *cfg;
+    scene->set_pattern();
+    return 0;
+}
+
+int cs_step(cs_scene* scene, const double* pin_next, const double* obstacle_next, cs_step_report* report,
+            void* stream) {
+    if (!scene) return CS_BAD_ARGUMENT;
+    if (report) std::memset(report, 0, sizeof(*report));
+    scene->s = (cudaStream_t)stream;
+    int rc = scene->step(pin_next, obstacle_next, report);
+    scene->stage(-1);
+    return rc;
+}
+
+int cs_get_state(cs_scene* sc, double* x, double* x_dot, double* x_prev, double* delta_f, double* obstacle_x,
+                 int* step_index, void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nb = sizeof(double) * 3 * sc->n;
+    if (x) CS_TRY(cudaMemcpyAsync(x, sc->x.p, nb, cudaMemcpyDeviceToHost, s));
+    if (x_dot) CS_TRY(cudaMemcpyAsync(x_dot, sc->v.p, nb, cudaMemcpyDeviceToHost, s));
+    if (x_prev) CS_TRY(cudaMemcpyAsync(x_prev, sc->xprev.p, nb, cudaMemcpyDeviceToHost, s));
+    if (delta_f) CS_TRY(cudaMemcpyAsync(delta_f, sc->df.p, nb, cudaMemcpyDeviceToHost, s));
+    if (obstacle_x && sc->nobs)
+        CS_TRY(cudaMemcpyAsync(obstacle_x, sc->obs.p, sizeof(double) * 3 * sc->nobs, cudaMemcpyDeviceToHost, s));
+    if (step_index) *step_index = sc->step_index;
+    CS_TRY(cudaStreamSynchronize(s));
+    return 0;
+}
+
+int cs_set_state(cs_scene* sc, const double* x, const double* x_dot, const double* x_prev, const double* delta_f,
+                 const double* obstacle_x, int step_index, void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nb = sizeof(double) * 3 * sc->n;
+    if (x) CS_TRY(cudaMemcpyAsync(sc->x.p, x, nb, cudaMemcpyHostToDevice, s));
+    if (x_dot) CS_TRY(cudaMemcpyAsync(sc->v.p, x_dot, nb, cudaMemcpyHostToDevice, s));
+    if (x_prev) CS_TRY(cudaMemcpyAsync(sc->xprev.p, x_prev, nb, cudaMemcpyHostToDevice, s));
+    if (delta_f) CS_TRY(cudaMemcpyAsync(sc->df.p, delta_f, nb, cudaMemcpyHostToDevice, s));
+    if (obstacle_x && sc->nobs)
+        CS_TRY(cudaMemcpyAsync(sc->obs.p, obstacle_x, sizeof(double) * 3 * sc->nobs, cudaMemcpyHostToDevice, s));
+    if (step_index >= 0) sc->step_index = step_index;
+    CS_TRY(cudaStreamSynchronize(s));
+    return 0;
+}
+
+int cs_state_device(cs_scene* sc, double** x, double** x_dot, double** delta_f, double** obstacle_x) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    if (x) *x = sc->x.p;
+    if (x_dot) *x_dot = sc->v.p;
+    if (delta_f) *delta_f = sc->df.p;
+    if (obstacle_x) *obstacle_x = sc->obs.p;
+    return 0;
+}
+
+int cs_full_ccd(const int8_t* kind, const int* idx4, const double* x_start, const double* x_end, long long P,
+                double tol, double* toi, void* stream) {
+    if (P < 0) return CS_BAD_ARGUMENT;
+    if (P == 0) return 0;
+    k_full_ccd<<<(int)((P + 127) / 128), 128, 0, (cudaStream_t)stream>>>(kind, (const int4*)idx4, x_start, x_end, P,
+                                                                         P == 1 ? 1 : 0, tol, toi);
+    CS_CHECK_LAUNCH();
+    return 0;
+}
+
+int cs_distance_toi(const int8_t* kind, const int* idx4, const double* x_start, const double* x_end, long long P,
+                    double floor_frac, int max_iterations, double* toi, void* stream) {
+    if (P < 0) return CS_BAD_ARGUMENT;
+    if (P == 0) return 0;
+    k_distance_toi<<<(int)((P + 127) / 128), 128, 0, (cudaStream_t)stream>>>(kind, (const int4*)idx4, x_start, x_end,
+                                                                             P, floor_frac, max_iterations, toi);
+    CS_CHECK_LAUNCH();
+    return 0;
+}
+
+int cs_partial_ccd(const int8_t* kind, const int* idx4, const double* x_start, const double* x_end, long long P,
+                   int samples, uint8_t* active, void* stream) {
+    if (P < 0 || (samples != 1 && samples != 3 && samples != 6)) return CS_BAD_ARGUMENT;
+    if (P == 0) return 0;
+    cs_scene tmp;
+    tmp.cfg.samples = samples;
+    tmp.set_pattern();
+    // classification only: feed an impossible gap so the NDB half leaves `active` untouched
+    DBuf<double> bary, normal, weight;
+    DBuf<int> life;
+    DBuf<uint8_t> eng;
+    CS_RET(bary.ensure(2 * P));
+    CS_RET(normal.ensure(3 * P));
+    CS_RET(weight.ensure(P));
+    CS_RET(life.ensure(P));
+    CS_RET(eng.ensure(P));
+    cudaStream_t s = (cudaStream_t)stream;
+    CS_TRY(cudaMemsetAsync(bary.p, 0, sizeof(double) * 2 * P, s));
+    CS_TRY(cudaMemsetAsync(normal.p, 0, sizeof(double) * 3 * P, s));
+    CS_TRY(cudaMemsetAsync(life.p, 0, sizeof(int) * P, s));
+    k_partial_ndb<<<(int)((P + 127) / 128), 128, 0, s>>>(kind, (const int4*)idx4, x_start, x_end, P, tmp.pat, bary.p,
+                                                         normal.p, -1.0, 1.0, 2.0, life.p, weight.p, eng.p, 1, active,
+                                                         nullptr);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaStreamSynchronize(s));
+    bary.release();
+    normal.release();
+    weight.release();
+    life.release();
+    eng.release();
+    return 0;
+}
+
+int cs_pair_witness(const int8_t* kind, const int* idx4, const double* x, long long P, double* p1, double* p2,
+                    double* bary, double* dist, double* normal, void* stream) {
+    if (P < 0) return CS_BAD_ARGUMENT;
+    if (P == 0) return 0;
+    k_witness<<<(int)((P + 127) / 128), 128, 0, (cudaStream_t)stream>>>(kind, (const int4*)idx4, x, P, bary, dist,
+                                                                        normal, p1, p2);
+    CS_CHECK_LAUNCH();
+    return 0;
+}
+
+int cs_broad_phase(cs_scene* sc, const double* x_start_w, const double* x_end_w, double margin, long long* count,
+                   void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    CS_RET(sc->broad_phase(x_start_w, x_end_w, margin, *sc->cur));
+    if (count) *count = sc->cur->P;
+    CS_TRY(cudaStreamSynchronize(sc->s));
+    return 0;
+}
+
+int cs_scene_pairs(cs_scene* sc, int8_t* kind, int* idx4, void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long P = sc->cur->P;
+    if (P == 0) return 0;
+    if (kind) CS_TRY(cudaMemcpyAsync(kind, sc->cur->kind.p, P, cudaMemcpyDeviceToDevice, s));
+    if (idx4) CS_TRY(cudaMemcpyAsync(idx4, sc->cur->idx.p, sizeof(int4) * P, cudaMemcpyDeviceToDevice, s));
+    return 0;
+}
+
+int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const int* coll_ids, const double* coll_w,
+                    const double* coll_t, int n_coll, double* b, double* delta, void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    cudaStream_t s = sc->s;
+    bool with = false;
+    CS_TRY(cudaMemsetAsync(sc->seg_beg.p, 0, sizeof(int) * sc->nf, s));
+    CS_TRY(cudaMemsetAsync(sc->seg_end.p, 0, sizeof(int) * sc->nf, s));
+    if (n_coll > 0) {
+        const int m = n_coll;
+        CS_RET(sc->skey.ensure(m));
+        CS_RET(sc->ssrc.ensure(m));
+        CS_RET(sc->skey_s.ensure(m));
+        CS_RET(sc->ssrc_s.ensure(m));
+        CS_RET(sc->sw.ensure(m));
+        CS_RET(sc->stt.ensure(3LL * m));
+        CS_RET(sc->rowflag.ensure(m));
+        CS_TRY(cudaMemcpyAsync(sc->sw.p, coll_w, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+        CS_TRY(cudaMemcpyAsync(sc->stt.p, coll_t, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, s));
+        k_stamp_keys<<<sc->grid(m), 256, 0, s>>>(coll_ids, m, sc->free_index.p, sc->n, sc->skey.p);
+        k_iota<<<sc->grid(m), 256, 0, s>>>(sc->ssrc.p, m);
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, sc->skey.p, sc->skey_s.p, sc->ssrc.p, sc->ssrc_s.p, m, 0, 31, s);
+        CS_RET(sc->cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceRadixSort::SortPairs(sc->cub_tmp.p, bytes, sc->skey.p, sc->skey_s.p, sc->ssrc.p,
+                                               sc->ssrc_s.p, m, 0, 31, s));
+        CS_TRY(cudaMemsetAsync(sc->rowflag.p, 0, sizeof(int) * m, s));
+        k_mark_segments<<<sc->grid(m), 256, 0, s>>>(sc->skey_s.p, m, sc->seg_beg.p, sc->seg_end.p, sc->rowflag.p);
+        CS_CHECK_LAUNCH();
+        with = true;
+    }
+    k_assemble_rhs<<<sc->grid(sc->nf), 256, 0, s>>>(sc->nf, sc->free_ids.p, x, z, sc->mh2.p, sc->edges(),
+                                                    sc->rinc_ptr.p, sc->rinc.p, sc->has_fp ? sc->hfp_ptr.p : nullptr,
+                                                    sc->hfp_col.p, sc->hfp_val.p, x, with ? sc->seg_beg.p : nullptr,
+                                                    sc->seg_end.p, sc->ssrc_s.p, sc->sw.p, sc->stt.p, b, delta);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaStreamSynchronize(s));
+    return 0;
+}
+
+int cs_ajacobi_smooth(cs_scene* sc, const double* b, double* x, int iterations, double omega, const double* delta,
+                      void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    const double* dl = delta;
+    if (dl == nullptr) {
+        CS_TRY(cudaMemsetAsync(sc->delta.p, 0, sizeof(double) * sc->nf, sc->s));
+        dl = sc->delta.p;
+    }
+    CS_RET(sc->smooth(b, x, iterations, omega, dl));
+    return sc->check_divergence();
+}
+
+int cs_reduced_correction(cs_scene* sc, const double* b, double* x, const double* delta, int reuse, void* stream) {
+    if (!sc || !delta) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    int rows = 0;
+    if (!reuse) {
+        // active rows = flatnonzero(delta) (subspace.py:182)
+        CS_RET(sc->rows_act.ensure(sc->nf));
+        CS_RET(sc->rowflag.ensure(sc->nf));
+        k_nonzero_flags<<<sc->grid(sc->nf), 256, 0, sc->s>>>(delta, sc->nf, sc->rowflag.p);
+        size_t bytes = 0;
+        cub::CountingInputIterator<int> it(0);
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, sc->rowflag.p, sc->rows_act.p, sc->d_iscal.p + I_ROWS, sc->nf,
+                                   sc->s);
+        CS_RET(sc->cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(sc->cub_tmp.p, bytes, it, sc->rowflag.p, sc->rows_act.p,
+                                          sc->d_iscal.p + I_ROWS, sc->nf, sc->s));
+        rows = sc->nf;
+    }
+    CS_RET(sc->reduced(b, x, delta, !reuse, rows));
+    CS_TRY(cudaStreamSynchronize(sc->s));
+    return 0;
+}
+
+int cs_warmstart_correction(cs_scene* sc, const double* b, double* x, void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    CS_RET(sc->warm_correction(b, x));
+    CS_TRY(cudaStreamSynchronize(sc->s));
+    return 0;
+}
+
+int cs_energy_gradient(cs_scene* sc, const double* x, const double* z, const int* q_ids, const double* q_w,
+                       const double* q_t, int n_q, double* grad, void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    cudaStream_t s = sc->s;
+    bool with = false;
+    CS_TRY(cudaMemsetAsync(sc->seg_beg.p, 0, sizeof(int) * sc->nf, s));
+    CS_TRY(cudaMemsetAsync(sc->seg_end.p, 0, sizeof(int) * sc->nf, s));
+    if (n_q > 0) {
+        const int m = n_q;
+        CS_RET(sc->skey.ensure(m));
+        CS_RET(sc->ssrc.ensure(m));
+        CS_RET(sc->skey_s.ensure(m));
+        CS_RET(sc->ssrc_s.ensure(m));
+        CS_RET(sc->sw.ensure(m));
+        CS_RET(sc->stt.ensure(3LL * m));
+        CS_RET(sc->rowflag.ensure(m));
+        CS_TRY(cudaMemcpyAsync(sc->sw.p, q_w, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+        CS_TRY(cudaMemcpyAsync(sc->stt.p, q_t, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, s));
+        k_stamp_keys<<<sc->grid(m), 256, 0, s>>>(q_ids, m, sc->free_index.p, sc->n, sc->skey.p);
+        k_iota<<<sc->grid(m), 256, 0, s>>>(sc->ssrc.p, m);
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, sc->skey.p, sc->skey_s.p, sc->ssrc.p, sc->ssrc_s.p, m, 0, 31, s);
+        CS_RET(sc->cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceRadixSort::SortPairs(sc->cub_tmp.p, bytes, sc->skey.p, sc->skey_s.p, sc->ssrc.p,
+                                               sc->ssrc_s.p, m, 0, 31, s));
+        CS_TRY(cudaMemsetAsync(sc->rowflag.p, 0, sizeof(int) * m, s));
+        k_mark_segments<<<sc->grid(m), 256, 0, s>>>(sc->skey_s.p, m, sc->seg_beg.p, sc->seg_end.p, sc->rowflag.p);
+        with = true;
+    }
+    k_energy_grad<<<sc->grid(sc->n), 256, 0, s>>>(sc->n, x, z, sc->mass.p, sc->cfg.h, sc->edges(), sc->ginc_ptr.p,
+                                                  sc->ginc.p, BendSet{sc->st.p, sc->bk.p, sc->bw.p}, sc->binc_ptr.p,
+                                                  sc->binc.p, sc->free_index.p, with ? sc->seg_beg.p : nullptr,
+                                                  sc->seg_end.p, sc->ssrc_s.p, sc->sw.p, sc->stt.p, grad);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaStreamSynchronize(s));
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,562 @@
+// Narrow phase: per-pair fp64 kernels, bit-identical to the reference.
+//
+//   k_full_ccd       reference ccd.py:138-196   (cubic coplanarity TOI + flat fallback)
+//   k_distance_toi   reference ccd.py:221-266   (conservative-advancement line-search filter)
+//   k_witness        reference stepper.py:194-216 + geometry.py:115-148
+//   k_partial_ndb    reference partial.py:149-204 fused with the NDB life-span update
+//                    (stepper.py:517-523, _pair_gaps :218-236, pairs.py:65-70)
+//   k_engage_init    stepper.py:483-487 / 564-565 (engaged set + weights after a CCD site)
+//
+// One thread per pair; all positions are fp64 world arrays (n_w, 3).  These
+// kernels are FP64-ALU / latency bound: the pair stream is
+// ~25-64 B/pair while a full-CCD pair costs 300-2000 flops.
+#include "common.cuh"
+
+namespace cs {
+
+// inv(vander([0, 1/3, 2/3, 1], increasing)) exactly as numpy/LAPACK produce it
+// (reference ccd.py:21-22); hex literals pinned by tests/test_oracle_golden.py.
+__constant__ double kFit[4][4] = {
+    {0x1.0p+0, 0x0.0p+0, 0x0.0p+0, 0x0.0p+0},
+    {-0x1.6000000000001p+2, 0x1.2p+3, -0x1.1fffffffffffcp+2, 0x1.0p+0},
+    {0x1.2000000000001p+3, -0x1.68p+4, 0x1.1ffffffffffffp+4, -0x1.2p+2},
+    {-0x1.2000000000001p+2, 0x1.bp+3, -0x1.bp+3, 0x1.2p+2},
+};
+
+__device__ __forceinline__ double horner(const double c[4], double t) {
+    return c[0] + t * (c[1] + t * (c[2] + t * c[3]));
+}
+
+// correctly rounded x^3 (numpy `** 3` goes through libm pow, not x*x*x)
+__device__ __forceinline__ double cube_rn(double x) {
+    double h = x * x;
+    double l = fma(x, x, -h);
+    double hh = h * x;
+    double e1 = fma(h, x, -hh);
+    return hh + (e1 + l * x);
+}
+
+struct Corners {
+    d3 p[4];
+};
+
+__device__ __forceinline__ Corners gather4(const double* __restrict__ x, int4 id) {
+    Corners c;
+    c.p[0] = ld3(x, id.x);
+    c.p[1] = ld3(x, id.y);
+    c.p[2] = ld3(x, id.z);
+    c.p[3] = ld3(x, id.w);
+    return c;
+}
+
+__device__ __forceinline__ d3 lerp_node(d3 a, d3 b, double t) {
+    double s = 1.0 - t;  // (1.0 - t) * x_start + t * x_end, reference ccd.py:40
+    return (s * a) + (t * b);
+}
+
+__device__ __forceinline__ double triple(int kind, const d3 p[4]) {
+    d3 u, v, w;
+    if (kind == CS_VT) {
+        u = p[2] - p[1];
+        v = p[3] - p[1];
+        w = p[0] - p[1];
+    } else {
+        u = p[1] - p[0];
+        v = p[3] - p[2];
+        w = p[2] - p[0];
+    }
+    return dot3(cross3(u, v), w);
+}
+
+// inflated inside test at time t (reference ccd.py:111-135)
+__device__ bool confirm_hit(int kind, const Corners& a, const Corners& b, double t, double tol) {
+    d3 q[4];
+    double s = 1.0 - t;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = (s * a.p[k]) + (t * b.p[k]);
+    if (kind == CS_VT) {
+        double u, v;
+        d3 cl;
+        double d = pt_tri_closest(q[0], q[1], q[2], q[3], u, v, cl);
+        double size = norm3(q[2] - q[1]) + norm3(q[3] - q[1]);
+        bool inside = (u >= -1e-8) && (v >= -1e-8) && (u + v <= 1.0 + 1e-8);
+        return inside && (d <= tol * np_max(size, 1.0));
+    }
+    double s2, t2;
+    d3 pa, pb;
+    double d = seg_seg_closest(q[0], q[1], q[2], q[3], s2, t2, pa, pb);
+    double size = norm3(q[1] - q[0]) + norm3(q[3] - q[2]);
+    return d <= tol * np_max(size, 1.0);
+}
+
+__device__ __forceinline__ double pair_extent(const Corners& a, const Corners& b) {
+    d3 lo = a.p[0], hi = a.p[0];
+    // min/max are exact, so evaluation order is irrelevant
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const d3 q0 = a.p[k], q1 = b.p[k];
+        lo.x = np_min(lo.x, np_min(q0.x, q1.x));
+        lo.y = np_min(lo.y, np_min(q0.y, q1.y));
+        lo.z = np_min(lo.z, np_min(q0.z, q1.z));
+        hi.x = np_max(hi.x, np_max(q0.x, q1.x));
+        hi.y = np_max(hi.y, np_max(q0.y, q1.y));
+        hi.z = np_max(hi.z, np_max(q0.z, q1.z));
+    }
+    return norm3(hi - lo);
+}
+
+__global__ void k_full_ccd(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+                           const double* __restrict__ x0, const double* __restrict__ x1, int64_t P,
+                           int single, double tol, double* __restrict__ toi_out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const int kd = kind[i];
+    const int4 id = idx[i];
+    Corners a = gather4(x0, id), b = gather4(x1, id);
+
+    // coplanarity samples at t = 0, 1/3, 2/3, 1 and the monomial fit (ccd.py:36-44)
+    const double nodes[4] = {0.0, 1.0 / 3.0, 2.0 / 3.0, 1.0};
+    double f[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        d3 q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[k] = lerp_node(a.p[k], b.p[k], nodes[j]);
+        f[j] = triple(kd, q);
+    }
+    double c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (!single) {  // OpenBLAS dgemm k=4 kernel: forward FMA chain
+            double acc = f[0] * kFit[j][0];
+            acc = fma(f[1], kFit[j][1], acc);
+            acc = fma(f[2], kFit[j][2], acc);
+            c[j] = fma(f[3], kFit[j][3], acc);
+        } else {        // m == 1 takes OpenBLAS's gemv-like path
+            double even = f[0] * kFit[j][0] + f[2] * kFit[j][2];
+            double odd = f[1] * kFit[j][1] + f[3] * kFit[j][3];
+            c[j] = even + odd;
+        }
+    }
+    const double csum = ((fabs(c[0]) + fabs(c[1])) + fabs(c[2])) + fabs(c[3]);
+    const double ext = pair_extent(a, b);
+    const bool flat = csum <= 1e-12 * np_max(cube_rn(fabs(ext)), 1e-30);
+
+    const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
+    double toi = NaN;
+    if (!flat) {
+        // ---- _candidate_roots (ccd.py:53-108)
+        double qa = 3.0 * c[3], qb = 2.0 * c[2], ql = c[1];
+        bool quad = fabs(qa) > 0.0;
+        double disc = qb * qb - (4.0 * qa) * ql;
+        bool real = quad && disc >= 0.0;
+        double sq = sqrt(real ? disc : 0.0);
+        double r1 = real ? (-qb - sq) / (2.0 * qa) : NaN;
+        double r2 = real ? (-qb + sq) / (2.0 * qa) : NaN;
+        double rl = (!quad && fabs(qb) > 0.0) ? -ql / qb : NaN;
+        double br0 = quad ? np_min(r1, r2) : rl;
+        double br1 = quad ? np_max(r1, r2) : NaN;
+        if (!(br0 > 0.0 && br0 < 1.0)) br0 = NaN;
+        if (!(br1 > 0.0 && br1 < 1.0)) br1 = NaN;
+        if (br0 != br0 && br1 == br1) {  // np.sort puts nan last
+            br0 = br1;
+            br1 = NaN;
+        } else if (br0 == br0 && br1 == br1 && br1 < br0) {
+            double tmp = br0;
+            br0 = br1;
+            br1 = tmp;
+        }
+        double k1 = (br0 != br0) ? 1.0 : br0;
+        double k2 = (br1 != br1) ? k1 : np_max(br1, k1);
+        double lo[3] = {0.0, k1, k2}, hi[3] = {k1, k2, 1.0};
+        double roots[5];
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            double flo = horner(c, lo[s]), fhi = horner(c, hi[s]);
+            bool bracket = (hi[s] > lo[s]) && (flo * fhi < 0.0);
+            bool at_end = (hi[s] > lo[s]) && (fhi == 0.0);
+            double r = NaN;
+            if (bracket) {
+                double al = lo[s], ah = hi[s];
+                for (int it = 0; it < 80; ++it) {
+                    double mid = 0.5 * (al + ah);
+                    double fm = horner(c, mid);
+                    if (np_sign(fm) == np_sign(flo)) {
+                        al = mid;
+                        flo = fm;
+                    } else {
+                        ah = mid;
+                    }
+                }
+                r = 0.5 * (al + ah);
+            } else if (at_end) {
+                r = hi[s];
+            }
+            roots[s] = r;
+        }
+        const double mag = csum + 1e-300;
+        const double brk[2] = {br0, br1};
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            double tb = brk[j];
+            double fv = fabs(horner(c, tb != tb ? 0.0 : tb));
+            roots[3 + j] = (tb == tb && fv <= 1e-9 * mag) ? tb : NaN;
+        }
+#pragma unroll
+        for (int s = 0; s < 5; ++s)
+            if (!(roots[s] > 0.0 && roots[s] <= 1.0)) roots[s] = NaN;
+        // validate in ascending order; first confirmed root is the TOI
+        for (int pass = 0; pass < 5; ++pass) {
+            int best = -1;
+            for (int s = 0; s < 5; ++s)
+                if (roots[s] == roots[s] && (best < 0 || roots[s] < roots[best])) best = s;
+            if (best < 0) break;
+            double t = roots[best];
+            roots[best] = NaN;
+            if (confirm_hit(kd, a, b, t, tol)) {
+                toi = t;
+                break;
+            }
+        }
+    } else {
+        // ---- dense distance sampling for identically coplanar motion (ccd.py:171-195)
+        double d0 = pair_distance(kd, a.p[0], a.p[1], a.p[2], a.p[3]);
+        double mv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mv[k] = norm3(b.p[k] - a.p[k]);
+        double ra, rb;
+        if (kd == CS_VT) {
+            ra = np_max(np_max(np_max(mv[0], 0.0), 0.0), 0.0);
+            rb = np_max(np_max(np_max(0.0, mv[1]), mv[2]), mv[3]);
+        } else {
+            ra = np_max(np_max(np_max(mv[0], mv[1]), 0.0), 0.0);
+            rb = np_max(np_max(np_max(0.0, 0.0), mv[2]), mv[3]);
+        }
+        double reach = ra + rb;
+        double e1 = np_max(ext, 1.0);
+        if (d0 <= reach + 1e-9 * e1) {
+            d3 dp[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dp[k] = b.p[k] - a.p[k];
+            for (int s = 1; s <= 64; ++s) {
+                double t = (double)s * (1.0 / 64.0);
+                d3 q[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) q[k] = a.p[k] + t * dp[k];
+                double d = pair_distance(kd, q[0], q[1], q[2], q[3]);
+                if (d <= 1e-9 * e1) {
+                    toi = t;
+                    break;
+                }
+            }
+        }
+    }
+    toi_out[i] = toi;
+}
+
+__global__ void k_distance_toi(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+                               const double* __restrict__ x0, const double* __restrict__ x1, int64_t P,
+                               double floor_frac, int max_iter, double* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const int kd = kind[i];
+    const int4 id = idx[i];
+    Corners a = gather4(x0, id), b = gather4(x1, id);
+    d3 dp[4];
+    double mv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        dp[k] = b.p[k] - a.p[k];
+        mv[k] = norm3(dp[k]);
+    }
+    // L = max(side-1 displacement) + max(side-2 displacement)  (ccd.py:241-245)
+    double la, lb;
+    if (kd == CS_VT) {
+        la = np_max(np_max(np_max(mv[0], 0.0), 0.0), 0.0);
+        lb = np_max(np_max(np_max(0.0, mv[1]), mv[2]), mv[3]);
+    } else {
+        la = np_max(np_max(np_max(mv[0], mv[1]), 0.0), 0.0);
+        lb = np_max(np_max(np_max(0.0, 0.0), mv[2]), mv[3]);
+    }
+    const double L = la + lb;
+    double d = pair_distance(kd, a.p[0], a.p[1], a.p[2], a.p[3]);
+    const double goal = floor_frac * d;
+    const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
+    double toi = NaN;
+    if (d <= 0.0) toi = 0.0;
+    if (d > 0.0 && L > 0.0) {
+        double t = 0.0;
+        bool alive = true;
+        for (int it = 0; it < max_iter; ++it) {
+            t += (d - goal) / L;
+            if (!(t <= 1.0)) {
+                alive = false;  // left the interval: never reaches the goal
+                break;
+            }
+            d3 q[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) q[k] = a.p[k] + t * dp[k];
+            d = pair_distance(kd, q[0], q[1], q[2], q[3]);
+            if (d <= goal * 0x1.000000044b830p+0) {  // goal * (1.0 + 1e-9), ccd.py:261
+                toi = t;
+                alive = false;
+                break;
+            }
+        }
+        if (alive) toi = t;  // unresolved: safe time reached so far
+    }
+    out[i] = toi;
+}
+
+// Witness refresh: bary/params, distance and separating normal (stepper.py:194-216).
+__global__ void k_witness(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+                          const double* __restrict__ x, int64_t P, double* __restrict__ bary,
+                          double* __restrict__ dist, double* __restrict__ normal, double* __restrict__ p1_out,
+                          double* __restrict__ p2_out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const int kd = kind[i];
+    Corners a = gather4(x, idx[i]);
+    d3 p1, p2;
+    double l1, l2, d;
+    if (kd == CS_VT) {
+        d = pt_tri_closest(a.p[0], a.p[1], a.p[2], a.p[3], l1, l2, p2);
+        p1 = a.p[0];
+    } else {
+        d = seg_seg_closest(a.p[0], a.p[1], a.p[2], a.p[3], l1, l2, p1, p2);
+    }
+    d3 n = p1 - p2;
+    double nn = norm3(n);
+    if (nn > 1e-12) {
+        n = d3{n.x / nn, n.y / nn, n.z / nn};
+    } else {
+        d3 alt = kd == CS_VT ? cross3(a.p[2] - a.p[1], a.p[3] - a.p[1]) : cross3(a.p[1] - a.p[0], a.p[3] - a.p[2]);
+        double an = norm3(alt);
+        if (an > 0.0) alt = d3{alt.x / an, alt.y / an, alt.z / an};
+        if (an == 0.0) alt = d3{1.0, 0.0, 0.0};
+        n = alt;
+    }
+    bary[2 * i] = l1;
+    bary[2 * i + 1] = l2;
+    dist[i] = d;
+    if (normal) st3(normal, i, n);
+    if (p1_out) st3(p1_out, i, p1);
+    if (p2_out) st3(p2_out, i, p2);
+}
+
+__device__ __forceinline__ double ndb_weight(int life, double k, double base) {
+    int span = life < 64 ? life : 64;
+    double p = (base == 2.0) ? ldexp(1.0, span) : pow(base, (double)span);
+    return k * p;
+}
+
+// frozen-witness points on both sides at positions x (stepper.py:226-236, 254-263)
+__device__ __forceinline__ void witness_sides(int kd, const Corners& q, double l1, double l2, d3& s1, d3& s2) {
+    if (kd == CS_VT) {
+        s1 = q.p[0];
+        s2 = (q.p[1] + l1 * (q.p[2] - q.p[1])) + l2 * (q.p[3] - q.p[1]);
+    } else {
+        s1 = q.p[0] + l1 * (q.p[1] - q.p[0]);
+        s2 = q.p[2] + l2 * (q.p[3] - q.p[2]);
+    }
+}
+
+struct SamplePattern {
+    double vt[6][2];
+    double ee[6][2];
+    int width;  // max(kv, ke); shorter pattern already padded by repetition
+};
+
+// Partial CCD classifier + NDB update, one pass per inner LG iteration.
+__global__ void k_partial_ndb(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+                              const double* __restrict__ xa, const double* __restrict__ xc, int64_t P,
+                              SamplePattern pat, const double* __restrict__ bary,
+                              const double* __restrict__ normal, double d_hat, double k_ndb, double base,
+                              int* __restrict__ life, double* __restrict__ weight,
+                              uint8_t* __restrict__ engaged, int write_active, uint8_t* __restrict__ active_out,
+                              int* __restrict__ eng_count) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool eng = false;
+    if (i < P) {
+    const int kd = kind[i];
+    const int4 id = idx[i];
+    Corners s = gather4(xa, id), e = gather4(xc, id);
+    // projection sample: closest point at the interval start (partial.py:170-178)
+    double pl1, pl2;
+    {
+        d3 tmp1, tmp2;
+        if (kd == CS_VT)
+            pt_tri_closest(s.p[0], s.p[1], s.p[2], s.p[3], pl1, pl2, tmp1);
+        else
+            seg_seg_closest(s.p[0], s.p[1], s.p[2], s.p[3], pl1, pl2, tmp1, tmp2);
+    }
+    d3 be[3], bs[3];
+    if (kd == CS_VT) {
+        be[0] = e.p[1] - e.p[0]; be[1] = e.p[2] - e.p[1]; be[2] = e.p[3] - e.p[1];
+        bs[0] = s.p[1] - s.p[0]; bs[1] = s.p[2] - s.p[1]; bs[2] = s.p[3] - s.p[1];
+    } else {
+        be[0] = e.p[2] - e.p[0]; be[1] = e.p[0] - e.p[1]; be[2] = e.p[3] - e.p[2];
+        bs[0] = s.p[2] - s.p[0]; bs[1] = s.p[0] - s.p[1]; bs[2] = s.p[3] - s.p[2];
+    }
+    double g[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) g[a][b] = dot3(be[a], bs[b]);
+    const double c1 = g[0][1] + g[1][0], c2 = g[0][2] + g[2][0], c12 = g[1][2] + g[2][1];
+    bool act = false;
+    for (int k = 0; k <= pat.width; ++k) {
+        double l1, l2;
+        if (k < pat.width) {
+            l1 = kd == CS_VT ? pat.vt[k][0] : pat.ee[k][0];
+            l2 = kd == CS_VT ? pat.vt[k][1] : pat.ee[k][1];
+        } else {
+            l1 = pl1;
+            l2 = pl2;
+        }
+        double q = g[0][0] + c1 * l1;
+        q = q + c2 * l2;
+        q = q + g[1][1] * (l1 * l1);
+        q = q + c12 * (l1 * l2);
+        q = q + g[2][2] * (l2 * l2);
+        act = act || (q <= 0.0);
+    }
+    // gap along the frozen witness direction at the candidate (stepper.py:218-236)
+    d3 s1, s2;
+    witness_sides(kd, e, bary[2 * i], bary[2 * i + 1], s1, s2);
+    const double gap = dot3(s1 - s2, ld3(normal, i));
+    act = act || (gap < d_hat);
+    int lf = act ? min(life[i] + 1, 64) : 0;
+    eng = act || (gap < 2.0 * d_hat);
+    life[i] = lf;
+    engaged[i] = eng;
+    weight[i] = eng ? ndb_weight(lf, k_ndb, base) : 0.0;
+    if (write_active) active_out[i] = act;
+    }
+    if (eng_count != nullptr) {
+        const unsigned ballot = __ballot_sync(0xffffffffu, eng);
+        if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(eng_count, __popc(ballot));
+    }
+}
+
+// Engaged set and weights after a full-CCD site (stepper.py:483-487, 564-565).
+__global__ void k_engage_init(const double* __restrict__ toi, const double* __restrict__ dist, const int* __restrict__ life,
+                              int64_t P, double d_hat, double k_ndb, double base, uint8_t* __restrict__ engaged,
+                              double* __restrict__ weight, int* __restrict__ eng_count) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool eng = false;
+    if (i < P) {
+        double t = toi[i];
+        eng = (t == t) || (dist[i] < 2.0 * d_hat);
+        engaged[i] = eng;
+        weight[i] = eng ? ndb_weight(life[i], k_ndb, base) : 0.0;
+    }
+    if (eng_count != nullptr) {
+        const unsigned ballot = __ballot_sync(0xffffffffu, eng);
+        if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(eng_count, __popc(ballot));
+    }
+}
+
+// Per engaged pair: 4 positional targets (stepper.py:238-285).  Entries for
+// immovable or zero-weight endpoints get key 0x7fffffff (sorted to the end).
+// frozen_k >= 0 selects residual forwarding's frozen weights (stepper.py:635-642).
+__global__ void k_collision_terms(const int* __restrict__ sel, int64_t A, const int8_t* __restrict__ kind,
+                                  const int4* __restrict__ idx, const double* __restrict__ xw,
+                                  const double* __restrict__ bary, const double* __restrict__ normal,
+                                  const double* __restrict__ weight, double d_hat, int n_cloth,
+                                  const int* __restrict__ free_index, int cloth_only,
+                                  int* __restrict__ key, double* __restrict__ w_out, double* __restrict__ t_out) {
+    int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (a >= A) return;
+    const int i = sel[a];
+    const int kd = kind[i];
+    const int4 id = idx[i];
+    Corners q = gather4(xw, id);
+    const double l1 = bary[2 * i], l2 = bary[2 * i + 1];
+    d3 s1, s2;
+    witness_sides(kd, q, l1, l2, s1, s2);
+    const d3 nrm = ld3(normal, i);
+    const double gap = dot3(s1 - s2, nrm);
+    double deficit = d_hat - gap;
+    deficit = (deficit != deficit) ? deficit : (deficit > 0.0 ? deficit : 0.0);
+    double gam[4];
+    if (kd == CS_VT) {
+        gam[0] = 1.0;
+        gam[1] = (1.0 - l1) - l2;
+        gam[2] = l1;
+        gam[3] = l2;
+    } else {
+        gam[0] = 1.0 - l1;
+        gam[1] = l1;
+        gam[2] = 1.0 - l2;
+        gam[3] = l2;
+    }
+    const int ids[4] = {id.x, id.y, id.z, id.w};
+    bool mov[4];
+    bool m1 = false, m2 = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int v = ids[k];
+        mov[k] = (v < n_cloth) && (free_index[v < n_cloth ? v : n_cloth - 1] >= 0);
+        bool first = (kd == CS_VT) ? (k == 0) : (k < 2);
+        if (first) m1 = m1 || mov[k];
+        else m2 = m2 || mov[k];
+    }
+    const bool both = m1 && m2;
+    const double sh1 = (both ? 0.5 : (m1 ? 1.0 : 0.0)) * deficit;
+    const double sh2 = (both ? 0.5 : (m2 ? 1.0 : 0.0)) * deficit;
+    const double wp = weight[i];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        bool first = (kd == CS_VT) ? (k == 0) : (k < 2);
+        double mvs = first ? sh1 : -sh2;
+        d3 tg = q.p[k] + mvs * nrm;
+        double g = clip01(gam[k]);
+        double w = wp * g;
+        bool keep = mov[k] && (w > 0.0);
+        if (cloth_only && ids[k] >= n_cloth) keep = false;
+        int64_t o = 4 * a + k;
+        key[o] = keep ? free_index[ids[k]] : 0x7fffffff;
+        w_out[o] = w;
+        st3(t_out, o, tg);
+    }
+}
+
+// min over non-NaN TOIs; flag any TOI <= 0 (stepper.py:445-452).  Two passes.
+__global__ void k_min_toi_partial(const double* __restrict__ toi, int64_t P, double* __restrict__ part) {
+    __shared__ double sm[256];
+    double m = __longlong_as_double(0x7ff0000000000000ULL);  // +inf
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+        double t = toi[i];
+        if (t == t && t < m) m = t;
+    }
+    sm[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+
+__global__ void k_min_toi_final(const double* __restrict__ part, int nparts, double alpha, double* __restrict__ out) {
+    __shared__ double sm[256];
+    double m = __longlong_as_double(0x7ff0000000000000ULL);
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) m = fmin(m, part[i]);
+    sm[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double t = sm[0];
+        // out[0] = min toi (inf if none), out[1] = clamp factor (1 if none), out[2] = penetration flag
+        out[0] = t;
+        bool none = isinf(t);
+        out[1] = none ? 1.0 : alpha * t;
+        out[2] = (!none && t <= 0.0) ? 1.0 : 0.0;
+    }
+}
+
+}  // namespace cs

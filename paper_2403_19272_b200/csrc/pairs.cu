@@ -1,0 +1,163 @@
+// Pair bookkeeping between CCD sites.
+//
+//   k_hash_insert / k_hash_lookup   life-span carry-over by canonical pair key
+//                                   (reference stepper.py:300-305, pairs.py:51-62).
+//                                   Keys: VT (0, v, f), EE (1, E, F) with E < F, which
+//                                   identify the same pairs as the reference's sorted
+//                                   vertex-id keys.  Open addressing, 64-bit CAS; the
+//                                   result is order independent, hence deterministic.
+//   k_mark_segments                 per-free-vertex [beg, end) ranges over the stably
+//                                   sorted collision stamps (np.add.at order per vertex)
+//   k_flag_engaged                  engaged & weight > 0 flags (stepper.py:245)
+#include "common.cuh"
+
+namespace cs {
+
+#define CS_EMPTY_KEY 0xffffffffffffffffull
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+__global__ void k_hash_insert(const unsigned long long* __restrict__ keys, const int* __restrict__ life, int64_t P,
+                              unsigned long long* __restrict__ tkeys, int* __restrict__ tvals,
+                              unsigned long long mask) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const unsigned long long k = keys[i];
+    unsigned long long h = mix64(k) & mask;
+    while (true) {
+        const unsigned long long prev = atomicCAS(&tkeys[h], CS_EMPTY_KEY, k);
+        if (prev == CS_EMPTY_KEY || prev == k) {
+            tvals[h] = life[i];
+            return;
+        }
+        h = (h + 1) & mask;
+    }
+}
+
+__global__ void k_hash_lookup(const unsigned long long* __restrict__ keys, int64_t P,
+                              const unsigned long long* __restrict__ tkeys, const int* __restrict__ tvals,
+                              unsigned long long mask, int* __restrict__ life) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const unsigned long long k = keys[i];
+    unsigned long long h = mix64(k) & mask;
+    int out = 0;
+    while (true) {
+        const unsigned long long t = tkeys[h];
+        if (t == k) {
+            out = tvals[h];
+            break;
+        }
+        if (t == CS_EMPTY_KEY) break;
+        h = (h + 1) & mask;
+    }
+    life[i] = out;
+}
+
+__global__ void k_flag_engaged(const uint8_t* __restrict__ engaged, const double* __restrict__ weight, int64_t P,
+                               uint8_t* __restrict__ flags, int* __restrict__ count) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool f = false;
+    if (i < P) {
+        f = engaged[i] && (weight[i] > 0.0);
+        flags[i] = f;
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(count, __popc(ballot));
+}
+
+__global__ void k_count_true(const uint8_t* __restrict__ v, int64_t P, int* __restrict__ count) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool f = i < P && v[i];
+    const unsigned ballot = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(count, __popc(ballot));
+}
+
+// sorted keys (free row, or 0x7fffffff for dropped) -> seg_beg/seg_end per row,
+// plus the ascending list of distinct rows (collided vertices for the reduced update)
+__global__ void k_mark_segments(const int* __restrict__ skey, int m, int* __restrict__ seg_beg,
+                                int* __restrict__ seg_end, int* __restrict__ rows_out_flag) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const int k = skey[j];
+    if (k == 0x7fffffff) return;
+    if (j == 0 || skey[j - 1] != k) {
+        seg_beg[k] = j;
+        rows_out_flag[j] = 1;
+    }
+    if (j == m - 1 || skey[j + 1] != k) seg_end[k] = j + 1;
+}
+
+__global__ void k_iota(int* __restrict__ a, int64_t m) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) a[i] = (int)i;
+}
+
+__global__ void k_fill_u64(unsigned long long* __restrict__ a, int64_t m, unsigned long long v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) a[i] = v;
+}
+
+__global__ void k_rf_weights(const double* __restrict__ dist, int64_t P, double d_hat, double k,
+                             uint8_t* __restrict__ engaged, double* __restrict__ weight) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const bool e = dist[i] < 2.0 * d_hat;
+    engaged[i] = e;
+    weight[i] = e ? k : 0.0;
+}
+
+__global__ void k_neg_gather(const double* __restrict__ g, const int* __restrict__ free_ids, int nf,
+                             double* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nf) return;
+    const int v = free_ids[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[3 * i + c] = -g[3 * v + c];
+}
+
+}  // namespace cs
+
+namespace cs {
+
+// v = (x_final - x) / h  (stepper.py:597)
+__global__ void k_velocity_update(const double* __restrict__ xfin, const double* __restrict__ x,
+                                  double* __restrict__ v, int64_t m, double h) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) v[i] = (xfin[i] - x[i]) / h;
+}
+
+// delta_i = sum of stamp weights in np.add.at order (stepper.py:653-657)
+__global__ void k_stamp_delta(int nf, const int* __restrict__ seg_beg, const int* __restrict__ seg_end,
+                              const int* __restrict__ src, const double* __restrict__ w, double* __restrict__ delta) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nf) return;
+    double d = 0.0;
+    if (seg_beg != nullptr)
+        for (int k = seg_beg[i]; k < seg_end[i]; ++k) d = d + w[src[k]];
+    delta[i] = d;
+}
+
+// stamp sort keys from cloth vertex ids: free row or sentinel (constraints.py:252-255)
+__global__ void k_stamp_keys(const int* __restrict__ ids, int m, const int* __restrict__ free_index, int n,
+                             int* __restrict__ key) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const int v = ids[j];
+    const int f = (v >= 0 && v < n) ? free_index[v] : -1;
+    key[j] = f >= 0 ? f : 0x7fffffff;
+}
+
+__global__ void k_nonzero_flags(const double* __restrict__ d, int m, int* __restrict__ flags) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) flags[i] = d[i] != 0.0;
+}
+
+}  // namespace cs

@@ -1,0 +1,305 @@
+"""Drop-in ``Simulation`` (reference pkg/src/clothsim/stepper.py:124-681).
+
+Same constructor, attributes and ``step()/run()`` contract as the reference.
+Scene setup (elastic weights, H, eigenbasis, static collision topology) runs
+once on the host; every step runs on the GPU inside ``cs_step`` (the native
+driver in csrc/abi.cu), so Python crosses the C ABI once per frame.  Prescribed
+pin/obstacle motion callbacks stay in Python (as in the reference) and their
+values are uploaded each step.
+
+``state`` is the device-resident ``SimState``: reading it downloads a host
+mirror; in-place edits of that mirror (reference tests do
+``sim.state.x_dot[:] = ...``) are written back before the next device call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from . import _lib
+from .collision import CollisionWorld, PairSet, VT, EE, default_samples
+from .constraints import assemble_global, build_elastic
+from .device import scene_desc, step_config_c
+from .mesh import ClothMesh, SimState
+from .stepconfig import StepConfig, StepReport
+from .subspace import build_subspace
+
+PenetrationError = _lib.PenetrationError
+
+_TIMING_KEYS = ("warm_start", "local", "global", "smoothing", "broad", "narrow_partial", "narrow_full")
+
+
+def _rms(v: np.ndarray) -> float:
+    return float(np.linalg.norm(v)) / max(np.sqrt(v.size), 1.0)
+
+
+class Simulation:
+    """One cloth plus optional obstacle meshes, stepped on the GPU under a StepConfig."""
+
+    def __init__(self, mesh: ClothMesh, config: StepConfig, stretch_stiffness: float = 160.0,
+                 bend_stiffness: float = 3e-4, obstacles=None, pin_motion=None, obstacle_motion=None,
+                 eigensolver: str = "host"):
+        if config.barrier_mode != "ndb":
+            raise NotImplementedError("the GPU pipeline implements the NDB barrier mode (DBB: SURVEY.md section 8f #3)")
+        self.mesh = mesh
+        self.config = config
+        self.elastic = build_elastic(mesh, stretch_stiffness, bend_stiffness)
+        self.system = assemble_global(mesh, self.elastic, config.h)
+        r_bar = min(config.r_bar, mesh.free.size)
+        r = min(config.r, r_bar)
+        self.subspace = build_subspace(self.system, mesh.rest_positions[mesh.free], r_bar, r, method=eigensolver)
+        self.samples = default_samples(config.samples)
+        self.pin_motion = pin_motion
+        self.obstacle_motion = obstacle_motion
+
+        n = mesh.vertex_count
+        verts, tris = [], []
+        offset = n
+        for ov, ot in (obstacles or []):
+            verts.append(np.asarray(ov, dtype=np.float64))
+            tris.append(np.asarray(ot, dtype=np.int64) + offset)
+            offset += len(ov)
+        obstacle_x = np.concatenate(verts) if verts else np.zeros((0, 3))
+        self.world_triangles = np.concatenate([mesh.triangles] + tris) if tris else mesh.triangles
+        self.tri_static = np.zeros(len(self.world_triangles), dtype=bool)
+        self.tri_static[len(mesh.triangles):] = True
+        world_rest = np.concatenate([mesh.rest_positions, obstacle_x])
+        self.bvh = CollisionWorld.build(self.world_triangles, world_rest, self.tri_static)
+
+        self.k = config.ndb_k if config.ndb_k > 0 else self.elastic.mean_weight
+        self.kappa = config.dbb_kappa if config.dbb_kappa > 0 else self.k / ((config.d_hat / 2.0) ** 2 * np.log(2.0))
+        self.gravity_force = mesh.vertex_mass[:, None] * np.asarray(config.gravity)
+        self._verify_oracle = None
+        self.last_outer_deltas = []
+        self.last_report_c = None
+
+        self._lib = _lib.load()
+        desc, keep = scene_desc(mesh, self.elastic, self.system, self.subspace, self.bvh, obstacle_x,
+                                self.gravity_force, mesh.rest_positions)
+        self._cfg_c = step_config_c(config, self.k)
+        status = ctypes.c_int(0)
+        self._scene = self._lib.cs_scene_create(ctypes.byref(desc), ctypes.byref(self._cfg_c), ctypes.byref(status))
+        del keep
+        if not self._scene:
+            _lib.check(status.value or _lib.CS_BAD_ARGUMENT, "cs_scene_create")
+        self._n_obs = len(obstacle_x)
+        self._host_state = None
+        self._host_obstacles = None
+        self._step_index = 0
+
+    def __del__(self):
+        scene = getattr(self, "_scene", None)
+        if scene:
+            self._lib.cs_scene_destroy(scene)
+            self._scene = None
+
+    # ------------------------------------------------------------ state mirror
+    def _stream(self):
+        return _lib.stream_handle()
+
+    def _flush(self):
+        """Write back host-mirror edits before the device uses the state."""
+        st = self._host_state
+        if st is None:
+            return
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (st.x, st.x_dot, st.x_prev, st.delta_f)]
+        obs = np.ascontiguousarray(self._host_obstacles, dtype=np.float64) if self._n_obs else None
+        _lib.check(self._lib.cs_set_state(self._scene, *[a.ctypes.data for a in arrs],
+                                          obs.ctypes.data if obs is not None else None, int(st.step_index),
+                                          self._stream()), "cs_set_state")
+        self._step_index = int(st.step_index)
+
+    def host_state(self) -> SimState:
+        n = self.mesh.vertex_count
+        bufs = [np.empty((n, 3)) for _ in range(4)]
+        obs = np.empty((self._n_obs, 3))
+        idx = ctypes.c_int(0)
+        _lib.check(self._lib.cs_get_state(self._scene, *[b.ctypes.data for b in bufs],
+                                          obs.ctypes.data if self._n_obs else None, ctypes.byref(idx),
+                                          self._stream()), "cs_get_state")
+        self._host_obstacles = obs
+        return SimState(x=bufs[0], x_dot=bufs[1], x_prev=bufs[2], delta_f=bufs[3], step_index=self._step_index)
+
+    @property
+    def state(self) -> SimState:
+        if self._host_state is None:
+            self._host_state = self.host_state()
+        return self._host_state
+
+    @state.setter
+    def state(self, st: SimState):
+        self._host_state = SimState(x=np.array(st.x, dtype=np.float64), x_dot=np.array(st.x_dot, dtype=np.float64),
+                                    x_prev=np.array(st.x_prev, dtype=np.float64),
+                                    delta_f=np.array(st.delta_f, dtype=np.float64), step_index=int(st.step_index))
+        if self._host_obstacles is None:
+            self.host_state()
+
+    @property
+    def obstacle_x(self) -> np.ndarray:
+        if self._host_state is not None and self._host_obstacles is not None:
+            return self._host_obstacles
+        self.host_state()
+        return self._host_obstacles
+
+    @obstacle_x.setter
+    def obstacle_x(self, value):
+        _ = self.state
+        self._host_obstacles = np.array(value, dtype=np.float64).reshape(-1, 3)
+
+    # ------------------------------------------------------------ reference helpers
+    def world(self, cloth_x: np.ndarray, obstacle_x: np.ndarray | None = None) -> np.ndarray:
+        """stepper.py:177-180."""
+        if obstacle_x is None:
+            obstacle_x = self.obstacle_x
+        return np.concatenate([cloth_x, obstacle_x]) if len(obstacle_x) else cloth_x.copy()
+
+    def _pin_targets(self, t: float):
+        if self.pin_motion is None or self.mesh.pinned.size == 0:
+            return None
+        return np.ascontiguousarray(self.pin_motion(t), dtype=np.float64).reshape(-1, 3)
+
+    def _obstacle_targets(self, t: float):
+        if self.obstacle_motion is None or not self._n_obs:
+            return None
+        return np.ascontiguousarray(self.obstacle_motion(t), dtype=np.float64).reshape(-1, 3)
+
+    # ------------------------------------------------------------ stepping
+    def step(self) -> StepReport:
+        """One Delta-t step on the GPU (reference stepper.py:454-624)."""
+        cfg = self.config
+        self._flush()
+        t_now = self._step_index * cfg.h
+        pins = self._pin_targets(t_now + cfg.h)
+        obs = self._obstacle_targets(t_now + cfg.h)
+        rep = _lib.StepReportC()
+        rc = self._lib.cs_step(self._scene, pins.ctypes.data if pins is not None else None,
+                               obs.ctypes.data if obs is not None else None, ctypes.byref(rep), self._stream())
+        # a failed step leaves the state untouched (the reference raises before assigning)
+        self._host_state = None
+        _lib.check(rc, "cs_step")
+        self._step_index += 1
+        self.last_report_c = rep
+        self.last_outer_deltas = [rep.outer_deltas[i] for i in range(rep.n_outer_deltas)]
+        report = StepReport(
+            lg_iterations=rep.lg_iterations, outer_loops=rep.outer_loops, toi_exit=rep.toi_exit,
+            rf_triggered=bool(rep.rf_triggered), active_pairs=rep.active_pairs, full_ccd_calls=rep.full_ccd_calls,
+            partial_ccd_calls=rep.partial_ccd_calls, cap_hit=bool(rep.cap_hit),
+            timings={"warm_start": rep.t_warm_start, "local": rep.t_local, "global": rep.t_global,
+                     "smoothing": rep.t_smoothing, "broad": rep.t_broad, "narrow_partial": rep.t_narrow_partial,
+                     "narrow_full": rep.t_narrow_full, "rf": rep.t_rf})
+        if cfg.verify and self._verify_oracle is not None:
+            st = self.state
+            xw = self.world(st.x)
+            bad = self._verify_oracle(xw, self.bvh.triangles)
+            report.penetration_free = len(bad) == 0
+            if not report.penetration_free:
+                raise PenetrationError(f"step {self._step_index - 1}: {len(bad)} intersecting triangle pairs",
+                                       state_dump={"x": st.x, "pairs": bad})
+        return report
+
+    def run(self, steps: int, on_step=None) -> list:
+        """reference stepper.py:674-681."""
+        out = []
+        for _ in range(steps):
+            rep = self.step()
+            out.append(rep)
+            if on_step is not None:
+                on_step(self, rep)
+        return out
+
+    # ------------------------------------------------------------ stage-level API (device)
+    def _dbuf(self, a):
+        import torch
+
+        return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")
+
+    def warm_start(self, z: np.ndarray, pin_next: np.ndarray):
+        """Collision-free LG iterations in the wide basis (stepper.py:384-400), device stages."""
+        import torch
+
+        cfg, mesh = self.config, self.mesh
+        self._flush()
+        x = np.array(z, dtype=np.float64)
+        if mesh.pinned.size:
+            x[mesh.pinned] = pin_next
+        zd = self._dbuf(z)
+        xd = self._dbuf(x)
+        b = torch.empty((mesh.free.size, 3), dtype=torch.float64, device="cuda")
+        delta = torch.empty(mesh.free.size, dtype=torch.float64, device="cuda")
+        free = torch.as_tensor(mesh.free, device="cuda")
+        its = 0
+        for _ in range(cfg.warm_start_cap):
+            _lib.check(self._lib.cs_assemble_rhs(self._scene, zd.data_ptr(), xd.data_ptr(), None, None, None, 0,
+                                                 b.data_ptr(), delta.data_ptr(), self._stream()), "cs_assemble_rhs")
+            xf = xd[free].contiguous()
+            x0 = xf.clone()
+            _lib.check(self._lib.cs_warmstart_correction(self._scene, b.data_ptr(), xf.data_ptr(), self._stream()),
+                       "cs_warmstart_correction")
+            dx = float(torch.linalg.vector_norm(xf - x0)) / max(np.sqrt(xf.numel()), 1.0)
+            xd[free] = xf
+            its += 1
+            if dx < cfg.eps_initial:
+                break
+        return xd.cpu().numpy(), its
+
+    def energy(self, x: np.ndarray, z: np.ndarray, collision=None):
+        """Energy and gradient (stepper.py:309-380, 'quad' form).
+
+        The gradient comes from the device kernel the residual forwarding uses;
+        the scalar energy terms are a host diagnostic (not on the step path).
+        """
+        import torch
+
+        mesh, el, h = self.mesh, self.elastic, self.config.h
+        x = np.asarray(x, dtype=np.float64)
+        z = np.asarray(z, dtype=np.float64)
+        s = mesh.vertex_mass[:, None] / (h * h)
+        e_in = 0.5 * float(np.sum(s * (x - z) ** 2))
+        ln = np.linalg.norm(x[el.edges[:, 1]] - x[el.edges[:, 0]], axis=1)
+        e_st = 0.5 * float((el.stretch_w * (ln - el.edge_rest) ** 2).sum())
+        e_b = 0.0
+        if len(el.stencils):
+            flat = np.einsum("sj,sjd->sd", el.bend_k, x[el.stencils])
+            e_b = 0.5 * float(np.sum(el.bend_w * np.einsum("sd,sd->s", flat, flat)))
+        e_c = 0.0
+        ids = w = tg = None
+        nq = 0
+        if collision is not None:
+            if collision[0] != "quad":
+                raise ValueError(f"unknown collision energy form {collision[0]!r}")
+            _, ids_h, w_h, tg_h = collision
+            diff = x[ids_h] - tg_h
+            e_c = 0.5 * float(np.sum(w_h * np.einsum("mj,mj->m", diff, diff)))
+            ids = torch.as_tensor(np.asarray(ids_h, dtype=np.int32), device="cuda")
+            w = self._dbuf(w_h)
+            tg = self._dbuf(tg_h)
+            nq = len(ids_h)
+        grad = torch.empty((mesh.vertex_count, 3), dtype=torch.float64, device="cuda")
+        xd, zd = self._dbuf(x), self._dbuf(z)
+        _lib.check(self._lib.cs_energy_gradient(self._scene, xd.data_ptr(), zd.data_ptr(),
+                                                ids.data_ptr() if nq else None, w.data_ptr() if nq else None,
+                                                tg.data_ptr() if nq else None, nq, grad.data_ptr(), self._stream()),
+                   "cs_energy_gradient")
+        total = e_in + e_st + e_b + e_c
+        return total, grad.cpu().numpy(), {"inertia": e_in, "stretch": e_st, "bend": e_b, "barrier": e_c}
+
+    def broad_phase(self, x_start_w, x_end_w, margin: float | None = None) -> PairSet:
+        """Device broad phase over this scene's world (reference bvh.py:207-292)."""
+        import torch
+
+        margin = self.config.d_hat if margin is None else margin
+        a, b = self._dbuf(x_start_w), self._dbuf(x_end_w)
+        count = ctypes.c_longlong(0)
+        _lib.check(self._lib.cs_broad_phase(self._scene, a.data_ptr(), b.data_ptr(), margin, ctypes.byref(count),
+                                            self._stream()), "cs_broad_phase")
+        P = count.value
+        kind = torch.empty(max(P, 1), dtype=torch.int8, device="cuda")
+        idx = torch.empty((max(P, 1), 4), dtype=torch.int32, device="cuda")
+        _lib.check(self._lib.cs_scene_pairs(self._scene, kind.data_ptr(), idx.data_ptr(), self._stream()),
+                   "cs_scene_pairs")
+        kind = kind[:P].cpu().numpy()
+        idx = idx[:P].cpu().numpy().astype(np.int64)
+        return PairSet(kind=kind, idx=idx, life_span=np.zeros(P, np.int64), weight=np.zeros(P))
