@@ -1,0 +1,405 @@
+"""Benchmark: sim FPS & ms/frame at dt = 1/200 on the ~340K-vertex garment (BASELINE config 4).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload skirt|batch]
+
+One process per GPU (torchrun for N > 1).  A single garment does not shard
+(SURVEY.md section 8e): at N > 1 every rank steps its own independent replica
+(weak scaling, no collective on the hot path; the only collective is the
+max-over-ranks timing reduction).  ``--workload batch`` runs config 5 (64
+independent 100K-vertex drapes split 64/N per GPU).
+
+Rank 0 prints ONE JSON line.  ``value`` = whole-job steps/s (device time,
+CUDA events on the launching stream, max over ranks); ``e2e`` = the same
+metric through the public API with host buffers every step (pin/obstacle
+targets H2D inside cs_step, state x D2H after it).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sim FPS & ms/frame at Δt=1/200 (340K-vert garment); solver-kernel HBM GB/s"
+PAPER_FPS = 4.8          # fashion show, 340K-vertex skirt, RTX 3090
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="skirt", choices=["skirt", "batch", "small"])
+    ap.add_argument("--resolution", type=int, default=584)
+    ap.add_argument("--batch-scenes", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return ws, rank, local
+
+
+def max_over_ranks(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws: int):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def make_scenes(args, rank: int, ws: int):
+    import paper_2403_19272_b200 as P
+    from paper_2403_19272_b200 import scenes as S
+
+    cfg = P.StepConfig(h=1.0 / 200.0)
+    if args.workload == "skirt":
+        return [S.skirt_scene(cfg, around=args.resolution, down=args.resolution, eigensolver="device")], \
+            f"skirt_{args.resolution}x{args.resolution} (config 4)"
+    if args.workload == "small":
+        return [P.build_scene("sphere_drape", resolution=64, size=0.5, config=cfg)], "sphere_drape_64 (smoke)"
+    per = args.batch_scenes // ws
+    ids = range(rank * per, (rank + 1) * per)
+    return [S.drape_scene(i, resolution=317, config=cfg, eigensolver="device") for i in ids], \
+        f"drape_batch {args.batch_scenes}x317^2 (config 5)"
+
+
+# ------------------------------------------------------------------ CPU oracle timing (bounded sample)
+def cpu_oracle_estimate(o, counts):
+    """Oracle (numpy port, single thread) seconds per step on this workload, from a
+    bounded sample: warm start + one LG iteration on the full mesh, one broad
+    phase, and full CCD + distance march on a pair sample; scaled with the GPU
+    run's own per-step counts (LG iterations, CCD sites, pairs per site)."""
+    from oracle import narrow
+    from oracle.broad import broad_phase
+
+    st = o.state
+    cfg = o.cfg
+    t0 = time.perf_counter()
+    z = st.x + cfg.h * st.x_dot + (cfg.h * cfg.h) * (o.gravity_force + st.delta_f) / o.mesh.vertex_mass[:, None]
+    pins = st.x[o.mesh.pinned]
+    z[o.mesh.pinned] = pins
+    from oracle import solver
+
+    b, _ = solver.assemble_rhs(o.sys, o.mesh, o.el, z, z, pins)
+    solver.warmstart_correction(o.sub, o.sys, b, z[o.mesh.free])
+    t_ws = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rep = {"timings": {k: 0.0 for k in ("local", "global", "smoothing")}}
+    o.inner_solve(z, st.x.copy(), pins, None, rep)
+    t_lg = time.perf_counter() - t0
+    xw = o.world(st.x)
+    xw1 = xw + 1e-4
+    t0 = time.perf_counter()
+    kind, idx = broad_phase(xw, xw1, o.topo, cfg.d_hat)
+    t_bp = time.perf_counter() - t0
+    m = min(len(kind), 20000)
+    sel = np.random.default_rng(0).choice(len(kind), m, replace=False) if len(kind) > m else np.arange(len(kind))
+    t0 = time.perf_counter()
+    narrow.full_ccd(kind[sel], idx[sel], xw, xw1)
+    narrow.distance_toi(kind[sel], idx[sel], xw, xw1, floor_frac=1.0 - cfg.alpha)
+    t_pair = (time.perf_counter() - t0) / max(m, 1)
+    t0 = time.perf_counter()
+    narrow.partial_ccd(kind[sel], idx[sel], xw, xw1, cfg.samples)
+    t_partial = (time.perf_counter() - t0) / max(m, 1)
+    if counts.get("pairs") is None:
+        counts = dict(counts, pairs=float(len(kind)))
+    per_step = (t_ws * counts["ws_iters"] + counts["lg"] * (t_lg + counts["pairs"] * t_partial)
+                + counts["sites"] * (t_bp + counts["pairs"] * t_pair))
+    sample = (f"oracle numpy port, 1 thread: warm-start iteration {t_ws:.2f}s, LG iteration {t_lg:.2f}s, "
+              f"broad phase {t_bp:.2f}s ({len(kind)} pairs), CCD {t_pair * 1e6:.1f}us/pair + partial "
+              f"{t_partial * 1e6:.1f}us/pair on {m} pairs; scaled by the GPU run's per-step counts "
+              f"(ws {counts['ws_iters']:.1f}, LG {counts['lg']:.1f}, sites {counts['sites']:.1f}, "
+              f"pairs/site {counts['pairs']:.0f})")
+    return per_step, sample
+
+
+# ------------------------------------------------------------------ arms
+def reference_oracle(args):
+    """The oracle (CPU port of the reference algorithm) on this bench's workload, built
+    without any GPU code.  Setup arrays (mesh, weights, H) come from the shared host setup;
+    the eigenbasis is a seeded random orthonormal block of the right shape (basis values
+    do not change the per-step cost; the reference's own eigsh takes ~6 min at 341K)."""
+    import paper_2403_19272_b200 as P
+    from paper_2403_19272_b200 import scenes as S
+    from paper_2403_19272_b200.subspace import Subspace
+    from oracle.stepper import OracleSimulation
+
+    cfg = P.StepConfig(h=1.0 / 200.0)
+    if args.workload == "skirt":
+        parts = S.skirt_parts(around=args.resolution, down=args.resolution)
+        mesh, obstacles = parts["mesh"], parts["obstacles"]
+        pm, om, ks, kb = parts["pin_motion"], parts["obstacle_motion"], 160.0, 3e-4
+        workload = f"skirt_{args.resolution}x{args.resolution} (config 4)"
+    else:
+        rho, ks, kb = S.drape_materials(1)[0]
+        v, t = S.grid_cloth(317, 1.0, height=0.25 + 2.0 * cfg.d_hat + 0.01)
+        v[:, :2] -= 0.5
+        mesh = P.build_mesh(v, t, rho)
+        obstacles = [S.icosphere(3, 0.25)]
+        pm = om = None
+        workload = "drape 317^2 (one scene of config 5)"
+    el = P.build_elastic(mesh, ks, kb)
+    sy = P.assemble_global(mesh, el, cfg.h)
+    nf = mesh.free.size
+    rb, r = min(cfg.r_bar, nf), min(cfg.r, cfg.r_bar)
+    q, _ = np.linalg.qr(np.random.default_rng(0).standard_normal((nf, rb)))
+    lam = np.linspace(1.0, 2.0, rb)
+    hx = sy.H @ mesh.rest_positions[mesh.free]
+    sub = Subspace(U=q, eigenvalues=lam, r=r, UHX=q.T @ hx, VHX=q[:, :r].T @ hx, rest=mesh.rest_positions[mesh.free])
+    n = mesh.vertex_count
+    ov = [np.asarray(o[0], dtype=np.float64) for o in obstacles]
+    ot = [np.asarray(o[1], dtype=np.int64) for o in obstacles]
+    off = n
+    tris = [mesh.triangles]
+    for a_v, a_t in zip(ov, ot):
+        tris.append(a_t + off)
+        off += len(a_v)
+    wt = np.concatenate(tris)
+    stat = np.zeros(len(wt), bool)
+    stat[len(mesh.triangles):] = True
+    obs_x = np.concatenate(ov) if ov else np.zeros((0, 3))
+    o = OracleSimulation(mesh, cfg, el, sy, sub, el.mean_weight, obs_x, wt, stat, pm, om)
+    return o, workload
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's CPU algorithm (oracle port) on the same workload."""
+    if rank != 0:
+        return
+    t_start = time.time()
+    o, workload = reference_oracle(args)
+    # nominal per-step counts (the GPU arm reports its measured ones)
+    counts = {"ws_iters": 2.0, "lg": 5.0, "sites": 3.0, "pairs": None}
+    per_steps = []
+    sample = ""
+    for _ in range(max(1, min(args.steps, 2))):
+        per, sample = cpu_oracle_estimate(o, counts)
+        per_steps.append(per)
+    per = float(np.median(per_steps))
+    fps = 1.0 / per
+    line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "FPS", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": fps / PAPER_FPS, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload},
+            "cpu_baseline": {"value": fps, "unit": "FPS", "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": fps, "unit": "FPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.time() - t_start}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+
+    import paper_2403_19272_b200 as P  # noqa: F401
+    from paper_2403_19272_b200 import build
+
+    if ws == 1:
+        torch.cuda.set_device(0)
+    build.build()
+    t_setup = time.time()
+    sims, workload = make_scenes(args, rank, ws)
+    setup_s = time.time() - t_setup
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for s in sims:
+            s.step()
+    barrier(ws)
+    torch.cuda.synchronize()
+    reps = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            for s in sims:
+                reps.append((s.step(), s.last_report_c))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    dev_s = e0.elapsed_time(e1) / 1e3
+    dev_s = max_over_ranks(dev_s, ws)
+    scenes_total = len(sims) * ws
+    value = scenes_total * args.steps / dev_s
+
+    # end to end through the public API with host buffers each step
+    e2e = None
+    if not args.no_e2e:
+        k_e2e = max(3, args.steps // 2)
+        h2d = sum((s.mesh.pinned.size + s._n_obs) * 24 for s in sims)
+        d2h = sum(s.mesh.vertex_count * 24 for s in sims)
+        barrier(ws)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            for s in sims:
+                s.step()
+                _ = s.state.x          # D2H of the step's result
+        torch.cuda.synchronize()
+        wall = max_over_ranks(time.perf_counter() - t0, ws)
+        e2e = {"value": scenes_total * k_e2e / wall, "unit": "FPS", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": k_e2e}
+
+    if rank != 0:
+        return
+    # per-stage ms/frame and counters
+    keys = ["warm_start", "local", "global", "smoothing", "broad", "narrow_partial", "narrow_full", "rf"]
+    stage = {k: float(np.mean([r.timings[k] for r, _ in reps])) for k in keys}
+    lg = float(np.mean([r.lg_iterations for r, _ in reps]))
+    sites = float(np.mean([r.full_ccd_calls for r, _ in reps]))
+    pairs = float(np.mean([c.pairs_max_site for _, c in reps]))
+    ws_iters = float(np.mean([c.warm_start_iterations for _, c in reps]))
+    launches = int(sum(c.gpu_launches for _, c in reps))
+    sim0 = sims[0]
+    nf = sim0.mesh.free.size
+    nnz = sim0.system.H.nnz
+    # roofline: dominant solver kernel = A-Jacobi pass (k_jacobi_a / k_jacobi_b), one SELL SpMV each:
+    # algorithmic bytes per launch = 12 B/nnz (fp64 value + int32 col) + 88 B/row (x gather, b|x, t, diag, delta)
+    bytes_per_launch = 12.0 * nnz + 88.0 * nf
+    jac_launches = lg * 2 * ((sim0.config.smoothing_iterations + 1) // 2)
+    t_launch = stage["smoothing"] / 1e3 / max(jac_launches, 1)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_per_launch / t_launch / 1e9 if t_launch > 0 else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "jacobi_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        from oracle.stepper import OracleSimulation
+
+        per, sample = cpu_oracle_estimate(OracleSimulation.from_simulation(sim0),
+                                          {"ws_iters": ws_iters, "lg": lg, "sites": sites, "pairs": pairs})
+        cpu = {"value": 1.0 / per, "unit": "FPS", "cores": 1, "kind": "port", "sample": sample}
+    line = {
+        "metric": METRIC, "value": value, "unit": "FPS", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dev_s / args.steps / len(sims), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": value / PAPER_FPS if args.workload == "skirt" else None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "n_vertices": int(sim0.mesh.vertex_count), "n_free": int(nf),
+                   "nnz_H": int(nnz), "h": 1.0 / 200.0, "r_bar": int(sim0.subspace.U.shape[1]),
+                   "r": int(sim0.subspace.r), "scenes_per_gpu": len(sims),
+                   "parallelism": f"replicas x{ws}" if args.workload != "batch" else f"scene-parallel {ws}",
+                   "l2": "inputs larger than L2: the 120-mode basis U (n_f*120*8 B) and pair arrays are "
+                         "streamed every step", "setup_s": round(setup_s, 1)},
+        "stages_ms_per_frame": stage, "lg_iterations_per_step": lg, "ccd_sites_per_step": sites,
+        "pairs_per_site_max": pairs,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "kernel": "k_jacobi_a/k_jacobi_b (A-Jacobi SELL-32 SpMV pass)",
+                     "bytes_per_launch": bytes_per_launch, "launch_us": t_launch * 1e6},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

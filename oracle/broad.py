@@ -7,8 +7,8 @@ returns, derived from its code rather than its tree walk:
   margin-inflated swept boxes overlap, and every vertex-disjoint edge pair
   whose swept boxes overlap, minus pairs whose primitives are both on static
   (obstacle) triangles (bvh.py:236, 253-281).  Swept boxes are fp64 min/max
-  of start/end positions -/+ margin (bvh.py:140-143, 242-246).  Found here by an
-  x-sorted slab sweep with exact box tests.
+  of start/end positions -/+ margin (bvh.py:140-143, 242-246).  Found here by a
+  uniform-grid hash join with exact box tests.
 * the ROW ORDER and edge-edge ORIENTATION: each row sits at the first position
   the reference's concatenated candidate list produces it (bvh.py:283-286).
   That position is a pure function of the static patch partition
@@ -91,32 +91,48 @@ class WorldTopology:
                    inv.reshape(-1).reshape(3, m).T.copy(), patch, slot)
 
 
-def _box_pairs(lo_a, hi_a, lo_b, hi_b, chunk=512):
-    """All (i, j) with closed boxes overlapping, by an x-sorted slab sweep."""
+def _cell_entries(lo, hi, origin, h, dims):
+    """(owner, cell key) for every grid cell a box touches."""
+    c0 = np.floor((lo - origin) / h).astype(np.int64)
+    c1 = np.floor((hi - origin) / h).astype(np.int64)
+    span = c1 - c0 + 1
+    cnt = span.prod(axis=1)
+    owner = np.repeat(np.arange(len(lo)), cnt)
+    local = np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    sx, sy = span[owner, 0], span[owner, 1]
+    cx = c0[owner, 0] + local % sx
+    cy = c0[owner, 1] + (local // sx) % sy
+    cz = c0[owner, 2] + local // (sx * sy)
+    return owner, (cx * dims[1] + cy) * dims[2] + cz
+
+
+def _box_pairs(lo_a, hi_a, lo_b, hi_b):
+    """All (i, j) with closed boxes overlapping: uniform-grid hash join + exact fp64 test.
+
+    Two boxes that overlap share at least one grid cell (cells are closed on
+    the low side, and floor() is monotone), so the join is a superset and the
+    exact test below makes it the exact set.
+    """
     if len(lo_a) == 0 or len(lo_b) == 0:
         return np.zeros(0, np.int64), np.zeros(0, np.int64)
-    ob = np.argsort(lo_b[:, 0], kind="stable")
-    sorted_lo = lo_b[ob, 0]
-    widest = float((hi_b[:, 0] - lo_b[:, 0]).max())
-    oa = np.argsort(lo_a[:, 0], kind="stable")
-    got_i, got_j = [], []
-    for s in range(0, len(oa), chunk):
-        ia = oa[s:s + chunk]
-        x_lo = float(lo_a[ia, 0].min())
-        x_hi = float(hi_a[ia, 0].max())
-        pad = 1e-9 * (1.0 + abs(x_lo) + widest)
-        j0 = np.searchsorted(sorted_lo, x_lo - widest - pad, side="left")
-        j1 = np.searchsorted(sorted_lo, x_hi, side="right")
-        jb = ob[j0:j1]
-        if jb.size == 0:
-            continue
-        hit = ((lo_a[ia, None, :] <= hi_b[None, jb, :]) & (lo_b[None, jb, :] <= hi_a[ia, None, :])).all(axis=2)
-        r, c = np.nonzero(hit)
-        got_i.append(ia[r])
-        got_j.append(jb[c])
-    if not got_i:
-        return np.zeros(0, np.int64), np.zeros(0, np.int64)
-    return np.concatenate(got_i), np.concatenate(got_j)
+    ext = np.concatenate([hi_a - lo_a, hi_b - lo_b])
+    h = max(float(np.percentile(ext.max(axis=1), 90)), 1e-12)
+    origin = np.minimum(lo_a.min(axis=0), lo_b.min(axis=0)) - h
+    top = np.maximum(hi_a.max(axis=0), hi_b.max(axis=0))
+    dims = (np.floor((top - origin) / h).astype(np.int64) + 2)
+    oa, ka = _cell_entries(lo_a, hi_a, origin, h, dims)
+    ob, kb = _cell_entries(lo_b, hi_b, origin, h, dims)
+    order = np.argsort(kb, kind="stable")
+    kb, ob = kb[order], ob[order]
+    left = np.searchsorted(kb, ka, side="left")
+    right = np.searchsorted(kb, ka, side="right")
+    cnt = right - left
+    ia = np.repeat(oa, cnt)
+    pos = np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt) + np.repeat(left, cnt)
+    ib = ob[pos]
+    hit = ((lo_a[ia] <= hi_b[ib]) & (lo_b[ib] <= hi_a[ia])).all(axis=1)
+    code = np.unique(ia[hit] * np.int64(len(lo_b)) + ib[hit])
+    return code // len(lo_b), code % len(lo_b)
 
 
 def _pair_place(pa, sa, pb, sb):

@@ -247,14 +247,12 @@ def capped_cylinder(radius: float, z_lo: float, z_hi: float, around: int = 48, r
     return v, np.concatenate([t, caps_top, caps_bot]).astype(np.int64)
 
 
-def skirt_scene(cfg: StepConfig, around: int = 584, down: int = 584, radius: float = 0.22, length: float = 0.6,
+def skirt_parts(around: int = 584, down: int = 584, radius: float = 0.22, length: float = 0.6,
                 body_radius: float = 0.20, spin: float = np.pi, sway: float = 0.03, sway_hz: float = 1.0,
-                density: float = 0.3, stretch_stiffness: float = 160.0, bend_stiffness: float = 3e-4, **kw):
-    """BASELINE config 4: procedural tube skirt (around x down vertices, ~341K at 584^2)
-    on a capped-cylinder body that spins about z at `spin` rad/s and sways along x.
-    The waist ring is pinned and follows the body's rigid motion (pin_motion)."""
-    from .stepper import Simulation
-
+                density: float = 0.3):
+    """BASELINE config 4 geometry: procedural tube skirt (around x down vertices, ~341K
+    at 584^2) on a capped-cylinder body that spins about z at `spin` rad/s and sways
+    along x.  The waist ring is pinned and follows the body's rigid motion."""
     top = 0.0
     verts, tris = tube(around, down, radius, radius * 1.35, length, top)
     pins = np.arange(around)
@@ -273,8 +271,20 @@ def skirt_scene(cfg: StepConfig, around: int = 584, down: int = 584, radius: flo
         out[:, 2] = points[:, 2]
         return out
 
-    return Simulation(mesh, cfg, stretch_stiffness, bend_stiffness, obstacles=[(body_v, body_t)],
-                      pin_motion=lambda t: rigid(rest_pins, t), obstacle_motion=lambda t: rigid(body_v, t), **kw)
+    return {"mesh": mesh, "obstacles": [(body_v, body_t)], "pin_motion": lambda t: rigid(rest_pins, t),
+            "obstacle_motion": lambda t: rigid(body_v, t)}
+
+
+def skirt_scene(cfg: StepConfig, density: float = 0.3, stretch_stiffness: float = 160.0,
+                bend_stiffness: float = 3e-4, **kw):
+    """BASELINE config 4 as a GPU Simulation (geometry: skirt_parts)."""
+    from .stepper import Simulation
+
+    geo = {k: kw.pop(k) for k in list(kw) if k in ("around", "down", "radius", "length", "body_radius", "spin",
+                                                    "sway", "sway_hz")}
+    parts = skirt_parts(density=density, **geo)
+    return Simulation(parts["mesh"], cfg, stretch_stiffness, bend_stiffness, obstacles=parts["obstacles"],
+                      pin_motion=parts["pin_motion"], obstacle_motion=parts["obstacle_motion"], **kw)
 
 
 # ------------------------------------------------------------------ config 5
