@@ -108,6 +108,32 @@ class OracleSimulation:
         self.last_outer_deltas = []
 
     @classmethod
+    def from_parts(cls, parts: dict, config):
+        """Build the scene on the host only (no GPU): mirrors the reference
+        constructor (stepper.py:127-173) using the product's setup modules."""
+        from paper_2403_19272_b200.constraints import assemble_global, build_elastic
+        from paper_2403_19272_b200.subspace import build_subspace
+
+        mesh = parts["mesh"]
+        el = build_elastic(mesh, parts["stretch"], parts["bend"])
+        sy = assemble_global(mesh, el, config.h)
+        r_bar = min(config.r_bar, mesh.free.size)
+        sub = build_subspace(sy, mesh.rest_positions[mesh.free], r_bar, min(config.r, r_bar))
+        n = mesh.vertex_count
+        verts, tris = [], [mesh.triangles]
+        off = n
+        for v, t in (parts.get("obstacles") or []):
+            verts.append(np.asarray(v, dtype=np.float64))
+            tris.append(np.asarray(t, dtype=np.int64) + off)
+            off += len(v)
+        wt = np.concatenate(tris)
+        stat = np.zeros(len(wt), dtype=bool)
+        stat[len(mesh.triangles):] = True
+        obs = np.concatenate(verts) if verts else np.zeros((0, 3))
+        k = config.ndb_k if config.ndb_k > 0 else el.mean_weight
+        return cls(mesh, config, el, sy, sub, k, obs, wt, stat, parts.get("pin_motion"), parts.get("obstacle_motion"))
+
+    @classmethod
     def from_simulation(cls, sim):
         """Clone the setup of a product Simulation (same arrays, host copies)."""
         o = cls(sim.mesh, sim.config, sim.elastic, sim.system, sim.subspace, sim.k, sim.obstacle_x,

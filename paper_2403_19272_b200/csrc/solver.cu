@@ -578,10 +578,11 @@ __global__ void k_sqdiff_partial(const double* __restrict__ a, const double* __r
     __shared__ double sm[256];
     double s = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        // ids given: both a and b are cloth-indexed arrays compared over free rows
         const int ia = ids_a ? ids_a[i] : i;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const double d = a[3 * ia + c] - (b ? b[3 * i + c] : 0.0);
+            const double d = a[3 * ia + c] - (b ? b[3 * ia + c] : 0.0);
             s = fma(d, d, s);
         }
     }

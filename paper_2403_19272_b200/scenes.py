@@ -136,6 +136,89 @@ def _twist_motion(rest_pins: np.ndarray, center: np.ndarray, rate: float, half: 
     return pin_motion
 
 
+def scene_parts(kind: str, resolution: int = 32, size: float = 1.0, density: float = 0.3,
+                stretch_stiffness: float = 160.0, bend_stiffness: float = 3e-4, config: StepConfig | None = None,
+                **kw) -> dict:
+    """Host-side scene description (mesh, obstacles, prescribed motions, material).
+
+    Reference kinds follow scenes.py:144-207; the rest are the BASELINE configs.
+    """
+    cfg = config if config is not None else StepConfig()
+    out = {"stretch": stretch_stiffness, "bend": bend_stiffness, "obstacles": None, "pin_motion": None,
+           "obstacle_motion": None}
+    if kind == "free_fall":
+        v, t = grid_cloth(resolution, size, height=1.0)
+        out["mesh"] = build_mesh(v, t, density, pins=[])
+    elif kind == "hanging":
+        v, t = grid_cloth(resolution, size, height=0.0)
+        out["mesh"] = build_mesh(v, t, density, pins=_rows(resolution, [0]))
+    elif kind == "sphere_drape":
+        radius = 0.25 * size
+        v, t = grid_cloth(resolution, size, height=radius + 2.0 * cfg.d_hat + 0.01 * size)
+        v[:, :2] -= size / 2.0
+        out["mesh"] = build_mesh(v, t, density, pins=[])
+        out["obstacles"] = [icosphere(3, radius, center=(0.0, 0.0, 0.0))]
+    elif kind == "desk_fold":
+        v, t = grid_cloth(resolution, size, height=0.25 * size)
+        v[:, :2] -= size / 2.0
+        out["mesh"] = build_mesh(v, t, density, pins=[])
+        out["obstacles"] = [
+            box_mesh(center=(0.0, 0.0, 0.1 * size), extents=(0.45 * size, 0.45 * size, 0.2 * size), divisions=6),
+            box_mesh(center=(0.0, 0.0, -0.05 * size), extents=(2.0 * size, 2.0 * size, 0.02 * size), divisions=4)]
+    elif kind == "twist":
+        v, t = grid_cloth(resolution, size, height=0.0)
+        pins = _rows(resolution, [0, resolution - 1])
+        out["mesh"] = build_mesh(v, t, density, pins=pins)
+        out["pin_motion"] = _twist_motion(v[pins], v.mean(axis=0), np.pi / 2.0, len(pins) // 2)
+    # ---------------- BASELINE configs (new; no reference generator exists)
+    elif kind == "two_corner":
+        v, t = grid_cloth(resolution, size)
+        out["mesh"] = build_mesh(v, t, density, pins=[0, resolution - 1])
+    elif kind == "sphere_ground":
+        radius = 0.25 * size
+        v, t = grid_cloth(resolution, size, height=radius + 2.0 * cfg.d_hat + 0.01 * size)
+        v[:, :2] -= size / 2.0
+        out["mesh"] = build_mesh(v, t, density, pins=[])
+        out["obstacles"] = [icosphere(3, radius),
+                            box_mesh(center=(0.0, 0.0, -(radius + 0.01 * size)),
+                                     extents=(2.0 * size, 2.0 * size, 0.02 * size), divisions=4)]
+    elif kind == "stacked_twist":
+        sheets = int(kw.pop("sheets", 2))
+        gap = float(kw.pop("gap", 0.005))
+        v1, t1 = grid_cloth(resolution, size)
+        vs, ts, rails = [], [], []
+        for sh in range(sheets):
+            v = v1.copy()
+            v[:, 2] += sh * gap
+            vs.append(v)
+            ts.append(t1 + sh * len(v1))
+            rails.append(_rows(resolution, [0, resolution - 1]) + sh * len(v1))
+        verts = np.concatenate(vs)
+        mesh = build_mesh(verts, np.concatenate(ts), density, pins=np.concatenate(rails))
+        # left rails of every sheet turn one way, right rails the other
+        left = np.concatenate([r[:resolution] for r in rails])
+        right = np.concatenate([r[resolution:] for r in rails])
+        order = np.concatenate([left, right])
+        pos = np.searchsorted(mesh.pinned, order)
+        base = _twist_motion(verts[order], verts.mean(axis=0), np.pi / 2.0, len(left))
+
+        def pin_motion(t: float) -> np.ndarray:
+            res = np.empty((len(order), 3))
+            res[pos] = base(t)
+            return res
+
+        out["mesh"] = mesh
+        out["pin_motion"] = pin_motion
+    elif kind == "skirt":
+        geo = {k: kw.pop(k) for k in list(kw) if k in ("around", "down", "radius", "length", "body_radius", "spin",
+                                                        "sway", "sway_hz")}
+        out.update(skirt_parts(density=density, **geo))
+    else:
+        raise ValueError(f"unknown scene kind {kind!r}")
+    out["extra"] = kw
+    return out
+
+
 def build_scene(kind: str, resolution: int = 32, size: float = 1.0, density: float = 0.3,
                 stretch_stiffness: float = 160.0, bend_stiffness: float = 3e-4, config: StepConfig | None = None,
                 **kw):
@@ -143,74 +226,9 @@ def build_scene(kind: str, resolution: int = 32, size: float = 1.0, density: flo
     from .stepper import Simulation
 
     cfg = config if config is not None else StepConfig()
-    mat = (stretch_stiffness, bend_stiffness)
-    if kind == "free_fall":
-        v, t = grid_cloth(resolution, size, height=1.0)
-        return Simulation(build_mesh(v, t, density, pins=[]), cfg, *mat, **kw)
-    if kind == "hanging":
-        v, t = grid_cloth(resolution, size, height=0.0)
-        return Simulation(build_mesh(v, t, density, pins=_rows(resolution, [0])), cfg, *mat, **kw)
-    if kind == "sphere_drape":
-        radius = 0.25 * size
-        v, t = grid_cloth(resolution, size, height=radius + 2.0 * cfg.d_hat + 0.01 * size)
-        v[:, :2] -= size / 2.0
-        sphere = icosphere(3, radius, center=(0.0, 0.0, 0.0))
-        return Simulation(build_mesh(v, t, density, pins=[]), cfg, *mat, obstacles=[sphere], **kw)
-    if kind == "desk_fold":
-        v, t = grid_cloth(resolution, size, height=0.25 * size)
-        v[:, :2] -= size / 2.0
-        desk = box_mesh(center=(0.0, 0.0, 0.1 * size), extents=(0.45 * size, 0.45 * size, 0.2 * size), divisions=6)
-        floor = box_mesh(center=(0.0, 0.0, -0.05 * size), extents=(2.0 * size, 2.0 * size, 0.02 * size), divisions=4)
-        return Simulation(build_mesh(v, t, density, pins=[]), cfg, *mat, obstacles=[desk, floor], **kw)
-    if kind == "twist":
-        v, t = grid_cloth(resolution, size, height=0.0)
-        pins = _rows(resolution, [0, resolution - 1])
-        mesh = build_mesh(v, t, density, pins=pins)
-        motion = _twist_motion(v[pins], v.mean(axis=0), np.pi / 2.0, len(pins) // 2)
-        return Simulation(mesh, cfg, *mat, pin_motion=motion, **kw)
-    # ---------------- BASELINE configs (new; no reference generator exists)
-    if kind == "two_corner":
-        v, t = grid_cloth(resolution, size)
-        return Simulation(build_mesh(v, t, density, pins=[0, resolution - 1]), cfg, *mat, **kw)
-    if kind == "sphere_ground":
-        radius = 0.25 * size
-        v, t = grid_cloth(resolution, size, height=radius + 2.0 * cfg.d_hat + 0.01 * size)
-        v[:, :2] -= size / 2.0
-        sphere = icosphere(3, radius)
-        ground = box_mesh(center=(0.0, 0.0, -(radius + 0.01 * size)), extents=(2.0 * size, 2.0 * size, 0.02 * size),
-                          divisions=4)
-        return Simulation(build_mesh(v, t, density, pins=[]), cfg, *mat, obstacles=[sphere, ground], **kw)
-    if kind == "stacked_twist":
-        sheets = int(kw.pop("sheets", 2))
-        gap = float(kw.pop("gap", 0.005))
-        v1, t1 = grid_cloth(resolution, size)
-        vs, ts, pins = [], [], []
-        for s in range(sheets):
-            v = v1.copy()
-            v[:, 2] += s * gap
-            vs.append(v)
-            ts.append(t1 + s * len(v1))
-            pins.append(_rows(resolution, [0, resolution - 1]) + s * len(v1))
-        verts = np.concatenate(vs)
-        pins = np.concatenate(pins)
-        mesh = build_mesh(verts, np.concatenate(ts), density, pins=pins)
-        # left rails of every sheet turn one way, right rails the other
-        left = np.concatenate([p[:resolution] for p in np.split(pins, sheets)])
-        right = np.concatenate([p[resolution:] for p in np.split(pins, sheets)])
-        order = np.concatenate([left, right])
-        pos = np.searchsorted(mesh.pinned, order)
-        base = _twist_motion(verts[order], verts.mean(axis=0), np.pi / 2.0, len(left))
-
-        def pin_motion(t: float) -> np.ndarray:
-            out = np.empty((len(order), 3))
-            out[pos] = base(t)
-            return out
-
-        return Simulation(mesh, cfg, *mat, pin_motion=pin_motion, **kw)
-    if kind == "skirt":
-        return skirt_scene(cfg, density=density, stretch_stiffness=stretch_stiffness,
-                           bend_stiffness=bend_stiffness, **kw)
-    raise ValueError(f"unknown scene kind {kind!r}")
+    p = scene_parts(kind, resolution, size, density, stretch_stiffness, bend_stiffness, cfg, **kw)
+    return Simulation(p["mesh"], cfg, p["stretch"], p["bend"], obstacles=p["obstacles"], pin_motion=p["pin_motion"],
+                      obstacle_motion=p["obstacle_motion"], **p["extra"])
 
 
 # ------------------------------------------------------------------ config 4
@@ -278,13 +296,8 @@ def skirt_parts(around: int = 584, down: int = 584, radius: float = 0.22, length
 def skirt_scene(cfg: StepConfig, density: float = 0.3, stretch_stiffness: float = 160.0,
                 bend_stiffness: float = 3e-4, **kw):
     """BASELINE config 4 as a GPU Simulation (geometry: skirt_parts)."""
-    from .stepper import Simulation
-
-    geo = {k: kw.pop(k) for k in list(kw) if k in ("around", "down", "radius", "length", "body_radius", "spin",
-                                                    "sway", "sway_hz")}
-    parts = skirt_parts(density=density, **geo)
-    return Simulation(parts["mesh"], cfg, stretch_stiffness, bend_stiffness, obstacles=parts["obstacles"],
-                      pin_motion=parts["pin_motion"], obstacle_motion=parts["obstacle_motion"], **kw)
+    return build_scene("skirt", density=density, stretch_stiffness=stretch_stiffness, bend_stiffness=bend_stiffness,
+                       config=cfg, **kw)
 
 
 # ------------------------------------------------------------------ config 5

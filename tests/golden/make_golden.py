@@ -1,0 +1,172 @@
+"""Generate golden fixtures by running the REAL reference (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The reference is imported read-only from /root/reference/pkg/src; its outputs
+are stored as compressed .npz next to this script.  Nothing at test time
+reads /root/reference.  Fixtures:
+
+  setup_<scene>.npz      mesh topology, masses, weights, H / H_fp, eigenbasis
+  narrow.npz             full_ccd / distance_toi / partial_ccd / pair_witness on
+                         random and near-contact pairs (+ single-pair batches)
+  broad_<k>.npz          broad_phase rows (kind, idx) in the reference's order
+  solver.npz             assemble_rhs / ajacobi_smooth / reduced_correction /
+                         warmstart_correction on a pinned system
+  traj_<scene>.npz       positions + report counters after every step
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.environ.get("CLOTHSIM_REF", "/root/reference/pkg/src"))
+
+import clothsim  # noqa: E402
+from clothsim.collision import (broad_phase, default_samples, distance_toi, full_ccd, pair_witness,  # noqa: E402
+                                partial_ccd, PatchBVH)
+from clothsim.constraints import assemble_rhs  # noqa: E402
+from clothsim.scenes import build_scene, grid_cloth, icosphere  # noqa: E402
+from clothsim.smoothing import ajacobi_smooth  # noqa: E402
+from clothsim.subspace import reduced_correction, warmstart_correction  # noqa: E402
+
+
+def save(name, **arrays):
+    np.savez_compressed(os.path.join(HERE, name), **arrays)
+    print("wrote", name, sum(a.nbytes for a in arrays.values()) // 1024, "KiB raw")
+
+
+def setup_fixture(tag, sim):
+    m, el, sy, sub = sim.mesh, sim.elastic, sim.system, sim.subspace
+    save(f"setup_{tag}.npz", rest=m.rest_positions, tris=m.triangles, edges=m.edges, rest_len=m.edge_rest_lengths,
+         stencils=m.bend_stencils, mass=m.vertex_mass, pinned=m.pinned, stretch_w=el.stretch_w, bend_k=el.bend_k,
+         bend_w=el.bend_w, H_data=sy.H.data, H_indices=sy.H.indices, H_indptr=sy.H.indptr, Hfp_data=sy.H_fp.data,
+         Hfp_indices=sy.H_fp.indices, Hfp_indptr=sy.H_fp.indptr, eigenvalues=sub.eigenvalues, U=sub.U,
+         k=np.array(sim.k), world_tris=sim.bvh.triangles, tri_static=sim.bvh.tri_static,
+         obstacle_x=sim.obstacle_x)
+
+
+def narrow_fixture():
+    rng = np.random.default_rng(7)
+    n = 3000
+    kind = np.zeros(n, dtype=np.int8)
+    kind[n // 2:] = 1
+    x0 = rng.uniform(-1.0, 1.0, size=(4 * n, 3))
+    x1 = x0 + rng.uniform(-1.0, 1.0, size=(4 * n, 3))
+    idx = np.arange(4 * n).reshape(n, 4)
+    # near-contact population: almost coplanar, slow, some static / in-plane
+    kn = (rng.random(n) < 0.5).astype(np.int8)
+    base = rng.normal(size=(n, 4, 3)) * 0.2
+    base[:, :, 2] *= 1e-3 * rng.random((n, 1))
+    move = rng.normal(size=(n, 4, 3)) * 0.01
+    move[rng.random(n) < 0.2] = 0.0
+    move[rng.random(n) < 0.2, :, 2] = 0.0
+    y0 = base.reshape(-1, 3)
+    y1 = (base + move).reshape(-1, 3)
+    out = dict(kind=kind, idx=idx, x0=x0, x1=x1, kind_n=kn, y0=y0, y1=y1)
+    out["toi"] = full_ccd(kind, idx, x0, x1)
+    out["toi_n"] = full_ccd(kn, idx, y0, y1)
+    for f in (0.2, 1.0 - 0.8):
+        out[f"dist_{f!r}"] = distance_toi(kind, idx, x0, x1, floor_frac=f)
+        out[f"dist_n_{f!r}"] = distance_toi(kn, idx, y0, y1, floor_frac=f)
+    for c in (1, 3, 6):
+        out[f"partial_{c}"] = partial_ccd(kind, idx, x0, x0 + 0.4 * (x1 - x0), default_samples(c))
+        out[f"partial_n_{c}"] = partial_ccd(kn, idx, y0, y1, default_samples(c))
+    p1, p2, bary, dist = pair_witness(kn, idx, y0)
+    out.update(w_p1=p1, w_p2=p2, w_bary=bary, w_dist=dist)
+    single = np.full(200, np.nan)
+    for i in range(200):
+        single[i] = full_ccd(kind[i:i + 1], np.array([[0, 1, 2, 3]]), x0[4 * i:4 * i + 4], x1[4 * i:4 * i + 4])[0]
+    out["toi_single"] = single
+    save("narrow.npz", **out)
+
+
+def broad_fixtures():
+    rng = np.random.default_rng(11)
+    cases = [(6, False, 0.08, 0.15, 0.01), (12, True, 0.02, 0.05, 0.01), (20, True, 0.004, 0.01, 1e-3),
+             (33, False, 0.002, 0.004, 1e-3)]
+    for k, (res, obst, jit, mv, margin) in enumerate(cases):
+        v, t = grid_cloth(res, 1.0)
+        if obst:
+            sv, st = icosphere(2, 0.3, center=(0.5, 0.5, -0.05))
+            wt = np.concatenate([t, st + len(v)])
+            wr = np.concatenate([v, sv])
+            stat = np.zeros(len(wt), bool)
+            stat[len(t):] = True
+        else:
+            wt, wr, stat = t, v, np.zeros(len(t), bool)
+        x0 = wr + jit * rng.normal(size=wr.shape)
+        x1 = x0 + mv * rng.normal(size=wr.shape)
+        ps = broad_phase(x0, x1, PatchBVH.build(wt, wr, stat), margin)
+        save(f"broad_{k}.npz", tris=wt, tri_static=stat, x0=x0, x1=x1, margin=np.array(margin), kind=ps.kind,
+             idx=ps.idx)
+
+
+def solver_fixture():
+    rng = np.random.default_rng(13)
+    sim = build_scene("twist", resolution=16, size=0.5, config=clothsim.StepConfig(h=1.0 / 200.0))
+    m, el, sy, sub = sim.mesh, sim.elastic, sim.system, sim.subspace
+    n, nf = m.vertex_count, m.free.size
+    x = m.rest_positions + 0.01 * rng.normal(size=(n, 3))
+    z = m.rest_positions + 0.01 * rng.normal(size=(n, 3))
+    pins = x[m.pinned]
+    ids = rng.integers(0, n, size=300)
+    w = rng.uniform(1.0, 1e4, size=300)
+    tg = rng.normal(size=(300, 3))
+    b0, d0 = assemble_rhs(sy, m, el, z, x, pins)
+    b1, d1 = assemble_rhs(sy, m, el, z, x, pins, collision_vertices=ids, collision_weights=w, collision_targets=tg)
+    bb = rng.normal(size=(nf, 3))
+    xx = rng.normal(size=(nf, 3))
+    dl = np.where(rng.random(nf) < 0.1, rng.uniform(0, 50, nf), 0.0)
+    sm = ajacobi_smooth(sy, bb, xx, 32, 0.0, dl)
+    rc0, _ = reduced_correction(sub, sy, bb, xx, np.zeros(nf))
+    rc1, _ = reduced_correction(sub, sy, bb, xx, dl)
+    big = np.zeros(nf)
+    big[rng.choice(nf, 20, replace=False)] = 2.0 ** 60
+    rc2, red2 = reduced_correction(sub, sy, bb, xx, big)
+    ws = warmstart_correction(sub, sy, bb, xx)
+    save("solver.npz", x=x, z=z, pins=pins, ids=ids, w=w, tg=tg, b0=b0, d0=d0, b1=b1, d1=d1, bb=bb, xx=xx, dl=dl,
+         smooth=sm, rc0=rc0, rc1=rc1, big=big, rc2=rc2, rc2_fallback=np.array(red2.used_fallback), ws=ws)
+    setup_fixture("twist16", sim)
+
+
+def traj_fixture(tag, kind, steps, cfg_kw, **scene_kw):
+    sim = build_scene(kind, config=clothsim.StepConfig(**cfg_kw), **scene_kw)
+    if tag in ("hanging10", "sphere14"):
+        setup_fixture(tag, sim)
+    xs, lg, rf, outer, toi = [], [], [], [], []
+    for _ in range(steps):
+        r = sim.step()
+        xs.append(sim.state.x.copy())
+        lg.append(r.lg_iterations)
+        rf.append(r.rf_triggered)
+        outer.append(r.outer_loops)
+        toi.append(r.toi_exit)
+    save(f"traj_{tag}.npz", x=np.stack(xs), lg=np.array(lg), rf=np.array(rf), outer=np.array(outer),
+         toi=np.array(toi), obstacle_x=sim.obstacle_x)
+
+
+def two_corner_fixture(steps=3):
+    """BASELINE config 1: 64x64 grid pinned at two corners, h = 1/200."""
+    v, t = grid_cloth(64, 1.0)
+    mesh = clothsim.build_mesh(v, t, 0.3, pins=[0, 63])
+    sim = clothsim.Simulation(mesh, clothsim.StepConfig(h=1.0 / 200.0))
+    xs, lg = [], []
+    for _ in range(steps):
+        r = sim.step()
+        xs.append(sim.state.x.copy())
+        lg.append(r.lg_iterations)
+    save("traj_two_corner64.npz", x=np.stack(xs), lg=np.array(lg))
+
+
+if __name__ == "__main__":
+    narrow_fixture()
+    broad_fixtures()
+    solver_fixture()
+    traj_fixture("hanging10", "hanging", 6, dict(h=1.0 / 200.0), resolution=10)
+    traj_fixture("sphere14", "sphere_drape", 12, {}, resolution=14, size=0.2)
+    traj_fixture("twist10", "twist", 6, {}, resolution=10, size=0.3)
+    two_corner_fixture()

@@ -23,10 +23,16 @@ def sim(cuda):
     return P.build_scene("twist", resolution=24, size=0.5, config=cfg)
 
 
+_KEEP = []
+
+
 def _dev(a, dtype=None):
+    """Device copy kept alive for the whole module (raw pointers go to the C ABI)."""
     import torch
 
-    return torch.as_tensor(np.ascontiguousarray(a), device="cuda", dtype=dtype)
+    t = torch.as_tensor(np.ascontiguousarray(a), device="cuda", dtype=dtype)
+    _KEEP.append(t)
+    return t
 
 
 def _stamps(sim, rng, count):
