@@ -70,9 +70,6 @@ typedef struct {
     const uint8_t *tri_static, *vert_static, *vert_used, *edge_static;
     const int *edge_tris, *edge_slot;   /* (n_world_edges*2) */
     const int *patch, *patch_slot;      /* (n_world_tris) reference build_patches partition */
-    /* static-topology trees (Morton order of rest pose) */
-    const int *tri_left, *tri_right, *tri_parent, *tri_leaf_parent, *tri_prim;
-    const int *edge_left, *edge_right, *edge_parent, *edge_leaf_parent, *edge_prim;
     /* initial state */
     const double *x0;           /* (n_cloth*3) */
     const double *obstacle_x0;  /* (n_obstacle*3) */

@@ -36,10 +36,6 @@ class SceneDesc(ctypes.Structure):
         ("world_tris", c_int_p), ("world_edges", c_int_p),
         ("tri_static", c_u8_p), ("vert_static", c_u8_p), ("vert_used", c_u8_p), ("edge_static", c_u8_p),
         ("edge_tris", c_int_p), ("edge_slot", c_int_p), ("patch", c_int_p), ("patch_slot", c_int_p),
-        ("tri_left", c_int_p), ("tri_right", c_int_p), ("tri_parent", c_int_p), ("tri_leaf_parent", c_int_p),
-        ("tri_prim", c_int_p),
-        ("edge_left", c_int_p), ("edge_right", c_int_p), ("edge_parent", c_int_p), ("edge_leaf_parent", c_int_p),
-        ("edge_prim", c_int_p),
         ("x0", c_dbl_p), ("obstacle_x0", c_dbl_p),
     ]
 

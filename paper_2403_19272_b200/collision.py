@@ -7,8 +7,8 @@ results back, so reference callers and tests can be re-pointed unchanged.
 
 Static setup pieces live here too: the reference's patch partition
 (``build_patches``, reference bvh.py:20-51 - needed to reproduce the
-reference's edge-edge row orientation) and the world topology + static
-Morton-order trees the device broad phase refits each query.
+reference's edge-edge row orientation) and the static world topology the device
+broad phase (a per-query hash grid, csrc/broad.cu) enumerates.
 """
 
 from __future__ import annotations
@@ -270,69 +270,13 @@ def build_patches(triangles: np.ndarray, n_vertices: int = 0) -> list:
     return groups
 
 
-def _spread_bits(v: np.ndarray) -> np.ndarray:
-    v = v.astype(np.uint64) & np.uint64(0x3FF)
-    v = (v | (v << np.uint64(16))) & np.uint64(0x030000FF)
-    v = (v | (v << np.uint64(8))) & np.uint64(0x0300F00F)
-    v = (v | (v << np.uint64(4))) & np.uint64(0x030C30C3)
-    v = (v | (v << np.uint64(2))) & np.uint64(0x09249249)
-    return v
-
-
-def morton_tree(centroids: np.ndarray):
-    """Balanced binary tree over Morton-sorted primitives (built once, refit per query).
-
-    Returns int32 arrays (left, right, parent, leaf_parent, prim); child codes
-    >= 0 are internal nodes, < 0 encode leaf position ~pos.
-    """
-    L = len(centroids)
-    lo = centroids.min(axis=0)
-    span = np.maximum(centroids.max(axis=0) - lo, 1e-30)
-    q = np.clip(((centroids - lo) / span * 1023.0).astype(np.int64), 0, 1023)
-    code = (_spread_bits(q[:, 0]) << np.uint64(2)) | (_spread_bits(q[:, 1]) << np.uint64(1)) | _spread_bits(q[:, 2])
-    prim = np.lexsort((np.arange(L), code)).astype(np.int32)
-    ni = max(L - 1, 1)
-    left = np.full(ni, -1, np.int32)
-    right = np.full(ni, -1, np.int32)
-    parent = np.full(ni, -1, np.int32)
-    leaf_parent = np.full(L, -1, np.int32)
-    if L == 1:
-        return left, right, parent, leaf_parent, prim
-    ids, lo_r, hi_r = np.array([0]), np.array([0]), np.array([L])
-    nxt = 1
-    while ids.size:
-        mid = (lo_r + hi_r) // 2
-        child_ids = []
-        new_ids, new_lo, new_hi = [], [], []
-        for side, (a, b) in enumerate(((lo_r, mid), (mid, hi_r))):
-            size = b - a
-            leaf = size == 1
-            code_arr = np.empty(ids.size, np.int64)
-            code_arr[leaf] = ~a[leaf]
-            leaf_parent[a[leaf]] = ids[leaf]
-            k = int((~leaf).sum())
-            fresh = np.arange(nxt, nxt + k)
-            nxt += k
-            code_arr[~leaf] = fresh
-            parent[fresh] = ids[~leaf]
-            new_ids.append(fresh)
-            new_lo.append(a[~leaf])
-            new_hi.append(b[~leaf])
-            child_ids.append(code_arr)
-        left[ids] = child_ids[0]
-        right[ids] = child_ids[1]
-        ids = np.concatenate(new_ids)
-        lo_r = np.concatenate(new_lo)
-        hi_r = np.concatenate(new_hi)
-    return left, right, parent, leaf_parent, prim
-
-
 @dataclass
 class CollisionWorld:
     """Static world topology (cloth first, then obstacles) for the device broad phase.
 
     Plays the role of the reference's PatchBVH (bvh.py:54-137): fixed topology
-    from the rest pose, boxes refit per query.  ``triangles``/``tri_static``
+    from the rest pose (``rest_positions`` kept for signature parity); the
+    device rebuilds its hash grid from the query boxes every call.  ``triangles``/``tri_static``
     keep the reference attribute names.
     """
 
@@ -348,8 +292,6 @@ class CollisionWorld:
     vert_static: np.ndarray
     vert_used: np.ndarray
     edge_static: np.ndarray
-    tri_tree: tuple
-    edge_tree: tuple
 
     @classmethod
     def build(cls, triangles, rest_positions, tri_static=None) -> "CollisionWorld":
@@ -386,8 +328,5 @@ class CollisionWorld:
         vstat[tris[~stat].ravel()] = False
         estat = np.zeros(len(edges), bool)
         estat[tri_edges[stat].ravel()] = True
-        rest = np.asarray(rest_positions, dtype=np.float64)
-        tri_tree = morton_tree(rest[tris].mean(axis=1))
-        edge_tree = morton_tree(rest[edges].mean(axis=1))
         return cls(tris, stat, edges, tri_edges, patches, patch_of, slot_of, edge_tris, edge_slot, vstat, used,
-                   estat, tri_tree, edge_tree)
+                   estat)

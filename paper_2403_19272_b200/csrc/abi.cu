@@ -48,8 +48,10 @@ struct DBuf {
         if (m <= n && p) return 0;
         if (p) cudaFree(p);
         p = nullptr;
+        // regrowth reserves 2x: per-step sizes (pairs, grid entries) drift and
+        // every cudaFree/cudaMalloc of a large buffer stalls the stream
         size_t want = std::max<size_t>(m, 1);
-        if (n) want = std::max(want, n + n / 2);
+        if (n) want = std::max(2 * want, n + n / 2);
         cudaError_t e = cudaMalloc(&p, want * sizeof(T));
         if (e != cudaSuccess) {
             n = 0;
@@ -74,39 +76,47 @@ struct DBuf {
     }
 };
 
-struct TreeBuf {
-    int nleaf = 0;
-    DBuf<int> left, right, parent, leaf_parent, prim, flags;
-    DBuf<double> node_lo, node_hi, leaf_lo, leaf_hi;
-    int create(int nl, const int* l, const int* r, const int* par, const int* lpar, const int* pr) {
-        nleaf = nl;
-        const int ni = std::max(nl - 1, 1);
-        CS_RET(left.upload(l, nl - 1));
-        CS_RET(right.upload(r, nl - 1));
-        CS_RET(parent.upload(par, nl - 1));
-        CS_RET(leaf_parent.upload(lpar, nl));
-        CS_RET(prim.upload(pr, nl));
-        CS_RET(flags.ensure(ni));
-        CS_RET(node_lo.ensure(3 * (size_t)ni));
-        CS_RET(node_hi.ensure(3 * (size_t)ni));
-        CS_RET(leaf_lo.ensure(3 * (size_t)nl));
-        CS_RET(leaf_hi.ensure(3 * (size_t)nl));
+// one hash-grid entry table (vertices, triangles or edges) of the broad phase
+struct EntryBuf {
+    int np = 0;
+    unsigned T = 0;  // buckets (power of two)
+    int log2T = 0;
+    long long m = 0;  // entries
+    int n_over_h = 0;
+    DBuf<double> box, part, inv;
+    DBuf<int> count, offset, prim, perm, perm_s, prim_s, run, n_run, bstart, bend, over, n_over, pcount, poffset;
+    DBuf<unsigned> key, key_s;
+    DBuf<unsigned long long> code, code_s;
+    DBuf<uint8_t> is_over, head;
+    int create(int n_prim, bool has_box) {
+        np = n_prim;
+        if (has_box) CS_RET(box.ensure(6LL * np));
+        CS_RET(inv.ensure(1));
+        CS_RET(count.ensure(np + 1));
+        CS_RET(offset.ensure(np + 1));
+        CS_RET(over.ensure(np));
+        CS_RET(n_over.ensure(1));
+        CS_RET(n_run.ensure(1));
+        CS_RET(is_over.ensure(np));
         return 0;
     }
-    Tree view() {
-        Tree t;
-        t.nleaf = nleaf;
-        t.left = left.p;
-        t.right = right.p;
-        t.parent = parent.p;
-        t.leaf_parent = leaf_parent.p;
-        t.prim = prim.p;
-        t.node_lo = node_lo.p;
-        t.node_hi = node_hi.p;
-        t.leaf_lo = leaf_lo.p;
-        t.leaf_hi = leaf_hi.p;
-        t.flags = flags.p;
-        return t;
+    void set_buckets(long long want) {
+        T = 1024;
+        log2T = 10;
+        while ((long long)T < want) {
+            T <<= 1;
+            ++log2T;
+        }
+    }
+    EntryTable view() const {
+        return EntryTable{key_s.p, prim_s.p, code_s.p, run.p, n_run.p, bstart.p, bend.p, (int)m};
+    }
+    void release() {
+        for (DBuf<int>* b : {&count, &offset, &prim, &perm, &perm_s, &prim_s, &run, &n_run, &bstart, &bend, &over,
+                             &n_over, &pcount, &poffset})
+            b->release();
+        box.release(); part.release(); inv.release(); key.release(); key_s.release(); code.release();
+        code_s.release(); is_over.release(); head.release();
     }
 };
 
@@ -119,6 +129,9 @@ struct PairBuf {
     DBuf<int> life;
     DBuf<uint8_t> engaged;
     int reserve(long long m) {
+        // first real sizing (from the 1024-row placeholder) takes 3x headroom: pair
+        // counts drift upward while cloth settles and a regrowth stalls the stream
+        if (kind.n <= 1024 && m > 1024) m *= 3;
         CS_RET(kind.ensure(m));
         CS_RET(idx.ensure(m));
         CS_RET(keys.ensure(m));
@@ -141,7 +154,7 @@ struct PairBuf {
 // scalar slots (doubles) read back in one D2H copy
 enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_NORM1 = 5, S_NORM_F = 6,
        S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_COUNT = 16 };
-enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_COUNT = 8 };
+enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_COUNT = 8 };
 
 const int kStages = 8;
 enum { T_WARM = 0, T_LOCAL, T_GLOBAL, T_SMOOTH, T_BROAD, T_PARTIAL, T_FULL, T_RF };
@@ -166,7 +179,9 @@ struct cs_scene {
     // world topology
     DBuf<int> wtris, wedges, edge_tris, edge_slot, patch, pslot;
     DBuf<uint8_t> tri_static, vert_static, vert_used, edge_static;
-    TreeBuf ttree, etree;
+    DBuf<ulonglong2> eflip;
+    EntryBuf vtab, ttab, etab;
+    DBuf<int> ocount, ooffset;
     // state
     DBuf<double> x, v, xprev, df, obs;
     int step_index = 0;
@@ -174,7 +189,6 @@ struct cs_scene {
     DBuf<double> z, xs_w, xc_w, anchor_w, tmp_w, xf, xf0, b, t, delta, prev_outer, grad, fr;
     DBuf<double> pins_next_d, obs_next_d;
     DBuf<double> vlo, vhi;
-    DBuf<int> counts, offsets;
     PairBuf pa, pb;  // current and next pair sets
     PairBuf* cur = &pa;
     PairBuf* nxt = &pb;
@@ -184,7 +198,6 @@ struct cs_scene {
     DBuf<int> hvals;
     DBuf<double> part, part2, rhs_red, gram_red, q, Xred, beta_red, norms;
     int pending_checks = 0;
-    DBuf<int> counts2, offsets2;
     DBuf<int> fallback;
     DBuf<char> cub_tmp;
     DBuf<double> d_scal;
@@ -347,6 +360,7 @@ struct cs_scene {
         w.edge_slot = edge_slot.p;
         w.patch = patch.p;
         w.pslot = pslot.p;
+        w.flip = eflip.p;
         return w;
     }
 
@@ -358,35 +372,174 @@ struct cs_scene {
         return 0;
     }
 
-    // broad phase into pr (bvh.py:207-292): count -> scan -> write, one host sync
+    // hash-grid table stage 1: per-primitive cell counts, scan, oversize list
+    int table_count(EntryBuf& G, BoxSrc src, const double* inv) {
+        k_cell_count<<<grid(G.np), 256, 0, s>>>(src, inv, G.count.p, G.is_over.p);
+        ++launches;
+        CS_CHECK_LAUNCH();
+        CS_TRY(cudaMemsetAsync(G.count.p + G.np, 0, sizeof(int), s));
+        CS_RET(scan(G.count.p, G.offset.p, G.np + 1));
+        size_t bytes = 0;
+        cub::CountingInputIterator<int> it(0);
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, G.is_over.p, G.over.p, G.n_over.p, G.np, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, G.is_over.p, G.over.p, G.n_over.p, G.np, s));
+        return 0;
+    }
+    // stage 2 (entry count m known on host): fill, stable radix sort by bucket,
+    // sorted (primitive, code) arrays, run heads (+ dense bucket ranges if dense)
+    int table_build(EntryBuf& G, BoxSrc src, const double* inv, bool dense) {
+        const long long m = G.m;
+        CS_RET(G.run.ensure(std::max<long long>(m, 1)));
+        CS_TRY(cudaMemsetAsync(G.n_run.p, 0, sizeof(int), s));
+        if (dense) {
+            CS_RET(G.bstart.ensure(G.T));
+            CS_RET(G.bend.ensure(G.T));
+            CS_TRY(cudaMemsetAsync(G.bstart.p, 0, sizeof(int) * G.T, s));
+            CS_TRY(cudaMemsetAsync(G.bend.p, 0, sizeof(int) * G.T, s));
+        }
+        if (m == 0) return 0;
+        CS_RET(G.key.ensure(m));
+        CS_RET(G.key_s.ensure(m));
+        CS_RET(G.prim.ensure(m));
+        CS_RET(G.prim_s.ensure(m));
+        CS_RET(G.perm.ensure(m));
+        CS_RET(G.perm_s.ensure(m));
+        CS_RET(G.code.ensure(m));
+        CS_RET(G.code_s.ensure(m));
+        CS_RET(G.head.ensure(m));
+        k_cell_fill<<<grid(8LL * G.np), 256, 0, s>>>(src, inv, G.T - 1, G.count.p, G.offset.p, G.key.p, G.prim.p,
+                                               G.code.p);
+        k_iota<<<grid(m), 256, 0, s>>>(G.perm.p, m);
+        launches += 2;
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, G.key.p, G.key_s.p, G.perm.p, G.perm_s.p, (int)m, 0, G.log2T,
+                                        s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, G.key.p, G.key_s.p, G.perm.p, G.perm_s.p, (int)m, 0,
+                                               G.log2T, s));
+        k_entries_sorted<<<grid(m), 256, 0, s>>>(G.perm_s.p, (int)m, G.prim.p, G.code.p, G.key_s.p, G.prim_s.p,
+                                                 G.code_s.p, G.head.p, dense ? G.bstart.p : nullptr,
+                                                 dense ? G.bend.p : nullptr);
+        ++launches;
+        bytes = 0;
+        cub::CountingInputIterator<int> it(0);
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, G.head.p, G.run.p, G.n_run.p, (int)m, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, G.head.p, G.run.p, G.n_run.p, (int)m, s));
+        CS_CHECK_LAUNCH();
+        return 0;
+    }
+    int run_blocks(long long m) {
+        return (int)std::max<long long>(1, std::min<long long>((m + kPairWarps - 1) / kPairWarps, 32LL * sm_count));
+    }
+
+    // broad phase into pr (bvh.py:207-292): entry tables -> bucket-pair count -> scan -> write; two host syncs
     int broad_phase(const double* xa, const double* xb, double margin, PairBuf& pr) {
         k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(xa, xb, nw, margin, vlo.p, vhi.p);
-        CS_TRY(cudaMemsetAsync(ttree.flags.p, 0, sizeof(int) * std::max(ttree.nleaf - 1, 1), s));
-        CS_TRY(cudaMemsetAsync(etree.flags.p, 0, sizeof(int) * std::max(etree.nleaf - 1, 1), s));
-        k_refit<<<grid(ttree.nleaf), 256, 0, s>>>(ttree.view(), wtris.p, 3, vlo.p, vhi.p);
-        k_refit<<<grid(etree.nleaf), 256, 0, s>>>(etree.view(), wedges.p, 2, vlo.p, vhi.p);
-        CS_TRY(cudaMemsetAsync(counts.p + nw, 0, sizeof(int), s));
-        CS_TRY(cudaMemsetAsync(counts2.p + new_, 0, sizeof(int), s));
-        k_query_vt<0><<<grid(nw, 128), 128, 0, s>>>(ttree.view(), world(), vlo.p, vhi.p, counts.p, nullptr,
-                                                      nullptr, nullptr, nullptr);
-        k_query_ee<0><<<grid(new_, 128), 128, 0, s>>>(etree.view(), world(), new_, vlo.p, vhi.p, counts2.p,
-                                                        nullptr, nullptr, nullptr, nullptr);
+        const int gt = grid(ntw), ge = grid(new_);
+        CS_RET(ttab.part.ensure(4LL * gt));
+        CS_RET(etab.part.ensure(4LL * ge));
+        k_prim_boxes<3><<<gt, 256, 0, s>>>(wtris.p, ntw, tri_static.p, vlo.p, vhi.p, ttab.box.p, ttab.part.p);
+        k_cell_size<<<1, 256, 0, s>>>(ttab.part.p, gt, ttab.inv.p);
+        k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, etab.box.p, etab.part.p);
+        k_cell_size<<<1, 256, 0, s>>>(etab.part.p, ge, etab.inv.p);
         launches += 5;
-        CS_CHECK_LAUNCH();
-        CS_RET(scan(counts.p, offsets.p, nw + 1));
-        CS_RET(scan(counts2.p, offsets2.p, new_ + 1));
-        CS_TRY(cudaMemcpyAsync(&h_iscal[I_VT], offsets.p + nw, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaMemcpyAsync(&h_iscal[I_EE], offsets2.p + new_, sizeof(int), cudaMemcpyDeviceToHost, s));
+        const BoxSrc vs{nullptr, vlo.p, vhi.p, vert_used.p, nw};
+        const BoxSrc ts{ttab.box.p, nullptr, nullptr, nullptr, ntw};
+        const BoxSrc es{etab.box.p, nullptr, nullptr, nullptr, new_};
+        CS_RET(table_count(vtab, vs, ttab.inv.p));
+        CS_RET(table_count(ttab, ts, ttab.inv.p));
+        CS_RET(table_count(etab, es, etab.inv.p));
+        EntryBuf* tabs[3] = {&vtab, &ttab, &etab};
+        for (int k = 0; k < 3; ++k) {
+            CS_TRY(cudaMemcpyAsync(&h_iscal[8 + k], tabs[k]->offset.p + tabs[k]->np, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CS_TRY(cudaMemcpyAsync(&h_iscal[12 + k], tabs[k]->n_over.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        }
         CS_TRY(cudaStreamSynchronize(s));
-        const long long n_vt = h_iscal[I_VT], n_ee = h_iscal[I_EE];
-        const long long P = n_vt + n_ee;
+        for (int k = 0; k < 3; ++k) {
+            tabs[k]->m = h_iscal[8 + k];
+            tabs[k]->n_over_h = h_iscal[12 + k];
+        }
+        vtab.set_buckets(std::max(vtab.m, ttab.m));
+        ttab.T = vtab.T;
+        ttab.log2T = vtab.log2T;
+        etab.set_buckets(etab.m);
+        CS_RET(table_build(vtab, vs, ttab.inv.p, false));
+        CS_RET(table_build(ttab, ts, ttab.inv.p, true));
+        CS_RET(table_build(etab, es, etab.inv.p, false));
+        // pair counts: [VT runs][VT oversize][EE runs][EE oversize]
+        const int n_ovt = vtab.n_over_h + ttab.n_over_h, n_oee = etab.n_over_h;
+        for (EntryBuf* G : {&vtab, &etab}) {
+            CS_RET(G->pcount.ensure(G->m + 1));
+            CS_RET(G->poffset.ensure(G->m + 1));
+            CS_TRY(cudaMemsetAsync(G->pcount.p, 0, sizeof(int) * (G->m + 1), s));
+        }
+        CS_RET(ocount.ensure(n_ovt + n_oee + 2));
+        CS_RET(ooffset.ensure(n_ovt + n_oee + 2));
+        CS_TRY(cudaMemsetAsync(ocount.p, 0, sizeof(int) * (n_ovt + n_oee + 2), s));
+        int* oc_vt = ocount.p;
+        int* oc_ee = ocount.p + n_ovt + 1;
+        int* oo_vt = ooffset.p;
+        int* oo_ee = ooffset.p + n_ovt + 1;
+        const WorldTopo W = world();
+        const EntryTable VT = vtab.view(), TT = ttab.view(), ET = etab.view();
+        PairOut O{};
+        if (vtab.m) {
+            O.counts = vtab.pcount.p;
+            k_pairs_vt<0><<<run_blocks(vtab.m), 32 * kPairWarps, 0, s>>>(VT, TT, vlo.p, vhi.p, ttab.box.p, ttab.inv.p, W, O);
+            ++launches;
+        }
+        if (n_ovt) {
+            O.counts = oc_vt;
+            k_over_vt<0><<<grid(n_ovt, 64), 64, 0, s>>>(vtab.over.p, vtab.n_over_h, ttab.over.p, ttab.n_over_h,
+                                                         vtab.is_over.p, vlo.p, vhi.p, ttab.box.p, ntw, W, O);
+            ++launches;
+        }
+        if (etab.m) {
+            O.counts = etab.pcount.p;
+            k_pairs_ee<0><<<run_blocks(etab.m), 32 * kPairWarps, 0, s>>>(ET, etab.box.p, etab.inv.p, W, O);
+            ++launches;
+        }
+        if (n_oee) {
+            O.counts = oc_ee;
+            k_over_ee<0><<<grid(n_oee, 64), 64, 0, s>>>(etab.over.p, n_oee, etab.is_over.p, etab.box.p, new_, W, O);
+            ++launches;
+        }
+        CS_CHECK_LAUNCH();
+        CS_RET(scan(vtab.pcount.p, vtab.poffset.p, (int)vtab.m + 1));
+        CS_RET(scan(oc_vt, oo_vt, n_ovt + 1));
+        CS_RET(scan(etab.pcount.p, etab.poffset.p, (int)etab.m + 1));
+        CS_RET(scan(oc_ee, oo_ee, n_oee + 1));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[8], vtab.poffset.p + vtab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[9], oo_vt + n_ovt, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[10], etab.poffset.p + etab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[11], oo_ee + n_oee, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        const long long c0 = h_iscal[8], c1 = h_iscal[9], c2 = h_iscal[10], c3 = h_iscal[11];
+        const long long P = c0 + c1 + c2 + c3;
         CS_RET(pr.reserve(std::max<long long>(P, 1)));
-        k_query_vt<1><<<grid(nw, 128), 128, 0, s>>>(ttree.view(), world(), vlo.p, vhi.p, nullptr, offsets.p,
-                                                      pr.kind.p, pr.idx.p, pr.keys.p);
-        k_query_ee<1><<<grid(new_, 128), 128, 0, s>>>(etree.view(), world(), new_, vlo.p, vhi.p, nullptr,
-                                                        offsets2.p, pr.kind.p + n_vt, pr.idx.p + n_vt,
-                                                        pr.keys.p + n_vt);
-        launches += 2;
+        auto out_at = [&](long long base, const int* offs) {
+            return PairOut{nullptr, offs, pr.kind.p + base, pr.idx.p + base, pr.keys.p + base};
+        };
+        if (vtab.m && c0)
+            k_pairs_vt<1><<<run_blocks(vtab.m), 32 * kPairWarps, 0, s>>>(VT, TT, vlo.p, vhi.p, ttab.box.p, ttab.inv.p, W,
+                                                             out_at(0, vtab.poffset.p));
+        if (n_ovt && c1)
+            k_over_vt<1><<<grid(n_ovt, 64), 64, 0, s>>>(vtab.over.p, vtab.n_over_h, ttab.over.p, ttab.n_over_h,
+                                                         vtab.is_over.p, vlo.p, vhi.p, ttab.box.p, ntw, W,
+                                                         out_at(c0, oo_vt));
+        if (etab.m && c2)
+            k_pairs_ee<1><<<run_blocks(etab.m), 32 * kPairWarps, 0, s>>>(ET, etab.box.p, etab.inv.p, W,
+                                                             out_at(c0 + c1, etab.poffset.p));
+        if (n_oee && c3)
+            k_over_ee<1><<<grid(n_oee, 64), 64, 0, s>>>(etab.over.p, n_oee, etab.is_over.p, etab.box.p, new_, W,
+                                                        out_at(c0 + c1 + c2, oo_ee));
+        launches += 4;
+        if (c2 + c3) {
+            k_ee_orient<<<grid(c2 + c3), 256, 0, s>>>(pr.keys.p + c0 + c1, pr.idx.p + c0 + c1, c2 + c3, W);
+            ++launches;
+        }
         CS_CHECK_LAUNCH();
         pr.P = P;
         return 0;
@@ -443,13 +596,22 @@ struct cs_scene {
         return 0;
     }
 
-    // life-span carry old -> new (stepper.py:300-305)
+    // life-span carry old -> new (stepper.py:300-305).  Only pairs with a nonzero
+    // life span can carry anything, so the hash table holds just those (one
+    // extra 4-byte read-back sizes it; nothing to do when no pair is alive).
     int carry(PairBuf& old, PairBuf& nw_) {
         if (nw_.P == 0) return 0;
         CS_TRY(cudaMemsetAsync(nw_.life.p, 0, sizeof(int) * nw_.P, s));
         if (old.P == 0) return 0;
-        unsigned long long cap = 1;
-        while (cap < 2ull * (unsigned long long)old.P) cap <<= 1;
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_LIVE, 0, sizeof(int), s));
+        k_count_nonzero<<<grid(old.P), 256, 0, s>>>(old.life.p, old.P, d_iscal.p + I_LIVE);
+        ++launches;
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_LIVE], d_iscal.p + I_LIVE, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        const long long live = h_iscal[I_LIVE];
+        if (live == 0) return 0;
+        unsigned long long cap = 1024;
+        while (cap < 2ull * (unsigned long long)live) cap <<= 1;
         CS_RET(hkeys.ensure(cap));
         CS_RET(hvals.ensure(cap));
         k_fill_u64<<<grid(cap), 256, 0, s>>>(hkeys.p, cap, CS_EMPTY_KEY);
@@ -639,8 +801,12 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(edge_slot.upload(d->edge_slot, 2LL * new_));
     CS_RET(patch.upload(d->patch, ntw));
     CS_RET(pslot.upload(d->patch_slot, ntw));
-    CS_RET(ttree.create(ntw, d->tri_left, d->tri_right, d->tri_parent, d->tri_leaf_parent, d->tri_prim));
-    CS_RET(etree.create(new_, d->edge_left, d->edge_right, d->edge_parent, d->edge_leaf_parent, d->edge_prim));
+    CS_RET(eflip.ensure(new_));
+    k_edge_flip_info<<<grid(new_), 256>>>(new_, edge_tris.p, edge_slot.p, tri_static.p, patch.p, pslot.p, eflip.p);
+    CS_TRY(cudaGetLastError());
+    CS_RET(vtab.create(nw, false));
+    CS_RET(ttab.create(ntw, true));
+    CS_RET(etab.create(new_, true));
     // state
     CS_RET(x.upload(d->x0, 3LL * n));
     CS_RET(xprev.upload(d->x0, 3LL * n));
@@ -659,10 +825,6 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(obs_next_d.ensure(std::max(3 * nobs, 1)));
     CS_RET(vlo.ensure(3LL * nw));
     CS_RET(vhi.ensure(3LL * nw));
-    CS_RET(counts.ensure(nw + 1));
-    CS_RET(offsets.ensure(nw + 1));
-    CS_RET(counts2.ensure(new_ + 1));
-    CS_RET(offsets2.ensure(new_ + 1));
     CS_RET(seg_beg.ensure(nf));
     CS_RET(seg_end.ensure(nf));
     CS_RET(rhs_red.ensure(3 * 128));
@@ -676,7 +838,7 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_TRY(cudaMemset(d_scal.p, 0, sizeof(double) * S_COUNT));
     CS_TRY(cudaMemset(d_iscal.p, 0, sizeof(int) * I_COUNT));
     CS_TRY(cudaMallocHost(&h_scal, sizeof(double) * S_COUNT));
-    CS_TRY(cudaMallocHost(&h_iscal, sizeof(int) * I_COUNT));
+    CS_TRY(cudaMallocHost(&h_iscal, sizeof(int) * (I_COUNT + 8)));  // [I_COUNT, +8): broad-phase scratch
     CS_RET(pa.reserve(1024));
     CS_RET(pb.reserve(1024));
     CS_TRY(cudaDeviceSynchronize());
@@ -693,8 +855,8 @@ void cs_scene::release() {
     // DBuf members release through their owners
     DBuf<int>* ints[] = {&free_ids, &free_index, &pin_ids, &pin_slot, &e0, &e1, &rinc_ptr, &rinc, &ginc_ptr, &ginc,
                          &st, &binc_ptr, &binc, &sell_ptr, &sell_col, &hfp_ptr, &hfp_col, &wtris, &wedges,
-                         &edge_tris, &edge_slot, &patch, &pslot, &counts, &offsets, &sel, &skey, &ssrc, &skey_s,
-                         &ssrc_s, &seg_beg, &seg_end, &rowflag, &rows_act, &hvals, &fallback, &d_iscal, &counts2, &offsets2};
+                         &edge_tris, &edge_slot, &patch, &pslot, &sel, &skey, &ssrc, &skey_s,
+                         &ssrc_s, &seg_beg, &seg_end, &rowflag, &rows_act, &hvals, &fallback, &d_iscal};
     for (auto* p : ints) p->release();
     DBuf<double>* dbl[] = {&mass, &fext, &mh2, &erest, &ew, &bk, &bw, &sell_val, &diag, &hfp_val, &U, &V, &lam,
                            &x, &v, &xprev, &df, &obs, &z, &xs_w, &xc_w, &anchor_w, &tmp_w, &xf, &xf0, &b, &t,
@@ -705,10 +867,16 @@ void cs_scene::release() {
     vert_static.release();
     vert_used.release();
     edge_static.release();
+    eflip.release();
     hkeys.release();
     cub_tmp.release();
     pa.release();
     pb.release();
+    vtab.release();
+    ttab.release();
+    etab.release();
+    ocount.release();
+    ooffset.release();
 }
 
 int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_report* rep) {

@@ -7,30 +7,36 @@
 // with the reference's edge-edge ORIENTATION (which edge comes first in the row),
 // computed from the static patch partition exactly as the reference's
 // first-occurrence dedup picks it (bvh.py:264-286).  Row order is deterministic
-// (vertex-major VT block, then edge-major EE block, traversal order inside).
+// (VT block, then EE block; inside a block: hash-bucket order, then entry
+// order) but is not the reference's order - only the rounding of the
+// np.add.at collision stamps depends on it.
 //
-// Structure: two static-topology binary trees over Morton-sorted rest-pose
-// primitives (triangles for VT queries, edges for EE queries), built once on the
-// host; per query: vertex boxes -> leaf boxes -> atomic-flag bottom-up refit ->
-// count pass -> exclusive scan -> write pass.  Boxes stay fp64 so overlap tests
-// are exact (an fp32 filter could reject a pair the reference keeps).
+// Structure (B200-first: sort-based, no pointer chasing, warp-cooperative):
+//   1. vertex boxes (fp64, exact min/max -/+ margin) -> primitive boxes
+//      (triangles, edges); a fixed-order reduction of the mean box extent of
+//      the moving primitives picks each grid's cell size
+//   2. every box is entered once per cell it spans, as (bucket = hash(cell),
+//      primitive, cell code); entries are radix-sorted by bucket (stable, so a
+//      bucket lists its entries in primitive-then-cell order)
+//   3. one warp per non-empty bucket tests all entry pairs of that bucket that
+//      carry the same cell code: VT = bucket's vertex entries x the triangle
+//      entries of the same bucket, EE = all edge-entry pairs i < j.  A pair is
+//      reported only in the cell holding its intersection box's min corner,
+//      so every overlapping pair is produced exactly once.  Ballot compaction
+//      keeps the output order deterministic; count pass -> scan -> write pass.
+//   4. primitives spanning more than kMaxCellsPerPrim cells (pathological
+//      motion or giant obstacle faces) are not entered; a brute-force pass pairs
+//      them with every primitive of the other set.
+//
+// Exactness: cell indices are floor(x * inv_cell) of the same fp64 box
+// coordinates everywhere; floor of a correctly rounded product is monotone, so
+// the min-corner cell lies inside both boxes' cell ranges.  Cell size and hash
+// only change speed, never the set.
 #include "common.cuh"
 
 namespace cs {
 
-struct Tree {
-    int nleaf;                       // number of primitives
-    const int* __restrict__ left;    // (nleaf-1) child codes: >=0 internal, <0 leaf ~pos
-    const int* __restrict__ right;
-    const int* __restrict__ parent;  // (nleaf-1) internal parent (-1 root)
-    const int* __restrict__ leaf_parent;  // (nleaf)
-    const int* __restrict__ prim;    // (nleaf) primitive id at sorted leaf position
-    double* node_lo;                 // (nleaf-1)*3
-    double* node_hi;
-    double* leaf_lo;                 // (nleaf)*3 in leaf order
-    double* leaf_hi;
-    int* flags;                      // (nleaf-1)
-};
+constexpr long long kMaxCellsPerPrim = 1LL << 15;
 
 __global__ void k_vertex_boxes(const double* __restrict__ x0, const double* __restrict__ x1, int n, double margin,
                                double* __restrict__ vlo, double* __restrict__ vhi) {
@@ -41,93 +47,227 @@ __global__ void k_vertex_boxes(const double* __restrict__ x0, const double* __re
     vhi[i] = np_max(a, b) + margin;
 }
 
-// leaf boxes (primitive = triangle (arity 3) or edge (arity 2)) then bottom-up refit
-__global__ void k_refit(Tree T, const int* __restrict__ verts, int arity, const double* __restrict__ vlo,
-                        const double* __restrict__ vhi) {
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= T.nleaf) return;
-    const int pr = T.prim[p];
+// ------------------------------------------------------------------ boxes + cell size
+// box[6p..6p+5] = lo.xyz, hi.xyz over the primitive's vertex boxes.  Block
+// partial sums of the max-axis extent (moving primitives, all primitives) for the
+// cell size: part[4 b + {0,1,2,3}] = {sum moving, count moving, sum all, count all}.
+template <int ARITY>
+__global__ void __launch_bounds__(256) k_prim_boxes(const int* __restrict__ verts, int np,
+                                                    const uint8_t* __restrict__ is_static,
+                                                    const double* __restrict__ vlo, const double* __restrict__ vhi,
+                                                    double* __restrict__ box, double* __restrict__ part) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (p < np) {
+        double lo[3], hi[3];
+        const int a = verts[ARITY * p];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            lo[c] = vlo[3 * a + c];
+            hi[c] = vhi[3 * a + c];
+        }
+#pragma unroll
+        for (int k = 1; k < ARITY; ++k) {
+            const int b = verts[ARITY * p + k];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                lo[c] = np_min(lo[c], vlo[3 * b + c]);
+                hi[c] = np_max(hi[c], vhi[3 * b + c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            box[6 * (int64_t)p + c] = lo[c];
+            box[6 * (int64_t)p + 3 + c] = hi[c];
+        }
+        const double ext = fmax(fmax(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
+        const bool moving = !is_static[p];
+        v[0] = moving ? ext : 0.0;
+        v[1] = moving ? 1.0 : 0.0;
+        v[2] = ext;
+        v[3] = 1.0;
+    }
+    // fixed-order block tree reduction (deterministic)
+    __shared__ double sh[4][8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double s = v[k];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if ((threadIdx.x & 31) == 0) sh[k][threadIdx.x >> 5] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += sh[threadIdx.x][w];
+        part[4 * blockIdx.x + threadIdx.x] = s;
+    }
+}
+
+// inv_cell[0] = 1 / mean max-axis box extent of the moving primitives (all
+// primitives if none move); fixed-order reduction of the block partials.
+__global__ void k_cell_size(const double* __restrict__ part, int nparts, double* __restrict__ inv_cell) {
+    __shared__ double sh[4][256];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] += part[4 * b + k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sh[k][threadIdx.x] = acc[k];
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double cell = sh[1][0] > 0.0 ? sh[0][0] / sh[1][0] : (sh[3][0] > 0.0 ? sh[2][0] / sh[3][0] : 1.0);
+        if (!(cell > 1e-12)) cell = 1e-12;
+        inv_cell[0] = 1.0 / cell;
+    }
+}
+
+// ------------------------------------------------------------------ cells
+__device__ __forceinline__ long long cell_of(double x, double inv) {
+    double c = floor(x * inv);
+    c = fmin(fmax(c, -1.0e15), 1.0e15);  // keep the integer conversion defined
+    return (long long)c;
+}
+
+// 21 bits per axis (wraps only across 2^21 cells - kilometres at cloth scales)
+__device__ __forceinline__ unsigned long long cell_code(long long ix, long long iy, long long iz) {
+    const unsigned long long m = (1ull << 21) - 1;
+    return ((unsigned long long)ix & m) | (((unsigned long long)iy & m) << 21) | (((unsigned long long)iz & m) << 42);
+}
+
+__device__ __forceinline__ unsigned bucket_of(unsigned long long code, unsigned mask) {
+    unsigned long long h = code * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 32;
+    return (unsigned)h & mask;
+}
+
+struct CellRange {
+    long long lo[3], hi[3];
+    __device__ long long count() const {
+        return (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
+    }
+};
+
+__device__ __forceinline__ CellRange cell_range(const double lo[3], const double hi[3], double inv) {
+    CellRange r;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        r.lo[c] = cell_of(lo[c], inv);
+        r.hi[c] = cell_of(hi[c], inv);
+    }
+    return r;
+}
+
+__device__ __forceinline__ void load_box(const double* __restrict__ box, int p, double lo[3], double hi[3]) {
+    const double2* b = reinterpret_cast<const double2*>(box + 6 * (int64_t)p);
+    const double2 a0 = b[0], a1 = b[1], a2 = b[2];
+    lo[0] = a0.x;
+    lo[1] = a0.y;
+    lo[2] = a1.x;
+    hi[0] = a1.y;
+    hi[1] = a2.x;
+    hi[2] = a2.y;
+}
+
+// Box source of a grid: primitive boxes (box != null) or vertex boxes (used vertices only).
+struct BoxSrc {
+    const double* __restrict__ box;
+    const double* __restrict__ vlo;
+    const double* __restrict__ vhi;
+    const uint8_t* __restrict__ used;
+    int np;
+    __device__ __forceinline__ bool load(int p, double lo[3], double hi[3]) const {
+        if (box) {
+            load_box(box, p, lo, hi);
+            return true;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            lo[c] = vlo[3 * (int64_t)p + c];
+            hi[c] = vhi[3 * (int64_t)p + c];
+        }
+        return used[p] != 0;
+    }
+};
+
+// per primitive: number of cells spanned (0 if oversize / unused) + oversize flag
+__global__ void k_cell_count(BoxSrc S, const double* __restrict__ inv_cell, int* __restrict__ count,
+                             uint8_t* __restrict__ over) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= S.np) return;
     double lo[3], hi[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        lo[c] = vlo[3 * verts[arity * pr] + c];
-        hi[c] = vhi[3 * verts[arity * pr] + c];
-    }
-    for (int k = 1; k < arity; ++k) {
-        const int v = verts[arity * pr + k];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            lo[c] = np_min(lo[c], vlo[3 * v + c]);
-            hi[c] = np_max(hi[c], vhi[3 * v + c]);
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        T.leaf_lo[3 * p + c] = lo[c];
-        T.leaf_hi[3 * p + c] = hi[c];
-    }
-    if (T.nleaf == 1) return;
-    int node = T.leaf_parent[p];
-    while (node >= 0) {
-        __threadfence();
-        if (atomicAdd(&T.flags[node], 1) == 0) return;  // first child to arrive stops
-        __threadfence();
-        const int l = T.left[node], r = T.right[node];
-        const volatile double* llo = l >= 0 ? T.node_lo + 3 * l : T.leaf_lo + 3 * (~l);
-        const volatile double* lhi = l >= 0 ? T.node_hi + 3 * l : T.leaf_hi + 3 * (~l);
-        const volatile double* rlo = r >= 0 ? T.node_lo + 3 * r : T.leaf_lo + 3 * (~r);
-        const volatile double* rhi = r >= 0 ? T.node_hi + 3 * r : T.leaf_hi + 3 * (~r);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            T.node_lo[3 * node + c] = fmin(llo[c], rlo[c]);
-            T.node_hi[3 * node + c] = fmax(lhi[c], rhi[c]);
-        }
-        node = T.parent[node];
-    }
-}
-
-__device__ __forceinline__ bool overlap(const double* lo_a, const double* hi_a, const double* __restrict__ lo_b,
-                                        const double* __restrict__ hi_b) {
-    return (lo_a[0] <= hi_b[0]) && (lo_b[0] <= hi_a[0]) && (lo_a[1] <= hi_b[1]) && (lo_b[1] <= hi_a[1]) &&
-           (lo_a[2] <= hi_b[2]) && (lo_b[2] <= hi_a[2]);
-}
-
-// Visit every leaf whose box overlaps [qlo, qhi]; f(leaf_pos) called in traversal order.
-template <typename F>
-__device__ __forceinline__ void traverse(const Tree& T, const double qlo[3], const double qhi[3], F&& f) {
-    if (T.nleaf == 1) {
-        if (overlap(qlo, qhi, T.leaf_lo, T.leaf_hi)) f(0);
+    if (!S.load(p, lo, hi)) {
+        count[p] = 0;
+        over[p] = 0;
         return;
     }
-    int stack[64];
-    int sp = 0;
-    int node = 0;
-    while (true) {
-        const int l = T.left[node], r = T.right[node];
-        bool go_l, go_r;
-        if (l >= 0) go_l = overlap(qlo, qhi, T.node_lo + 3 * l, T.node_hi + 3 * l);
-        else {
-            go_l = false;
-            if (overlap(qlo, qhi, T.leaf_lo + 3 * (~l), T.leaf_hi + 3 * (~l))) f(~l);
-        }
-        if (r >= 0) go_r = overlap(qlo, qhi, T.node_lo + 3 * r, T.node_hi + 3 * r);
-        else {
-            go_r = false;
-            if (overlap(qlo, qhi, T.leaf_lo + 3 * (~r), T.leaf_hi + 3 * (~r))) f(~r);
-        }
-        if (go_l && go_r) {
-            stack[sp++] = r;
-            node = l;
-        } else if (go_l) {
-            node = l;
-        } else if (go_r) {
-            node = r;
-        } else {
-            if (sp == 0) break;
-            node = stack[--sp];
-        }
+    const long long nc = cell_range(lo, hi, inv_cell[0]).count();
+    const bool big = nc > kMaxCellsPerPrim || nc <= 0;
+    count[p] = big ? 0 : (int)nc;
+    over[p] = big ? 1 : 0;
+}
+
+// 8 threads per primitive: thread k writes the primitive's cells k, k+8, ... in
+// (z, y, x) order (x fastest), so a warp's stores land on contiguous entries.
+__global__ void k_cell_fill(BoxSrc S, const double* __restrict__ inv_cell, unsigned mask,
+                            const int* __restrict__ count, const int* __restrict__ offset,
+                            unsigned* __restrict__ key, int* __restrict__ prim, unsigned long long* __restrict__ code) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int p = (int)(tid >> 3), k0 = (int)(tid & 7);
+    if (p >= S.np) return;
+    const int n = count[p];
+    if (k0 >= n) return;
+    double lo[3], hi[3];
+    S.load(p, lo, hi);
+    const CellRange r = cell_range(lo, hi, inv_cell[0]);
+    const long long sx = r.hi[0] - r.lo[0] + 1, sy = r.hi[1] - r.lo[1] + 1;
+    const int o = offset[p];
+    for (int k = k0; k < n; k += 8) {
+        const long long x = r.lo[0] + k % sx, y = r.lo[1] + (k / sx) % sy, z = r.lo[2] + k / (sx * sy);
+        const unsigned long long c = cell_code(x, y, z);
+        key[o + k] = bucket_of(c, mask);
+        prim[o + k] = p;
+        code[o + k] = c;
     }
 }
+
+// sorted order -> (primitive, code) arrays; run heads; dense bucket ranges
+__global__ void k_entries_sorted(const int* __restrict__ perm, int m, const int* __restrict__ prim,
+                                 const unsigned long long* __restrict__ code, const unsigned* __restrict__ key_s,
+                                 int* __restrict__ prim_s, unsigned long long* __restrict__ code_s,
+                                 uint8_t* __restrict__ head, int* __restrict__ bstart, int* __restrict__ bend) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int k = perm[i];
+    prim_s[i] = prim[k];
+    code_s[i] = code[k];
+    const unsigned b = key_s[i];
+    const bool h = i == 0 || key_s[i - 1] != b;
+    head[i] = h;
+    if (bstart) {
+        if (h) bstart[b] = i;
+        if (i == m - 1 || key_s[i + 1] != b) bend[b] = i + 1;
+    }
+}
+
+// one sorted entry table (vertices, triangles or edges)
+struct EntryTable {
+    const unsigned* __restrict__ key;           // bucket, sorted
+    const int* __restrict__ prim;
+    const unsigned long long* __restrict__ code;
+    const int* __restrict__ run;                // run heads (first entry of each bucket)
+    const int* __restrict__ n_run;              // device scalar
+    const int* __restrict__ bstart;             // dense bucket ranges (triangle table only)
+    const int* __restrict__ bend;
+    int m;                                      // entries
+};
 
 struct WorldTopo {
     int nw;                              // world vertices
@@ -141,36 +281,28 @@ struct WorldTopo {
     const int* __restrict__ edge_slot;   // (E,2) slot of the edge inside each triangle
     const int* __restrict__ patch;       // (m,) patch id (reference build_patches)
     const int* __restrict__ pslot;       // (m,) slot inside the patch
+    const ulonglong2* __restrict__ flip; // (E,) packed incident-triangle records for ee_flip
 };
 
-// pass 0: counts; pass 1: write rows at offsets
-template <int PASS>
-__global__ void k_query_vt(Tree T, WorldTopo W, const double* __restrict__ vlo, const double* __restrict__ vhi,
-                           int* __restrict__ counts, const int* __restrict__ offsets, int8_t* __restrict__ kind,
-                           int4* __restrict__ idx, unsigned long long* __restrict__ keys) {
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= W.nw) return;
-    int cnt = 0;
-    if (W.vert_used[v]) {
-        const double qlo[3] = {vlo[3 * v], vlo[3 * v + 1], vlo[3 * v + 2]};
-        const double qhi[3] = {vhi[3 * v], vhi[3 * v + 1], vhi[3 * v + 2]};
-        const bool vs = W.vert_static[v];
-        int out = PASS == 1 ? offsets[v] : 0;
-        traverse(T, qlo, qhi, [&](int leaf) {
-            const int f = T.prim[leaf];
-            const int a = W.tris[3 * f], b = W.tris[3 * f + 1], c = W.tris[3 * f + 2];
-            if (a == v || b == v || c == v) return;
-            if (vs && W.tri_static[f]) return;
-            if (PASS == 1) {
-                kind[out] = CS_VT;
-                idx[out] = make_int4(v, a, b, c);
-                keys[out] = ((unsigned long long)(unsigned)v << 32) | (unsigned)f;
-                ++out;
-            }
-            ++cnt;
-        });
-    }
-    if (PASS == 0) counts[v] = cnt;
+struct PairOut {
+    int* __restrict__ counts;            // pass 0
+    const int* __restrict__ offsets;     // pass 1 (row offsets relative to base)
+    int8_t* __restrict__ kind;
+    int4* __restrict__ idx;
+    unsigned long long* __restrict__ keys;
+};
+
+__device__ __forceinline__ bool overlap6(const double alo[3], const double ahi[3], const double blo[3],
+                                         const double bhi[3]) {
+    return (alo[0] <= bhi[0]) && (blo[0] <= ahi[0]) && (alo[1] <= bhi[1]) && (blo[1] <= ahi[1]) &&
+           (alo[2] <= bhi[2]) && (blo[2] <= ahi[2]);
+}
+
+// the intersection box's min corner lies in cell `code`
+__device__ __forceinline__ bool min_corner_in(const double alo[3], const double blo[3], double inv,
+                                              unsigned long long code) {
+    return cell_code(cell_of(fmax(alo[0], blo[0]), inv), cell_of(fmax(alo[1], blo[1]), inv),
+                     cell_of(fmax(alo[2], blo[2]), inv)) == code;
 }
 
 __device__ __forceinline__ unsigned long long place_key(int pa, int sa, int pb, int sb, bool& a_first) {
@@ -181,20 +313,43 @@ __device__ __forceinline__ unsigned long long place_key(int pa, int sa, int pb, 
     return ((((same << 24 | p1) << 24 | p2) << 3 | s1) << 3) | s2;
 }
 
+// Per-edge record of each incident triangle (built once per scene):
+//   bit 63 valid, bit 62 static, bits 8..39 patch, bits 3..5 patch slot, bits 0..1 edge slot
+__global__ void k_edge_flip_info(int n_edges, const int* __restrict__ edge_tris, const int* __restrict__ edge_slot,
+                                 const uint8_t* __restrict__ tri_static, const int* __restrict__ patch,
+                                 const int* __restrict__ pslot, ulonglong2* __restrict__ out) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_edges) return;
+    unsigned long long rec[2];
+    for (int k = 0; k < 2; ++k) {
+        const int a = edge_tris[2 * e + k];
+        rec[k] = a < 0 ? 0ull
+                       : (1ull << 63) | ((unsigned long long)(tri_static[a] != 0) << 62) |
+                             ((unsigned long long)(unsigned)patch[a] << 8) | ((unsigned long long)pslot[a] << 3) |
+                             (unsigned long long)edge_slot[2 * e + k];
+    }
+    out[e] = make_ulonglong2(rec[0], rec[1]);
+}
+
 // reference orientation of edge pair (E, F), E < F: true when F comes first (bvh.py:264-286)
 __device__ bool ee_flip(const WorldTopo& W, int E, int F) {
+    const ulonglong2 re = W.flip[E], rf = W.flip[F];
+    const unsigned long long ra[2] = {re.x, re.y}, rb[2] = {rf.x, rf.y};
     unsigned long long best = ~0ull;
     bool flip = false;
+#pragma unroll
     for (int ka = 0; ka < 2; ++ka) {
-        const int a = W.edge_tris[2 * E + ka];
-        if (a < 0) continue;
+        const unsigned long long a = ra[ka];
+        if (!(a >> 63)) continue;
+#pragma unroll
         for (int kb = 0; kb < 2; ++kb) {
-            const int b = W.edge_tris[2 * F + kb];
-            if (b < 0) continue;
-            if (W.tri_static[a] && W.tri_static[b]) continue;
+            const unsigned long long b = rb[kb];
+            if (!(b >> 63)) continue;
+            if (((a >> 62) & 1) && ((b >> 62) & 1)) continue;
             bool a_first;
-            const unsigned long long place = place_key(W.patch[a], W.pslot[a], W.patch[b], W.pslot[b], a_first);
-            const int sa = W.edge_slot[2 * E + ka], sb = W.edge_slot[2 * F + kb];
+            const unsigned long long place = place_key((int)((a >> 8) & 0xffffffffu), (int)((a >> 3) & 7),
+                                                       (int)((b >> 8) & 0xffffffffu), (int)((b >> 3) & 7), a_first);
+            const int sa = (int)(a & 3), sb = (int)(b & 3);
             const unsigned long long sub = a_first ? (sa * 3 + sb) : (sb * 3 + sa);
             const unsigned long long key = (place << 5) | (sub << 1) | (a_first ? 0ull : 1ull);
             if (key < best) {
@@ -206,39 +361,293 @@ __device__ bool ee_flip(const WorldTopo& W, int E, int F) {
     return flip;
 }
 
-template <int PASS>
-__global__ void k_query_ee(Tree T, WorldTopo W, int n_edges, const double* __restrict__ vlo,
-                           const double* __restrict__ vhi, int* __restrict__ counts,
-                           const int* __restrict__ offsets, int8_t* __restrict__ kind, int4* __restrict__ idx,
-                           unsigned long long* __restrict__ keys) {
-    const int E = blockIdx.x * blockDim.x + threadIdx.x;
-    if (E >= n_edges) return;
-    const int a0 = W.edges[2 * E], a1 = W.edges[2 * E + 1];
-    double qlo[3], qhi[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        qlo[c] = np_min(vlo[3 * a0 + c], vlo[3 * a1 + c]);
-        qhi[c] = np_max(vhi[3 * a0 + c], vhi[3 * a1 + c]);
+__device__ __forceinline__ void write_vt(const PairOut& O, int row, int v, int f, const WorldTopo& W) {
+    O.kind[row] = CS_VT;
+    O.idx[row] = make_int4(v, W.tris[3 * f], W.tris[3 * f + 1], W.tris[3 * f + 2]);
+    O.keys[row] = ((unsigned long long)(unsigned)v << 32) | (unsigned)f;
+}
+
+// EE rows are written as (lower edge, higher edge); k_ee_orient applies the
+// reference orientation afterwards in one dense pass (keeps the divergent
+// emission path short).
+__device__ __forceinline__ void write_ee(const PairOut& O, int row, int E, int F, const WorldTopo& W) {
+    const int lo = E < F ? E : F, hi = E < F ? F : E;
+    O.kind[row] = CS_EE;
+    O.idx[row] = make_int4(W.edges[2 * lo], W.edges[2 * lo + 1], W.edges[2 * hi], W.edges[2 * hi + 1]);
+    O.keys[row] = (1ull << 63) | ((unsigned long long)(unsigned)lo << 32) | (unsigned)hi;
+}
+
+__global__ void k_ee_orient(const unsigned long long* __restrict__ keys, int4* __restrict__ idx, int64_t n,
+                            WorldTopo W) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long k = keys[i];
+    const int lo = (int)((k >> 32) & 0x7fffffffu), hi = (int)(k & 0xffffffffu);
+    if (ee_flip(W, lo, hi)) {
+        const int4 v = idx[i];
+        idx[i] = make_int4(v.z, v.w, v.x, v.y);
     }
-    const bool es = W.edge_static[E];
-    int cnt = 0;
-    int out = PASS == 1 ? offsets[E] : 0;
-    traverse(T, qlo, qhi, [&](int leaf) {
-        const int F = T.prim[leaf];
-        if (F <= E) return;
-        const int b0 = W.edges[2 * F], b1 = W.edges[2 * F + 1];
-        if (a0 == b0 || a0 == b1 || a1 == b0 || a1 == b1) return;
-        if (es && W.edge_static[F]) return;
-        if (PASS == 1) {
-            const bool fl = ee_flip(W, E, F);
-            kind[out] = CS_EE;
-            idx[out] = fl ? make_int4(b0, b1, a0, a1) : make_int4(a0, a1, b0, b1);
-            keys[out] = (1ull << 63) | ((unsigned long long)(unsigned)E << 32) | (unsigned)F;
-            ++out;
+}
+
+__device__ __forceinline__ bool vt_ok(const WorldTopo& W, int v, int f) {
+    if (W.vert_static[v] && W.tri_static[f]) return false;
+    const int a = W.tris[3 * f], b = W.tris[3 * f + 1], c = W.tris[3 * f + 2];
+    return a != v && b != v && c != v;
+}
+
+__device__ __forceinline__ bool ee_ok(const WorldTopo& W, int E, int F) {
+    if (W.edge_static[E] && W.edge_static[F]) return false;
+    const int a0 = W.edges[2 * E], a1 = W.edges[2 * E + 1];
+    const int b0 = W.edges[2 * F], b1 = W.edges[2 * F + 1];
+    return a0 != b0 && a0 != b1 && a1 != b0 && a1 != b1;
+}
+
+// Warp-level ordered emission: lanes with `hit` get consecutive rows in lane order.
+template <int PASS, typename F>
+__device__ __forceinline__ void warp_emit(bool hit, int& base, int& cnt, F&& write) {
+    const unsigned mask = __ballot_sync(0xffffffffu, hit);
+    if (PASS == 1 && hit) write(base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1u)));
+    base += __popc(mask);
+    cnt += __popc(mask);
+}
+
+// Shared-memory copy of one bucket entry (box, cell code, primitive).
+struct SmEntry {
+    double lo[3], hi[3];
+    unsigned long long code;
+    int prim, pad;
+};
+constexpr int kRunCap = 128;  // edge / triangle runs up to this many entries are staged in shared memory
+constexpr int kRunCapV = 32;  // vertex runs
+constexpr int kPairWarps = 4; // warps per block of the bucket-pair kernels
+
+__device__ __forceinline__ bool sm_overlap(const SmEntry& a, const SmEntry& b) {
+    return (a.lo[0] <= b.hi[0]) && (b.lo[0] <= a.hi[0]) && (a.lo[1] <= b.hi[1]) && (b.lo[1] <= a.hi[1]) &&
+           (a.lo[2] <= b.hi[2]) && (b.lo[2] <= a.hi[2]);
+}
+
+// k in [0, m(m-1)/2) -> (i, j), i < j, row-major over i (emission order = i, then j)
+__device__ __forceinline__ void tri_index(int k, int m, int& i, int& j) {
+    const float b = 2.0f * m - 1.0f;
+    int r = (int)((b - sqrtf(b * b - 8.0f * (float)k)) * 0.5f);
+    r = max(0, min(r, m - 2));
+    while (r > 0 && r * (2 * m - 1 - r) / 2 > k) --r;
+    while (r + 1 <= m - 2 && (r + 1) * (2 * m - 2 - r) / 2 <= k) ++r;
+    i = r;
+    j = k - r * (2 * m - 1 - r) / 2 + r + 1;
+}
+
+// VT: one warp per vertex-table bucket run x the same bucket's triangle entries.
+template <int PASS>
+__global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, EntryTable T,
+                                                              const double* __restrict__ vlo,
+                                                              const double* __restrict__ vhi,
+                                                              const double* __restrict__ tbox,
+                                                              const double* __restrict__ inv_cell, WorldTopo W,
+                                                              PairOut O) {
+    __shared__ SmEntry smv[kPairWarps][kRunCapV], smt[kPairWarps][kRunCap];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nr = V.n_run[0];
+    const double inv = inv_cell[0];
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nr; r += (gridDim.x * blockDim.x) >> 5) {
+        const int vb = V.run[r], ve = r + 1 < nr ? V.run[r + 1] : V.m;
+        const unsigned b = V.key[vb];
+        const int tb = T.bstart[b], te = T.bend[b];
+        const int mv = ve - vb, mt = te - tb;
+        int base = PASS == 1 ? O.offsets[r] : 0, cnt = 0;
+        if (mt > 0 && mv <= kRunCapV && mt <= kRunCap) {
+            for (int k = lane; k < mv; k += 32) {
+                SmEntry& e = smv[w][k];
+                const int v = V.prim[vb + k];
+                e.prim = v;
+                e.code = V.code[vb + k];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    e.lo[c] = vlo[3 * (int64_t)v + c];
+                    e.hi[c] = vhi[3 * (int64_t)v + c];
+                }
+            }
+            for (int k = lane; k < mt; k += 32) {
+                SmEntry& e = smt[w][k];
+                e.prim = T.prim[tb + k];
+                e.code = T.code[tb + k];
+                load_box(tbox, e.prim, e.lo, e.hi);
+            }
+            __syncwarp();
+            const int np = mv * mt;
+            for (int k0 = 0; k0 < np; k0 += 32) {
+                const int k = k0 + lane;
+                bool hit = false;
+                int v = 0, f = 0;
+                if (k < np) {
+                    const int i = k / mt, j = k - i * mt;
+                    const SmEntry& a = smv[w][i];
+                    const SmEntry& c = smt[w][j];
+                    v = a.prim;
+                    f = c.prim;
+                    hit = a.code == c.code && sm_overlap(a, c) && min_corner_in(a.lo, c.lo, inv, a.code) &&
+                          vt_ok(W, v, f);
+                }
+                warp_emit<PASS>(hit, base, cnt, [&](int row) { write_vt(O, row, v, f, W); });
+            }
+            __syncwarp();
+        } else if (mt > 0) {
+            for (int i = vb; i < ve; ++i) {
+                const int v = V.prim[i];
+                const unsigned long long cv = V.code[i];
+                double qlo[3], qhi[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    qlo[c] = vlo[3 * (int64_t)v + c];
+                    qhi[c] = vhi[3 * (int64_t)v + c];
+                }
+                for (int j0 = tb; j0 < te; j0 += 32) {
+                    const int j = j0 + lane;
+                    bool hit = false;
+                    int f = 0;
+                    if (j < te && T.code[j] == cv) {
+                        f = T.prim[j];
+                        double lo[3], hi[3];
+                        load_box(tbox, f, lo, hi);
+                        hit = overlap6(qlo, qhi, lo, hi) && min_corner_in(qlo, lo, inv, cv) && vt_ok(W, v, f);
+                    }
+                    warp_emit<PASS>(hit, base, cnt, [&](int row) { write_vt(O, row, v, f, W); });
+                }
+            }
         }
-        ++cnt;
-    });
-    if (PASS == 0) counts[E] = cnt;
+        if (PASS == 0 && lane == 0) O.counts[r] = cnt;
+    }
+}
+
+// EE: one warp per edge-table bucket run; all entry pairs i < j of the run.
+template <int PASS>
+__global__ void __launch_bounds__(32 * kPairWarps) k_pairs_ee(EntryTable E, const double* __restrict__ ebox,
+                                                              const double* __restrict__ inv_cell, WorldTopo W,
+                                                              PairOut O) {
+    __shared__ SmEntry sme[kPairWarps][kRunCap];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nr = E.n_run[0];
+    const double inv = inv_cell[0];
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nr; r += (gridDim.x * blockDim.x) >> 5) {
+        const int eb = E.run[r], ee = r + 1 < nr ? E.run[r + 1] : E.m;
+        const int m = ee - eb;
+        int base = PASS == 1 ? O.offsets[r] : 0, cnt = 0;
+        if (m <= kRunCap) {
+            for (int k = lane; k < m; k += 32) {
+                SmEntry& e = sme[w][k];
+                e.prim = E.prim[eb + k];
+                e.code = E.code[eb + k];
+                load_box(ebox, e.prim, e.lo, e.hi);
+            }
+            __syncwarp();
+            const int np = m * (m - 1) / 2;
+            for (int k0 = 0; k0 < np; k0 += 32) {
+                const int k = k0 + lane;
+                bool hit = false;
+                int a = 0, f = 0;
+                if (k < np) {
+                    int i, j;
+                    tri_index(k, m, i, j);
+                    const SmEntry& x = sme[w][i];
+                    const SmEntry& y = sme[w][j];
+                    a = x.prim;
+                    f = y.prim;
+                    hit = x.code == y.code && sm_overlap(x, y) && min_corner_in(x.lo, y.lo, inv, x.code) &&
+                          ee_ok(W, a, f);
+                }
+                warp_emit<PASS>(hit, base, cnt, [&](int row) { write_ee(O, row, a, f, W); });
+            }
+            __syncwarp();
+        } else {
+            for (int i = eb; i + 1 < ee; ++i) {
+                const int a = E.prim[i];
+                const unsigned long long ca = E.code[i];
+                double qlo[3], qhi[3];
+                load_box(ebox, a, qlo, qhi);
+                for (int j0 = i + 1; j0 < ee; j0 += 32) {
+                    const int j = j0 + lane;
+                    bool hit = false;
+                    int f = 0;
+                    if (j < ee && E.code[j] == ca) {
+                        f = E.prim[j];
+                        double lo[3], hi[3];
+                        load_box(ebox, f, lo, hi);
+                        hit = overlap6(qlo, qhi, lo, hi) && min_corner_in(qlo, lo, inv, ca) && ee_ok(W, a, f);
+                    }
+                    warp_emit<PASS>(hit, base, cnt, [&](int row) { write_ee(O, row, a, f, W); });
+                }
+            }
+        }
+        if (PASS == 0 && lane == 0) O.counts[r] = cnt;
+    }
+}
+
+// Brute-force side for primitives that were not entered in the grid (oversize).
+// VT: thread t < n_ov handles oversize vertex over[t] against every triangle;
+// thread n_ov + k handles oversize triangle overt[k] against every entered vertex.
+template <int PASS>
+__global__ void k_over_vt(const int* __restrict__ over_v, int n_ov, const int* __restrict__ over_t, int n_ot,
+                          const uint8_t* __restrict__ v_over, const double* __restrict__ vlo,
+                          const double* __restrict__ vhi, const double* __restrict__ tbox, int ntris, WorldTopo W,
+                          PairOut O) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_ov + n_ot) return;
+    int row = PASS == 1 ? O.offsets[t] : 0, cnt = 0;
+    if (t < n_ov) {
+        const int v = over_v[t];
+        double qlo[3], qhi[3];
+        for (int c = 0; c < 3; ++c) {
+            qlo[c] = vlo[3 * (int64_t)v + c];
+            qhi[c] = vhi[3 * (int64_t)v + c];
+        }
+        for (int f = 0; f < ntris; ++f) {
+            double lo[3], hi[3];
+            load_box(tbox, f, lo, hi);
+            if (overlap6(qlo, qhi, lo, hi) && vt_ok(W, v, f)) {
+                if (PASS == 1) write_vt(O, row++, v, f, W);
+                ++cnt;
+            }
+        }
+    } else {
+        const int f = over_t[t - n_ov];
+        double lo[3], hi[3];
+        load_box(tbox, f, lo, hi);
+        for (int v = 0; v < W.nw; ++v) {
+            if (!W.vert_used[v] || v_over[v]) continue;
+            double qlo[3], qhi[3];
+            for (int c = 0; c < 3; ++c) {
+                qlo[c] = vlo[3 * (int64_t)v + c];
+                qhi[c] = vhi[3 * (int64_t)v + c];
+            }
+            if (overlap6(qlo, qhi, lo, hi) && vt_ok(W, v, f)) {
+                if (PASS == 1) write_vt(O, row++, v, f, W);
+                ++cnt;
+            }
+        }
+    }
+    if (PASS == 0) O.counts[t] = cnt;
+}
+
+// EE: oversize edge E against every other edge F (entered F always; oversize F only if F > E).
+template <int PASS>
+__global__ void k_over_ee(const int* __restrict__ over_e, int n_oe, const uint8_t* __restrict__ e_over,
+                          const double* __restrict__ ebox, int n_edges, WorldTopo W, PairOut O) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_oe) return;
+    int row = PASS == 1 ? O.offsets[t] : 0, cnt = 0;
+    const int E = over_e[t];
+    double qlo[3], qhi[3];
+    load_box(ebox, E, qlo, qhi);
+    for (int F = 0; F < n_edges; ++F) {
+        if (F == E || (e_over[F] && F < E)) continue;
+        double lo[3], hi[3];
+        load_box(ebox, F, lo, hi);
+        if (overlap6(qlo, qhi, lo, hi) && ee_ok(W, E, F)) {
+            if (PASS == 1) write_ee(O, row++, E, F, W);
+            ++cnt;
+        }
+    }
+    if (PASS == 0) O.counts[t] = cnt;
 }
 
 }  // namespace cs

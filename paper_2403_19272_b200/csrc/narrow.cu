@@ -105,6 +105,50 @@ __device__ __forceinline__ double pair_extent(const Corners& a, const Corners& b
     return norm3(hi - lo);
 }
 
+// Exact early-out for full_ccd: every TOI full_ccd can report needs a witness
+// distance <= tol * max(scale, 1) at that time (validated roots, ccd.py:111-135)
+// or <= 1e-9 * max(extent, 1) (flat fallback, ccd.py:171-195), with scale <= 2 x
+// the pair extent.  Positions at any t lie in the box of each side's start/end
+// corners (up to lerp rounding), so a box gap on some axis above that bound
+// proves the reference result is NaN.  The margin absorbs rounding by 1e-9
+// relative to the coordinates - far above the fp64 error of any of the terms.
+__device__ __forceinline__ bool separated_sides(int kd, const Corners& a, const Corners& b, double tol) {
+    const int na = kd == CS_VT ? 1 : 2;
+    double alo[3], ahi[3], blo[3], bhi[3], mag = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        alo[c] = blo[c] = INFINITY;
+        ahi[c] = bhi[c] = -INFINITY;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double q0[3] = {a.p[k].x, a.p[k].y, a.p[k].z}, q1[3] = {b.p[k].x, b.p[k].y, b.p[k].z};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double lo = fmin(q0[c], q1[c]), hi = fmax(q0[c], q1[c]);
+            mag = fmax(mag, fmax(fabs(lo), fabs(hi)));
+            if (k < na) {
+                alo[c] = fmin(alo[c], lo);
+                ahi[c] = fmax(ahi[c], hi);
+            } else {
+                blo[c] = fmin(blo[c], lo);
+                bhi[c] = fmax(bhi[c], hi);
+            }
+        }
+    }
+    double gap = 0.0, e2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        gap = fmax(gap, fmax(blo[c] - ahi[c], alo[c] - bhi[c]));
+        const double span = fmax(ahi[c], bhi[c]) - fmin(alo[c], blo[c]);
+        e2 += span * span;
+    }
+    if (!(gap > 0.0)) return false;  // NaN-safe: non-finite input takes the full path
+    const double ext = sqrt(e2);
+    const double bound = fmax(tol * fmax(2.0 * ext, 1.0), 1e-9 * fmax(ext, 1.0));
+    return gap > bound * (1.0 + 1e-6) + 1e-9 * mag;
+}
+
 __global__ void k_full_ccd(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                            const double* __restrict__ x0, const double* __restrict__ x1, int64_t P,
                            int single, double tol, double* __restrict__ toi_out) {
@@ -113,6 +157,11 @@ __global__ void k_full_ccd(const int8_t* __restrict__ kind, const int4* __restri
     const int kd = kind[i];
     const int4 id = idx[i];
     Corners a = gather4(x0, id), b = gather4(x1, id);
+    const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
+    if (separated_sides(kd, a, b, tol)) {
+        toi_out[i] = NaN;
+        return;
+    }
 
     // coplanarity samples at t = 0, 1/3, 2/3, 1 and the monomial fit (ccd.py:36-44)
     const double nodes[4] = {0.0, 1.0 / 3.0, 2.0 / 3.0, 1.0};
@@ -142,7 +191,6 @@ __global__ void k_full_ccd(const int8_t* __restrict__ kind, const int4* __restri
     const double ext = pair_extent(a, b);
     const bool flat = csum <= 1e-12 * np_max(cube_rn(fabs(ext)), 1e-30);
 
-    const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
     double toi = NaN;
     if (!flat) {
         // ---- _candidate_roots (ccd.py:53-108)
@@ -254,6 +302,38 @@ __global__ void k_full_ccd(const int8_t* __restrict__ kind, const int4* __restri
     toi_out[i] = toi;
 }
 
+// gap between the boxes of the two sides at the start positions, minus a
+// rounding allowance of 1e-9 x the coordinate magnitude (lower bound on the
+// witness distance; <= 0 when undecided)
+__device__ __forceinline__ double start_gap(int kd, const Corners& a) {
+    const int na = kd == CS_VT ? 1 : 2;
+    double alo[3], ahi[3], blo[3], bhi[3], mag = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        alo[c] = blo[c] = INFINITY;
+        ahi[c] = bhi[c] = -INFINITY;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double q[3] = {a.p[k].x, a.p[k].y, a.p[k].z};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            mag = fmax(mag, fabs(q[c]));
+            if (k < na) {
+                alo[c] = fmin(alo[c], q[c]);
+                ahi[c] = fmax(ahi[c], q[c]);
+            } else {
+                blo[c] = fmin(blo[c], q[c]);
+                bhi[c] = fmax(bhi[c], q[c]);
+            }
+        }
+    }
+    double gap = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) gap = fmax(gap, fmax(blo[c] - ahi[c], alo[c] - bhi[c]));
+    return gap - 1e-9 * mag;
+}
+
 __global__ void k_distance_toi(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                                const double* __restrict__ x0, const double* __restrict__ x1, int64_t P,
                                double floor_frac, int max_iter, double* __restrict__ out) {
@@ -279,9 +359,18 @@ __global__ void k_distance_toi(const int8_t* __restrict__ kind, const int4* __re
         lb = np_max(np_max(np_max(0.0, 0.0), mv[2]), mv[3]);
     }
     const double L = la + lb;
+    const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
+    // exact early-out: the first advance (d - goal) / L already leaves [0, 1]
+    // whenever the start-box gap bounds d from below well enough (ccd.py:251-255)
+    if (L > 0.0 && floor_frac < 1.0) {
+        const double g = start_gap(kd, a);
+        if (g > 0.0 && g * (1.0 - floor_frac) * (1.0 - 1e-9) > L * (1.0 + 1e-9)) {
+            out[i] = NaN;
+            return;
+        }
+    }
     double d = pair_distance(kd, a.p[0], a.p[1], a.p[2], a.p[3]);
     const double goal = floor_frac * d;
-    const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
     double toi = NaN;
     if (d <= 0.0) toi = 0.0;
     if (d > 0.0 && L > 0.0) {

@@ -29,6 +29,7 @@ __global__ void k_hash_insert(const unsigned long long* __restrict__ keys, const
                               unsigned long long mask) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= P) return;
+    if (life[i] == 0) return;  // absent keys read back as 0
     const unsigned long long k = keys[i];
     unsigned long long h = mix64(k) & mask;
     while (true) {
@@ -69,6 +70,13 @@ __global__ void k_flag_engaged(const uint8_t* __restrict__ engaged, const double
         f = engaged[i] && (weight[i] > 0.0);
         flags[i] = f;
     }
+    const unsigned ballot = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(count, __popc(ballot));
+}
+
+__global__ void k_count_nonzero(const int* __restrict__ v, int64_t P, int* __restrict__ count) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool f = i < P && v[i] != 0;
     const unsigned ballot = __ballot_sync(0xffffffffu, f);
     if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(count, __popc(ballot));
 }

@@ -274,24 +274,49 @@ __global__ void __launch_bounds__(256) k_project_partial(Sell H, const double* _
 
 // G partials over the ascending list of collided rows (count read on device):
 // block b owns a contiguous chunk of the list.
+// Block b owns a contiguous chunk of the collided-row list; rows are staged in
+// shared memory 32 at a time and every thread accumulates its (a, b) entries in
+// row order, s = fma(V_ia, delta_i V_ib, s).
 __global__ void __launch_bounds__(256) k_gram_partial(const int* __restrict__ rows,
                                                       const int* __restrict__ nrows_ptr,
                                                       const double* __restrict__ delta,
                                                       const double* __restrict__ V, int r,
                                                       double* __restrict__ part) {
+    constexpr int kTile = 32;
+    __shared__ double sv[kTile][33];
+    __shared__ double sd[kTile];
     const int cnt = *nrows_ptr;
     const int per = (cnt + gridDim.x - 1) / gridDim.x;
     const int beg = min(cnt, (int)blockIdx.x * per);
     const int end = min(cnt, beg + per);
-    for (int o = threadIdx.x; o < r * r; o += blockDim.x) {
-        const int a = o / r, bcol = o % r;
-        double s = 0.0;
-        for (int k = beg; k < end; ++k) {
-            const int i = rows[k];
-            const double* row = V + (int64_t)i * r;
-            s = fma(row[a], delta[i] * row[bcol], s);
+    const int nout = r * r;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int oa[4], ob[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int o = threadIdx.x + q * blockDim.x;
+        oa[q] = o < nout ? o / r : 0;
+        ob[q] = o < nout ? o % r : 0;
+    }
+    for (int t0 = beg; t0 < end; t0 += kTile) {
+        const int nt = min(kTile, end - t0);
+        for (int e = threadIdx.x; e < nt * r; e += blockDim.x) {
+            const int k = e / r, c = e - k * r;
+            sv[k][c] = V[(int64_t)rows[t0 + k] * r + c];
         }
-        part[(int64_t)blockIdx.x * r * r + o] = s;
+        if (threadIdx.x < nt) sd[threadIdx.x] = delta[rows[t0 + threadIdx.x]];
+        __syncthreads();
+        for (int k = 0; k < nt; ++k) {
+            const double dk = sd[k];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(sv[k][oa[q]], dk * sv[k][ob[q]], acc[q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int o = threadIdx.x + q * blockDim.x;
+        if (o < nout) part[(int64_t)blockIdx.x * nout + o] = acc[q];
     }
 }
 

@@ -136,9 +136,6 @@ def scene_desc(mesh, elastic, system, subspace, world, obstacle_x, gravity_force
     d.edge_slot = keep.ptr(world.edge_slot.astype(np.int32), I)
     d.patch = keep.ptr(world.patch_of_tri.astype(np.int32), I)
     d.patch_slot = keep.ptr(world.slot_of_tri.astype(np.int32), I)
-    for prefix, tree in (("tri", world.tri_tree), ("edge", world.edge_tree)):
-        for name, arr in zip(("left", "right", "parent", "leaf_parent", "prim"), tree):
-            setattr(d, f"{prefix}_{name}", keep.ptr(arr.astype(np.int32), I))
     d.x0 = keep.ptr(np.asarray(x0, dtype=np.float64), D)
     d.obstacle_x0 = keep.ptr(np.concatenate([np.asarray(obstacle_x, dtype=np.float64).ravel(), [0.0]]), D)
     return d, keep

@@ -149,6 +149,29 @@ def traj_fixture(tag, kind, steps, cfg_kw, **scene_kw):
          toi=np.array(toi), obstacle_x=sim.obstacle_x)
 
 
+def contact_state_fixture(steps=25):
+    """sphere_drape res 14 over the whole settling sequence, full SimState after every
+    step (for teacher-forced GPU steps) + the reference's own intersection count."""
+    from clothsim.oracles import oracle_intersect
+
+    sim = build_scene("sphere_drape", resolution=14, size=0.2, config=clothsim.StepConfig())
+    keys = ("x", "x_dot", "x_prev", "delta_f")
+    out = {k: [sim.state.__dict__[k].copy()] for k in keys}
+    out["obstacle_x"] = [sim.obstacle_x.copy()]
+    lg, toi, rf, bad = [], [], [], []
+    for _ in range(steps):
+        r = sim.step()
+        for k in keys:
+            out[k].append(getattr(sim.state, k).copy())
+        out["obstacle_x"].append(sim.obstacle_x.copy())
+        lg.append(r.lg_iterations)
+        toi.append(r.toi_exit)
+        rf.append(r.rf_triggered)
+        bad.append(len(oracle_intersect(sim.world(sim.state.x), sim.bvh.triangles)))
+    save("contact_sphere14.npz", **{k: np.stack(v) for k, v in out.items()}, lg=np.array(lg), toi=np.array(toi),
+         rf=np.array(rf), intersections=np.array(bad))
+
+
 def two_corner_fixture(steps=3):
     """BASELINE config 1: 64x64 grid pinned at two corners, h = 1/200."""
     v, t = grid_cloth(64, 1.0)
@@ -163,6 +186,10 @@ def two_corner_fixture(steps=3):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:          # regenerate selected fixtures only
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     narrow_fixture()
     broad_fixtures()
     solver_fixture()
@@ -170,3 +197,4 @@ if __name__ == "__main__":
     traj_fixture("sphere14", "sphere_drape", 12, {}, resolution=14, size=0.2)
     traj_fixture("twist10", "twist", 6, {}, resolution=10, size=0.3)
     two_corner_fixture()
+    contact_state_fixture()

@@ -81,28 +81,6 @@ def test_patches_partition_triangles():
     assert max(len(g) for g in P.build_patches(t, len(v))) <= 8
 
 
-def test_morton_tree_is_a_binary_tree():
-    from paper_2403_19272_b200.collision import morton_tree
-
-    rng = np.random.default_rng(0)
-    for L in (1, 2, 3, 7, 100, 1000):
-        left, right, parent, leaf_parent, prim = morton_tree(rng.random((L, 3)))
-        assert np.array_equal(np.sort(prim), np.arange(L))
-        if L == 1:
-            continue
-        kids = np.concatenate([left, right])
-        leaves = np.sort(~kids[kids < 0])
-        assert np.array_equal(leaves, np.arange(L))
-        internal = np.sort(kids[kids >= 0])
-        assert np.array_equal(internal, np.arange(1, L - 1))
-        for node in range(L - 1):
-            for c in (left[node], right[node]):
-                if c >= 0:
-                    assert parent[c] == node
-                else:
-                    assert leaf_parent[~c] == node
-
-
 def test_sell32_roundtrip():
     from paper_2403_19272_b200.device import sell32
 
