@@ -138,6 +138,14 @@ int cs_pair_witness(const int8_t *kind, const int *idx4, const double *x, long l
 int cs_broad_phase(cs_scene *scene, const double *x_start_w, const double *x_end_w, double margin,
                    long long *count, void *stream);
 int cs_scene_pairs(cs_scene *scene, int8_t *kind, int *idx4, void *stream);
+/* Simulation._full_ccd_site + _clamp (stepper.py:426-452): broad phase, full CCD (hit
+ * TOIs) and the distance-march line-search filter over the scene's pair buffer, with
+ * the device's filter/worklist narrow phase.  clamp = alpha * min filter TOI (1 if
+ * none); returns CS_PENETRATION when the minimum is <= 0.  cs_scene_pairs /
+ * cs_scene_pair_results copy the site's rows and (P) TOIs (DEVICE pointers). */
+int cs_ccd_site(cs_scene *scene, const double *x_start_w, const double *x_end_w, long long *count, double *clamp,
+                void *stream);
+int cs_scene_pair_results(cs_scene *scene, double *toi, double *toi_filter, void *stream);
 /* assemble_rhs (constraints.py:229-256); coll_* (n_coll) are the flat
  * (ids, weights, targets) of Simulation._collision_terms in order; ids are cloth ids. */
 int cs_assemble_rhs(cs_scene *scene, const double *z, const double *x, const int *coll_ids, const double *coll_w,

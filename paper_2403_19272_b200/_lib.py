@@ -68,7 +68,7 @@ CS_OK, CS_PENETRATION, CS_NONFINITE, CS_DIVERGENCE, CS_BAD_DIAGONAL, CS_BAD_ARGU
 EXPORTED = (
     "cs_scene_create", "cs_scene_destroy", "cs_scene_set_config", "cs_step", "cs_get_state", "cs_set_state",
     "cs_state_device", "cs_full_ccd", "cs_distance_toi", "cs_partial_ccd", "cs_pair_witness", "cs_broad_phase",
-    "cs_scene_pairs", "cs_assemble_rhs", "cs_ajacobi_smooth", "cs_reduced_correction", "cs_warmstart_correction",
+    "cs_scene_pairs", "cs_ccd_site", "cs_scene_pair_results", "cs_assemble_rhs", "cs_ajacobi_smooth", "cs_reduced_correction", "cs_warmstart_correction",
     "cs_energy_gradient", "cs_version",
 )
 
@@ -100,6 +100,8 @@ def load(path: str = LIB_PATH):
         "cs_pair_witness": (ctypes.c_int, [vp, vp, vp, ll, vp, vp, vp, vp, vp, vp]),
         "cs_broad_phase": (ctypes.c_int, [vp, vp, vp, ctypes.c_double, ctypes.POINTER(ll), vp]),
         "cs_scene_pairs": (ctypes.c_int, [vp, vp, vp, vp]),
+        "cs_ccd_site": (ctypes.c_int, [vp, vp, vp, ctypes.POINTER(ll), ctypes.POINTER(ctypes.c_double), vp]),
+        "cs_scene_pair_results": (ctypes.c_int, [vp, vp, vp, vp]),
         "cs_assemble_rhs": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp]),
         "cs_ajacobi_smooth": (ctypes.c_int, [vp, vp, vp, ctypes.c_int, ctypes.c_double, vp, vp]),
         "cs_reduced_correction": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, vp]),

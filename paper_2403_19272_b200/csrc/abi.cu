@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -44,7 +45,7 @@ template <typename T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
-    int ensure(size_t m) {
+    int ensure(size_t m, bool exact = false) {
         if (m <= n && p) return 0;
         if (p) cudaFree(p);
         p = nullptr;
@@ -52,6 +53,9 @@ struct DBuf {
         // every cudaFree/cudaMalloc of a large buffer stalls the stream
         size_t want = std::max<size_t>(m, 1);
         if (n) want = std::max(2 * want, n + n / 2);
+        else if (!exact && want > (1u << 16)) want *= 2;  // large first sizing: 2x
+        static const bool trace = std::getenv("CS_TRACE_ALLOC") != nullptr;
+        if (trace) std::fprintf(stderr, "[cs alloc] %zu -> %zu bytes\n", n * sizeof(T), want * sizeof(T));
         cudaError_t e = cudaMalloc(&p, want * sizeof(T));
         if (e != cudaSuccess) {
             n = 0;
@@ -62,7 +66,7 @@ struct DBuf {
         return 0;
     }
     int upload(const T* host, size_t m) {
-        CS_RET(ensure(m));
+        CS_RET(ensure(m, true));
         if (m && host) {
             cudaError_t e = cudaMemcpy(p, host, m * sizeof(T), cudaMemcpyHostToDevice);
             if (e != cudaSuccess) return 1000 + (int)e;
@@ -85,9 +89,11 @@ struct EntryBuf {
     int n_over_h = 0;
     DBuf<double> box, part, inv;
     DBuf<int> count, offset, prim, perm, perm_s, prim_s, run, n_run, bstart, bend, over, n_over, pcount, poffset;
+    DBuf<long long> iters, iter_off;
+    DBuf<unsigned> masks;
     DBuf<unsigned> key, key_s;
     DBuf<unsigned long long> code, code_s;
-    DBuf<uint8_t> is_over, head;
+    DBuf<uint8_t> is_over, head, zb, zb_s;
     int create(int n_prim, bool has_box) {
         np = n_prim;
         if (has_box) CS_RET(box.ensure(6LL * np));
@@ -109,14 +115,15 @@ struct EntryBuf {
         }
     }
     EntryTable view() const {
-        return EntryTable{key_s.p, prim_s.p, code_s.p, run.p, n_run.p, bstart.p, bend.p, (int)m};
+        return EntryTable{key_s.p, prim_s.p, code_s.p, zb_s.p, run.p, n_run.p, bstart.p, bend.p, (int)m};
     }
     void release() {
         for (DBuf<int>* b : {&count, &offset, &prim, &perm, &perm_s, &prim_s, &run, &n_run, &bstart, &bend, &over,
                              &n_over, &pcount, &poffset})
             b->release();
+        iters.release(); iter_off.release(); masks.release();
         box.release(); part.release(); inv.release(); key.release(); key_s.release(); code.release();
-        code_s.release(); is_over.release(); head.release();
+        code_s.release(); is_over.release(); head.release(); zb.release(); zb_s.release();
     }
 };
 
@@ -153,8 +160,8 @@ struct PairBuf {
 
 // scalar slots (doubles) read back in one D2H copy
 enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_NORM1 = 5, S_NORM_F = 6,
-       S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_COUNT = 16 };
-enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_COUNT = 8 };
+       S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_MINBITS = 10, S_COUNT = 16 };
+enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_WLF = 8, I_COUNT = 10 };
 
 const int kStages = 8;
 enum { T_WARM = 0, T_LOCAL, T_GLOBAL, T_SMOOTH, T_BROAD, T_PARTIAL, T_FULL, T_RF };
@@ -188,7 +195,8 @@ struct cs_scene {
     // work arrays
     DBuf<double> z, xs_w, xc_w, anchor_w, tmp_w, xf, xf0, b, t, delta, prev_outer, grad, fr;
     DBuf<double> pins_next_d, obs_next_d;
-    DBuf<double> vlo, vhi;
+    DBuf<double> vlo, vhi, vdisp, tdisp, edisp;
+    double bmargin = 0.0;
     PairBuf pa, pb;  // current and next pair sets
     PairBuf* cur = &pa;
     PairBuf* nxt = &pb;
@@ -199,6 +207,7 @@ struct cs_scene {
     DBuf<double> part, part2, rhs_red, gram_red, q, Xred, beta_red, norms;
     int pending_checks = 0;
     DBuf<int> fallback;
+    DBuf<int> wl_full, wl_dist;
     DBuf<char> cub_tmp;
     DBuf<double> d_scal;
     DBuf<int> d_iscal;
@@ -364,7 +373,8 @@ struct cs_scene {
         return w;
     }
 
-    int scan(const int* in, int* out, int m) {
+    template <typename I>
+    int scan(const I* in, I* out, int m) {
         size_t bytes = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, m, s);
         CS_RET(cub_tmp.ensure(bytes));
@@ -408,8 +418,10 @@ struct cs_scene {
         CS_RET(G.code.ensure(m));
         CS_RET(G.code_s.ensure(m));
         CS_RET(G.head.ensure(m));
+        CS_RET(G.zb.ensure(m));
+        CS_RET(G.zb_s.ensure(m));
         k_cell_fill<<<grid(8LL * G.np), 256, 0, s>>>(src, inv, G.T - 1, G.count.p, G.offset.p, G.key.p, G.prim.p,
-                                               G.code.p);
+                                               G.code.p, G.zb.p);
         k_iota<<<grid(m), 256, 0, s>>>(G.perm.p, m);
         launches += 2;
         size_t bytes = 0;
@@ -418,8 +430,8 @@ struct cs_scene {
         CS_RET(cub_tmp.ensure(bytes));
         CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, G.key.p, G.key_s.p, G.perm.p, G.perm_s.p, (int)m, 0,
                                                G.log2T, s));
-        k_entries_sorted<<<grid(m), 256, 0, s>>>(G.perm_s.p, (int)m, G.prim.p, G.code.p, G.key_s.p, G.prim_s.p,
-                                                 G.code_s.p, G.head.p, dense ? G.bstart.p : nullptr,
+        k_entries_sorted<<<grid(m), 256, 0, s>>>(G.perm_s.p, (int)m, G.prim.p, G.code.p, G.zb.p, G.key_s.p,
+                                                 G.prim_s.p, G.code_s.p, G.zb_s.p, G.head.p, dense ? G.bstart.p : nullptr,
                                                  dense ? G.bend.p : nullptr);
         ++launches;
         bytes = 0;
@@ -437,14 +449,18 @@ struct cs_scene {
     // broad phase into pr (bvh.py:207-292): entry tables -> bucket-pair count -> scan -> write; two host syncs
     int broad_phase(const double* xa, const double* xb, double margin, PairBuf& pr) {
         k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(xa, xb, nw, margin, vlo.p, vhi.p);
+        k_vertex_disp<<<grid(nw), 256, 0, s>>>(xa, xb, nw, vdisp.p);
+        bmargin = margin;
         const int gt = grid(ntw), ge = grid(new_);
         CS_RET(ttab.part.ensure(4LL * gt));
         CS_RET(etab.part.ensure(4LL * ge));
-        k_prim_boxes<3><<<gt, 256, 0, s>>>(wtris.p, ntw, tri_static.p, vlo.p, vhi.p, ttab.box.p, ttab.part.p);
+        k_prim_boxes<3><<<gt, 256, 0, s>>>(wtris.p, ntw, tri_static.p, vlo.p, vhi.p, vdisp.p, ttab.box.p, tdisp.p,
+                                           ttab.part.p);
         k_cell_size<<<1, 256, 0, s>>>(ttab.part.p, gt, ttab.inv.p);
-        k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, etab.box.p, etab.part.p);
+        k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, vdisp.p, etab.box.p, edisp.p,
+                                           etab.part.p);
         k_cell_size<<<1, 256, 0, s>>>(etab.part.p, ge, etab.inv.p);
-        launches += 5;
+        launches += 6;
         const BoxSrc vs{nullptr, vlo.p, vhi.p, vert_used.p, nw};
         const BoxSrc ts{ttab.box.p, nullptr, nullptr, nullptr, ntw};
         const BoxSrc es{etab.box.p, nullptr, nullptr, nullptr, new_};
@@ -453,13 +469,13 @@ struct cs_scene {
         CS_RET(table_count(etab, es, etab.inv.p));
         EntryBuf* tabs[3] = {&vtab, &ttab, &etab};
         for (int k = 0; k < 3; ++k) {
-            CS_TRY(cudaMemcpyAsync(&h_iscal[8 + k], tabs[k]->offset.p + tabs[k]->np, sizeof(int), cudaMemcpyDeviceToHost, s));
-            CS_TRY(cudaMemcpyAsync(&h_iscal[12 + k], tabs[k]->n_over.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + k], tabs[k]->offset.p + tabs[k]->np, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 4 + k], tabs[k]->n_over.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         }
         CS_TRY(cudaStreamSynchronize(s));
         for (int k = 0; k < 3; ++k) {
-            tabs[k]->m = h_iscal[8 + k];
-            tabs[k]->n_over_h = h_iscal[12 + k];
+            tabs[k]->m = h_iscal[I_COUNT + k];
+            tabs[k]->n_over_h = h_iscal[I_COUNT + 4 + k];
         }
         vtab.set_buckets(std::max(vtab.m, ttab.m));
         ttab.T = vtab.T;
@@ -468,6 +484,24 @@ struct cs_scene {
         CS_RET(table_build(vtab, vs, ttab.inv.p, false));
         CS_RET(table_build(ttab, ts, ttab.inv.p, true));
         CS_RET(table_build(etab, es, etab.inv.p, false));
+        // ballot buffers: warp iterations per run, scanned (one more host sync)
+        const EntryTable VT = vtab.view(), TT = ttab.view(), ET = etab.view();
+        for (EntryBuf* G : {&vtab, &etab}) {
+            CS_RET(G->iters.ensure(G->m + 1));
+            CS_RET(G->iter_off.ensure(G->m + 1));
+            CS_TRY(cudaMemsetAsync(G->iters.p, 0, sizeof(long long) * (G->m + 1), s));
+        }
+        if (vtab.m) k_run_iters<<<grid(vtab.m), 256, 0, s>>>(VT, TT, 1, vtab.iters.p);
+        if (etab.m) k_run_iters<<<grid(etab.m), 256, 0, s>>>(ET, ET, 0, etab.iters.p);
+        launches += 2;
+        CS_RET(scan(vtab.iters.p, vtab.iter_off.p, (int)vtab.m + 1));
+        CS_RET(scan(etab.iters.p, etab.iter_off.p, (int)etab.m + 1));
+        long long* hits_h = reinterpret_cast<long long*>(h_scal + S_COUNT);
+        CS_TRY(cudaMemcpyAsync(&hits_h[0], vtab.iter_off.p + vtab.m, sizeof(long long), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&hits_h[1], etab.iter_off.p + etab.m, sizeof(long long), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        CS_RET(vtab.masks.ensure(std::max<long long>(hits_h[0], 1)));
+        CS_RET(etab.masks.ensure(std::max<long long>(hits_h[1], 1)));
         // pair counts: [VT runs][VT oversize][EE runs][EE oversize]
         const int n_ovt = vtab.n_over_h + ttab.n_over_h, n_oee = etab.n_over_h;
         for (EntryBuf* G : {&vtab, &etab}) {
@@ -483,11 +517,11 @@ struct cs_scene {
         int* oo_vt = ooffset.p;
         int* oo_ee = ooffset.p + n_ovt + 1;
         const WorldTopo W = world();
-        const EntryTable VT = vtab.view(), TT = ttab.view(), ET = etab.view();
         PairOut O{};
         if (vtab.m) {
             O.counts = vtab.pcount.p;
-            k_pairs_vt<0><<<run_blocks(vtab.m), 32 * kPairWarps, 0, s>>>(VT, TT, vlo.p, vhi.p, ttab.box.p, ttab.inv.p, W, O);
+            k_pairs_vt<0><<<run_blocks(vtab.m), 32 * kPairWarps, 0, s>>>(VT, TT, vlo.p, vhi.p, ttab.box.p, ttab.inv.p, W,
+                                                                       vtab.iter_off.p, vtab.masks.p, O);
             ++launches;
         }
         if (n_ovt) {
@@ -498,7 +532,8 @@ struct cs_scene {
         }
         if (etab.m) {
             O.counts = etab.pcount.p;
-            k_pairs_ee<0><<<run_blocks(etab.m), 32 * kPairWarps, 0, s>>>(ET, etab.box.p, etab.inv.p, W, O);
+            k_pairs_ee<0><<<run_blocks(etab.m), 32 * kPairWarps, 0, s>>>(ET, etab.box.p, etab.inv.p, W,
+                                                                       etab.iter_off.p, etab.masks.p, O);
             ++launches;
         }
         if (n_oee) {
@@ -511,12 +546,12 @@ struct cs_scene {
         CS_RET(scan(oc_vt, oo_vt, n_ovt + 1));
         CS_RET(scan(etab.pcount.p, etab.poffset.p, (int)etab.m + 1));
         CS_RET(scan(oc_ee, oo_ee, n_oee + 1));
-        CS_TRY(cudaMemcpyAsync(&h_iscal[8], vtab.poffset.p + vtab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaMemcpyAsync(&h_iscal[9], oo_vt + n_ovt, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaMemcpyAsync(&h_iscal[10], etab.poffset.p + etab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaMemcpyAsync(&h_iscal[11], oo_ee + n_oee, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 0], vtab.poffset.p + vtab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], oo_vt + n_ovt, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 2], etab.poffset.p + etab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 3], oo_ee + n_oee, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaStreamSynchronize(s));
-        const long long c0 = h_iscal[8], c1 = h_iscal[9], c2 = h_iscal[10], c3 = h_iscal[11];
+        const long long c0 = h_iscal[I_COUNT + 0], c1 = h_iscal[I_COUNT + 1], c2 = h_iscal[I_COUNT + 2], c3 = h_iscal[I_COUNT + 3];
         const long long P = c0 + c1 + c2 + c3;
         CS_RET(pr.reserve(std::max<long long>(P, 1)));
         auto out_at = [&](long long base, const int* offs) {
@@ -524,14 +559,16 @@ struct cs_scene {
         };
         if (vtab.m && c0)
             k_pairs_vt<1><<<run_blocks(vtab.m), 32 * kPairWarps, 0, s>>>(VT, TT, vlo.p, vhi.p, ttab.box.p, ttab.inv.p, W,
-                                                             out_at(0, vtab.poffset.p));
+                                                                       vtab.iter_off.p, vtab.masks.p,
+                                                                       out_at(0, vtab.poffset.p));
         if (n_ovt && c1)
             k_over_vt<1><<<grid(n_ovt, 64), 64, 0, s>>>(vtab.over.p, vtab.n_over_h, ttab.over.p, ttab.n_over_h,
                                                          vtab.is_over.p, vlo.p, vhi.p, ttab.box.p, ntw, W,
                                                          out_at(c0, oo_vt));
         if (etab.m && c2)
             k_pairs_ee<1><<<run_blocks(etab.m), 32 * kPairWarps, 0, s>>>(ET, etab.box.p, etab.inv.p, W,
-                                                             out_at(c0 + c1, etab.poffset.p));
+                                                                       etab.iter_off.p, etab.masks.p,
+                                                                       out_at(c0 + c1, etab.poffset.p));
         if (n_oee && c3)
             k_over_ee<1><<<grid(n_oee, 64), 64, 0, s>>>(etab.over.p, n_oee, etab.is_over.p, etab.box.p, new_, W,
                                                         out_at(c0 + c1 + c2, oo_ee));
@@ -552,15 +589,23 @@ struct cs_scene {
         stage(T_FULL);
         const long long P = pr.P;
         if (P > 0) {
-            k_full_ccd<<<grid(P, 128), 128, 0, s>>>(pr.kind.p, pr.idx.p, xa, xb, P, P == 1 ? 1 : 0, 1e-6, pr.toi.p);
-            k_distance_toi<<<grid(P, 128), 128, 0, s>>>(pr.kind.p, pr.idx.p, xa, xb, P, 1.0 - cfg.alpha, 64,
-                                                        pr.filt.p);
-            launches += 2;
-            const int g = std::min(grid(P), 2 * sm_count);
-            CS_RET(part.ensure(g));
-            k_min_toi_partial<<<g, 256, 0, s>>>(pr.filt.p, P, part.p);
-            k_min_toi_final<<<1, 256, 0, s>>>(part.p, g, cfg.alpha, d_scal.p + S_CLAMP_MIN);
-            launches += 2;
+            // filter pass settles the provably-NaN pairs; heavy kernels run over worklists;
+            // the march minimum folds into an +inf-initialised slot
+            unsigned long long* min_slot = reinterpret_cast<unsigned long long*>(d_scal.p + S_MINBITS);
+            k_fill_u64<<<1, 32, 0, s>>>(min_slot, 1, 0x7ff0000000000000ull);
+            CS_RET(wl_full.ensure(P));
+            CS_RET(wl_dist.ensure(P));
+            CS_TRY(cudaMemsetAsync(d_iscal.p + I_WLF, 0, 2 * sizeof(int), s));
+            const SiteBoxes SB{vlo.p, vhi.p, vdisp.p, ttab.box.p, tdisp.p, etab.box.p, edisp.p, bmargin};
+            k_site_filter<<<grid(P), 256, 0, s>>>(pr.keys.p, P, SB, 1e-6, 1.0 - cfg.alpha, pr.toi.p, pr.filt.p,
+                                                  wl_full.p, wl_dist.p, d_iscal.p + I_WLF);
+            const int gw = std::max(1, std::min(grid(P, 128), 16 * sm_count));
+            k_full_ccd_wl<<<gw, 128, 0, s>>>(wl_full.p, d_iscal.p + I_WLF, pr.kind.p, pr.idx.p, xa, xb,
+                                             P == 1 ? 1 : 0, 1e-6, pr.toi.p);
+            k_distance_toi_wl<<<gw, 128, 0, s>>>(wl_dist.p, d_iscal.p + I_WLF + 1, pr.kind.p, pr.idx.p, xa, xb,
+                                                 1.0 - cfg.alpha, 64, pr.filt.p, min_slot);
+            k_clamp_from_min<<<1, 1, 0, s>>>(min_slot, cfg.alpha, d_scal.p + S_CLAMP_MIN);
+            launches += 5;
             CS_CHECK_LAUNCH();
             CS_RET(sync_scalars());
             if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;
@@ -825,6 +870,9 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(obs_next_d.ensure(std::max(3 * nobs, 1)));
     CS_RET(vlo.ensure(3LL * nw));
     CS_RET(vhi.ensure(3LL * nw));
+    CS_RET(vdisp.ensure(nw, true));
+    CS_RET(tdisp.ensure(ntw, true));
+    CS_RET(edisp.ensure(new_, true));
     CS_RET(seg_beg.ensure(nf));
     CS_RET(seg_end.ensure(nf));
     CS_RET(rhs_red.ensure(3 * 128));
@@ -837,7 +885,7 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(d_iscal.ensure(I_COUNT));
     CS_TRY(cudaMemset(d_scal.p, 0, sizeof(double) * S_COUNT));
     CS_TRY(cudaMemset(d_iscal.p, 0, sizeof(int) * I_COUNT));
-    CS_TRY(cudaMallocHost(&h_scal, sizeof(double) * S_COUNT));
+    CS_TRY(cudaMallocHost(&h_scal, sizeof(double) * (S_COUNT + 4)));  // [S_COUNT, +4): broad-phase scratch
     CS_TRY(cudaMallocHost(&h_iscal, sizeof(int) * (I_COUNT + 8)));  // [I_COUNT, +8): broad-phase scratch
     CS_RET(pa.reserve(1024));
     CS_RET(pb.reserve(1024));
@@ -856,11 +904,11 @@ void cs_scene::release() {
     DBuf<int>* ints[] = {&free_ids, &free_index, &pin_ids, &pin_slot, &e0, &e1, &rinc_ptr, &rinc, &ginc_ptr, &ginc,
                          &st, &binc_ptr, &binc, &sell_ptr, &sell_col, &hfp_ptr, &hfp_col, &wtris, &wedges,
                          &edge_tris, &edge_slot, &patch, &pslot, &sel, &skey, &ssrc, &skey_s,
-                         &ssrc_s, &seg_beg, &seg_end, &rowflag, &rows_act, &hvals, &fallback, &d_iscal};
+                         &ssrc_s, &seg_beg, &seg_end, &rowflag, &rows_act, &hvals, &fallback, &wl_full, &wl_dist, &d_iscal};
     for (auto* p : ints) p->release();
     DBuf<double>* dbl[] = {&mass, &fext, &mh2, &erest, &ew, &bk, &bw, &sell_val, &diag, &hfp_val, &U, &V, &lam,
                            &x, &v, &xprev, &df, &obs, &z, &xs_w, &xc_w, &anchor_w, &tmp_w, &xf, &xf0, &b, &t,
-                           &delta, &prev_outer, &grad, &fr, &pins_next_d, &obs_next_d, &vlo, &vhi, &sw, &stt,
+                           &delta, &prev_outer, &grad, &fr, &pins_next_d, &obs_next_d, &vlo, &vhi, &vdisp, &tdisp, &edisp, &sw, &stt,
                            &part, &part2, &rhs_red, &gram_red, &q, &Xred, &beta_red, &d_scal, &norms};
     for (auto* p : dbl) p->release();
     tri_static.release();
@@ -1271,6 +1319,28 @@ int cs_broad_phase(cs_scene* sc, const double* x_start_w, const double* x_end_w,
     CS_RET(sc->broad_phase(x_start_w, x_end_w, margin, *sc->cur));
     if (count) *count = sc->cur->P;
     CS_TRY(cudaStreamSynchronize(sc->s));
+    return 0;
+}
+
+int cs_ccd_site(cs_scene* sc, const double* x_start_w, const double* x_end_w, long long* count, double* clamp,
+                void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    double c = 1.0;
+    const int rc = sc->ccd_site(x_start_w, x_end_w, *sc->cur, nullptr, c);
+    if (count) *count = sc->cur->P;
+    if (clamp) *clamp = c;
+    CS_TRY(cudaStreamSynchronize(sc->s));
+    return rc;
+}
+
+int cs_scene_pair_results(cs_scene* sc, double* toi, double* toi_filter, void* stream) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long P = sc->cur->P;
+    if (P == 0) return 0;
+    if (toi) CS_TRY(cudaMemcpyAsync(toi, sc->cur->toi.p, sizeof(double) * P, cudaMemcpyDeviceToDevice, s));
+    if (toi_filter) CS_TRY(cudaMemcpyAsync(toi_filter, sc->cur->filt.p, sizeof(double) * P, cudaMemcpyDeviceToDevice, s));
     return 0;
 }
 

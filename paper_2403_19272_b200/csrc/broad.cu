@@ -47,6 +47,14 @@ __global__ void k_vertex_boxes(const double* __restrict__ x0, const double* __re
     vhi[i] = np_max(a, b) + margin;
 }
 
+// |x_end - x_start| per vertex, as the reference's distance march computes it (ccd.py:240)
+__global__ void k_vertex_disp(const double* __restrict__ x0, const double* __restrict__ x1, int n,
+                              double* __restrict__ vdisp) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    vdisp[v] = norm3(ld3(x1, v) - ld3(x0, v));
+}
+
 // ------------------------------------------------------------------ boxes + cell size
 // box[6p..6p+5] = lo.xyz, hi.xyz over the primitive's vertex boxes.  Block
 // partial sums of the max-axis extent (moving primitives, all primitives) for the
@@ -55,12 +63,17 @@ template <int ARITY>
 __global__ void __launch_bounds__(256) k_prim_boxes(const int* __restrict__ verts, int np,
                                                     const uint8_t* __restrict__ is_static,
                                                     const double* __restrict__ vlo, const double* __restrict__ vhi,
-                                                    double* __restrict__ box, double* __restrict__ part) {
+                                                    const double* __restrict__ vdisp, double* __restrict__ box,
+                                                    double* __restrict__ pdisp, double* __restrict__ part) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     if (p < np) {
         double lo[3], hi[3];
         const int a = verts[ARITY * p];
+        double dmax = vdisp[a];
+#pragma unroll
+        for (int k = 1; k < ARITY; ++k) dmax = fmax(dmax, vdisp[verts[ARITY * p + k]]);
+        pdisp[p] = dmax;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             lo[c] = vlo[3 * a + c];
@@ -165,16 +178,6 @@ __device__ __forceinline__ CellRange cell_range(const double lo[3], const double
     return r;
 }
 
-__device__ __forceinline__ void load_box(const double* __restrict__ box, int p, double lo[3], double hi[3]) {
-    const double2* b = reinterpret_cast<const double2*>(box + 6 * (int64_t)p);
-    const double2 a0 = b[0], a1 = b[1], a2 = b[2];
-    lo[0] = a0.x;
-    lo[1] = a0.y;
-    lo[2] = a1.x;
-    hi[0] = a1.y;
-    hi[1] = a2.x;
-    hi[2] = a2.y;
-}
 
 // Box source of a grid: primitive boxes (box != null) or vertex boxes (used vertices only).
 struct BoxSrc {
@@ -214,11 +217,17 @@ __global__ void k_cell_count(BoxSrc S, const double* __restrict__ inv_cell, int*
     over[p] = big ? 1 : 0;
 }
 
+// Low-corner bits: cell_of is monotone, so for two boxes A, B both spanning cell c,
+// cell_of(max(loA, loB)) = max(cell_of(loA), cell_of(loB)) per axis, which equals c
+// iff c is A's or B's low-corner cell on that axis.  With zb = per-axis "c is my
+// low-corner cell" bits, "the pair's min corner lies in c" is (zA | zB) == 7 -
+// the exact integer form of min_corner_in(), evaluated before any fp64 test.
 // 8 threads per primitive: thread k writes the primitive's cells k, k+8, ... in
 // (z, y, x) order (x fastest), so a warp's stores land on contiguous entries.
 __global__ void k_cell_fill(BoxSrc S, const double* __restrict__ inv_cell, unsigned mask,
                             const int* __restrict__ count, const int* __restrict__ offset,
-                            unsigned* __restrict__ key, int* __restrict__ prim, unsigned long long* __restrict__ code) {
+                            unsigned* __restrict__ key, int* __restrict__ prim, unsigned long long* __restrict__ code,
+                            uint8_t* __restrict__ zb) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int p = (int)(tid >> 3), k0 = (int)(tid & 7);
     if (p >= S.np) return;
@@ -235,19 +244,23 @@ __global__ void k_cell_fill(BoxSrc S, const double* __restrict__ inv_cell, unsig
         key[o + k] = bucket_of(c, mask);
         prim[o + k] = p;
         code[o + k] = c;
+        // which axes of this cell are the primitive's low-corner cell (see lo_corner_bits)
+        zb[o + k] = (uint8_t)((x == r.lo[0]) | ((y == r.lo[1]) << 1) | ((z == r.lo[2]) << 2));
     }
 }
 
 // sorted order -> (primitive, code) arrays; run heads; dense bucket ranges
 __global__ void k_entries_sorted(const int* __restrict__ perm, int m, const int* __restrict__ prim,
-                                 const unsigned long long* __restrict__ code, const unsigned* __restrict__ key_s,
-                                 int* __restrict__ prim_s, unsigned long long* __restrict__ code_s,
+                                 const unsigned long long* __restrict__ code, const uint8_t* __restrict__ zb,
+                                 const unsigned* __restrict__ key_s, int* __restrict__ prim_s,
+                                 unsigned long long* __restrict__ code_s, uint8_t* __restrict__ zb_s,
                                  uint8_t* __restrict__ head, int* __restrict__ bstart, int* __restrict__ bend) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     const int k = perm[i];
     prim_s[i] = prim[k];
     code_s[i] = code[k];
+    zb_s[i] = zb[k];
     const unsigned b = key_s[i];
     const bool h = i == 0 || key_s[i - 1] != b;
     head[i] = h;
@@ -262,6 +275,7 @@ struct EntryTable {
     const unsigned* __restrict__ key;           // bucket, sorted
     const int* __restrict__ prim;
     const unsigned long long* __restrict__ code;
+    const uint8_t* __restrict__ zb;             // low-corner bits
     const int* __restrict__ run;                // run heads (first entry of each bucket)
     const int* __restrict__ n_run;              // device scalar
     const int* __restrict__ bstart;             // dense bucket ranges (triangle table only)
@@ -402,22 +416,31 @@ __device__ __forceinline__ bool ee_ok(const WorldTopo& W, int E, int F) {
     return a0 != b0 && a0 != b1 && a1 != b0 && a1 != b1;
 }
 
-// Warp-level ordered emission: lanes with `hit` get consecutive rows in lane order.
-template <int PASS, typename F>
-__device__ __forceinline__ void warp_emit(bool hit, int& base, int& cnt, F&& write) {
-    const unsigned mask = __ballot_sync(0xffffffffu, hit);
-    if (PASS == 1 && hit) write(base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1u)));
-    base += __popc(mask);
-    cnt += __popc(mask);
+// Bucket-pair kernels run twice.  Pass 0 tests every candidate pair and stores
+// one 32-bit ballot word per warp iteration (masks) plus the run's hit count;
+// pass 1 replays the same loop structure reading the ballots (no box tests) and
+// writes rows at the run's scanned offset, hits in lane order.
+template <int PASS>
+__device__ __forceinline__ unsigned warp_hits(bool hit, unsigned* __restrict__ masks, int64_t it) {
+    if (PASS == 0) {
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if ((threadIdx.x & 31) == 0) masks[it] = m;
+        return m;
+    }
+    return masks[it];
+}
+__device__ __forceinline__ int lane_rank(unsigned mask) {
+    return __popc(mask & ((1u << (threadIdx.x & 31)) - 1u));
 }
 
-// Shared-memory copy of one bucket entry (box, cell code, primitive).
+// Shared-memory copy of one bucket entry: box, cell code, primitive, its vertices
+// (edge: a, b; triangle: a, b, c; vertex: a = id) and static flag.
 struct SmEntry {
     double lo[3], hi[3];
     unsigned long long code;
-    int prim, pad;
+    int prim, a, b, c, stat, z;
 };
-constexpr int kRunCap = 128;  // edge / triangle runs up to this many entries are staged in shared memory
+constexpr int kRunCap = 112;  // edge / triangle runs up to this many entries are staged in shared memory
 constexpr int kRunCapV = 32;  // vertex runs
 constexpr int kPairWarps = 4; // warps per block of the bucket-pair kernels
 
@@ -437,6 +460,32 @@ __device__ __forceinline__ void tri_index(int k, int m, int& i, int& j) {
     j = k - r * (2 * m - 1 - r) / 2 + r + 1;
 }
 
+// warp iterations a run takes (must mirror the loops below exactly)
+__device__ __forceinline__ long long iters_ee(int m) {
+    if (m < 2) return 0;
+    if (m <= kRunCap) return ((long long)m * (m - 1) / 2 + 31) / 32;
+    const long long n = m - 1, q = n / 32, r = n % 32;  // sum_{L=1..n} ceil(L/32)
+    return 32 * q * (q + 1) / 2 + (q + 1) * r;
+}
+__device__ __forceinline__ long long iters_vt(int mv, int mt) {
+    if (mt <= 0 || mv <= 0) return 0;
+    if (mv <= kRunCapV && mt <= kRunCap) return ((long long)mv * mt + 31) / 32;
+    return (long long)mv * ((mt + 31) / 32);
+}
+
+// per run: warp iterations (for the ballot buffer); entries beyond n_run stay 0
+__global__ void k_run_iters(EntryTable R, EntryTable T, int vt, long long* __restrict__ iters) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R.n_run[0]) return;
+    const int b0 = R.run[r], b1 = r + 1 < R.n_run[0] ? R.run[r + 1] : R.m;
+    if (vt) {
+        const unsigned b = R.key[b0];
+        iters[r] = iters_vt(b1 - b0, T.bend[b] - T.bstart[b]);
+    } else {
+        iters[r] = iters_ee(b1 - b0);
+    }
+}
+
 // VT: one warp per vertex-table bucket run x the same bucket's triangle entries.
 template <int PASS>
 __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, EntryTable T,
@@ -444,7 +493,8 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
                                                               const double* __restrict__ vhi,
                                                               const double* __restrict__ tbox,
                                                               const double* __restrict__ inv_cell, WorldTopo W,
-                                                              PairOut O) {
+                                                              const long long* __restrict__ iter_off,
+                                                              unsigned* __restrict__ masks, PairOut O) {
     __shared__ SmEntry smv[kPairWarps][kRunCapV], smt[kPairWarps][kRunCap];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nr = V.n_run[0];
@@ -455,42 +505,56 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
         const int tb = T.bstart[b], te = T.bend[b];
         const int mv = ve - vb, mt = te - tb;
         int base = PASS == 1 ? O.offsets[r] : 0, cnt = 0;
+        long long it = iter_off[r];
         if (mt > 0 && mv <= kRunCapV && mt <= kRunCap) {
-            for (int k = lane; k < mv; k += 32) {
-                SmEntry& e = smv[w][k];
-                const int v = V.prim[vb + k];
-                e.prim = v;
-                e.code = V.code[vb + k];
+            if (PASS == 0) {
+                for (int k = lane; k < mv; k += 32) {
+                    SmEntry& e = smv[w][k];
+                    const int v = V.prim[vb + k];
+                    e.prim = v;
+                    e.code = V.code[vb + k];
+                    e.z = V.zb[vb + k];
+                    e.stat = W.vert_static[v];
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    e.lo[c] = vlo[3 * (int64_t)v + c];
-                    e.hi[c] = vhi[3 * (int64_t)v + c];
+                    for (int c = 0; c < 3; ++c) {
+                        e.lo[c] = vlo[3 * (int64_t)v + c];
+                        e.hi[c] = vhi[3 * (int64_t)v + c];
+                    }
                 }
+                for (int k = lane; k < mt; k += 32) {
+                    SmEntry& e = smt[w][k];
+                    const int f = T.prim[tb + k];
+                    e.prim = f;
+                    e.code = T.code[tb + k];
+                    e.z = T.zb[tb + k];
+                    e.a = W.tris[3 * f];
+                    e.b = W.tris[3 * f + 1];
+                    e.c = W.tris[3 * f + 2];
+                    e.stat = W.tri_static[f];
+                    load_box(tbox, f, e.lo, e.hi);
+                }
+                __syncwarp();
             }
-            for (int k = lane; k < mt; k += 32) {
-                SmEntry& e = smt[w][k];
-                e.prim = T.prim[tb + k];
-                e.code = T.code[tb + k];
-                load_box(tbox, e.prim, e.lo, e.hi);
-            }
-            __syncwarp();
             const int np = mv * mt;
-            for (int k0 = 0; k0 < np; k0 += 32) {
+            for (int k0 = 0; k0 < np; k0 += 32, ++it) {
                 const int k = k0 + lane;
                 bool hit = false;
-                int v = 0, f = 0;
-                if (k < np) {
+                if (PASS == 0 && k < np) {
                     const int i = k / mt, j = k - i * mt;
-                    const SmEntry& a = smv[w][i];
-                    const SmEntry& c = smt[w][j];
-                    v = a.prim;
-                    f = c.prim;
-                    hit = a.code == c.code && sm_overlap(a, c) && min_corner_in(a.lo, c.lo, inv, a.code) &&
-                          vt_ok(W, v, f);
+                    const SmEntry& x = smv[w][i];
+                    const SmEntry& y = smt[w][j];
+                    hit = (x.z | y.z) == 7 && x.code == y.code && !(x.stat && y.stat) && x.prim != y.a &&
+                          x.prim != y.b && x.prim != y.c && sm_overlap(x, y);
                 }
-                warp_emit<PASS>(hit, base, cnt, [&](int row) { write_vt(O, row, v, f, W); });
+                const unsigned m = warp_hits<PASS>(hit, masks, it);
+                if (PASS == 1 && ((m >> lane) & 1u)) {
+                    const int i = k / mt, j = k - i * mt;
+                    write_vt(O, base + lane_rank(m), V.prim[vb + i], T.prim[tb + j], W);
+                }
+                base += __popc(m);
+                cnt += __popc(m);
             }
-            __syncwarp();
+            if (PASS == 0) __syncwarp();
         } else if (mt > 0) {
             for (int i = vb; i < ve; ++i) {
                 const int v = V.prim[i];
@@ -501,17 +565,19 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
                     qlo[c] = vlo[3 * (int64_t)v + c];
                     qhi[c] = vhi[3 * (int64_t)v + c];
                 }
-                for (int j0 = tb; j0 < te; j0 += 32) {
+                for (int j0 = tb; j0 < te; j0 += 32, ++it) {
                     const int j = j0 + lane;
                     bool hit = false;
-                    int f = 0;
-                    if (j < te && T.code[j] == cv) {
-                        f = T.prim[j];
+                    if (PASS == 0 && j < te && T.code[j] == cv) {
+                        const int f = T.prim[j];
                         double lo[3], hi[3];
                         load_box(tbox, f, lo, hi);
                         hit = overlap6(qlo, qhi, lo, hi) && min_corner_in(qlo, lo, inv, cv) && vt_ok(W, v, f);
                     }
-                    warp_emit<PASS>(hit, base, cnt, [&](int row) { write_vt(O, row, v, f, W); });
+                    const unsigned m = warp_hits<PASS>(hit, masks, it);
+                    if (PASS == 1 && ((m >> lane) & 1u)) write_vt(O, base + lane_rank(m), v, T.prim[j], W);
+                    base += __popc(m);
+                    cnt += __popc(m);
                 }
             }
         }
@@ -523,7 +589,8 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
 template <int PASS>
 __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_ee(EntryTable E, const double* __restrict__ ebox,
                                                               const double* __restrict__ inv_cell, WorldTopo W,
-                                                              PairOut O) {
+                                                              const long long* __restrict__ iter_off,
+                                                              unsigned* __restrict__ masks, PairOut O) {
     __shared__ SmEntry sme[kPairWarps][kRunCap];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nr = E.n_run[0];
@@ -532,49 +599,63 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_ee(EntryTable E, cons
         const int eb = E.run[r], ee = r + 1 < nr ? E.run[r + 1] : E.m;
         const int m = ee - eb;
         int base = PASS == 1 ? O.offsets[r] : 0, cnt = 0;
+        long long it = iter_off[r];
         if (m <= kRunCap) {
-            for (int k = lane; k < m; k += 32) {
-                SmEntry& e = sme[w][k];
-                e.prim = E.prim[eb + k];
-                e.code = E.code[eb + k];
-                load_box(ebox, e.prim, e.lo, e.hi);
+            if (PASS == 0) {
+                for (int k = lane; k < m; k += 32) {
+                    SmEntry& e = sme[w][k];
+                    const int q = E.prim[eb + k];
+                    e.prim = q;
+                    e.code = E.code[eb + k];
+                    e.z = E.zb[eb + k];
+                    e.a = W.edges[2 * q];
+                    e.b = W.edges[2 * q + 1];
+                    e.stat = W.edge_static[q];
+                    load_box(ebox, q, e.lo, e.hi);
+                }
+                __syncwarp();
             }
-            __syncwarp();
             const int np = m * (m - 1) / 2;
-            for (int k0 = 0; k0 < np; k0 += 32) {
+            for (int k0 = 0; k0 < np; k0 += 32, ++it) {
                 const int k = k0 + lane;
                 bool hit = false;
-                int a = 0, f = 0;
-                if (k < np) {
+                if (PASS == 0 && k < np) {
                     int i, j;
                     tri_index(k, m, i, j);
                     const SmEntry& x = sme[w][i];
                     const SmEntry& y = sme[w][j];
-                    a = x.prim;
-                    f = y.prim;
-                    hit = x.code == y.code && sm_overlap(x, y) && min_corner_in(x.lo, y.lo, inv, x.code) &&
-                          ee_ok(W, a, f);
+                    hit = (x.z | y.z) == 7 && x.code == y.code && !(x.stat && y.stat) && x.a != y.a &&
+                          x.a != y.b && x.b != y.a && x.b != y.b && sm_overlap(x, y);
                 }
-                warp_emit<PASS>(hit, base, cnt, [&](int row) { write_ee(O, row, a, f, W); });
+                const unsigned msk = warp_hits<PASS>(hit, masks, it);
+                if (PASS == 1 && ((msk >> lane) & 1u)) {
+                    int i, j;
+                    tri_index(k, m, i, j);
+                    write_ee(O, base + lane_rank(msk), E.prim[eb + i], E.prim[eb + j], W);
+                }
+                base += __popc(msk);
+                cnt += __popc(msk);
             }
-            __syncwarp();
+            if (PASS == 0) __syncwarp();
         } else {
             for (int i = eb; i + 1 < ee; ++i) {
                 const int a = E.prim[i];
                 const unsigned long long ca = E.code[i];
                 double qlo[3], qhi[3];
                 load_box(ebox, a, qlo, qhi);
-                for (int j0 = i + 1; j0 < ee; j0 += 32) {
+                for (int j0 = i + 1; j0 < ee; j0 += 32, ++it) {
                     const int j = j0 + lane;
                     bool hit = false;
-                    int f = 0;
-                    if (j < ee && E.code[j] == ca) {
-                        f = E.prim[j];
+                    if (PASS == 0 && j < ee && E.code[j] == ca) {
+                        const int f = E.prim[j];
                         double lo[3], hi[3];
                         load_box(ebox, f, lo, hi);
                         hit = overlap6(qlo, qhi, lo, hi) && min_corner_in(qlo, lo, inv, ca) && ee_ok(W, a, f);
                     }
-                    warp_emit<PASS>(hit, base, cnt, [&](int row) { write_ee(O, row, a, f, W); });
+                    const unsigned msk = warp_hits<PASS>(hit, masks, it);
+                    if (PASS == 1 && ((msk >> lane) & 1u)) write_ee(O, base + lane_rank(msk), a, E.prim[j], W);
+                    base += __popc(msk);
+                    cnt += __popc(msk);
                 }
             }
         }

@@ -70,6 +70,35 @@ __device__ __forceinline__ double np_sign(double v) {
 
 #define CS_TINY 1e-14  // reference geometry.py:7
 
+// fp64 box stored as 6 contiguous doubles lo.xyz, hi.xyz (16-byte aligned rows)
+__device__ __forceinline__ void load_box(const double* __restrict__ box, int p, double lo[3], double hi[3]) {
+    const double2* b = reinterpret_cast<const double2*>(box + 6 * (int64_t)p);
+    const double2 a0 = b[0], a1 = b[1], a2 = b[2];
+    lo[0] = a0.x;
+    lo[1] = a0.y;
+    lo[2] = a1.x;
+    hi[0] = a1.y;
+    hi[1] = a2.x;
+    hi[2] = a2.y;
+}
+
+
+// Count `flag` over the whole block with one global atomic per block (warp ballots
+// -> shared partials).  Every thread of the block must call it (integer count, so
+// the result is order independent).
+__device__ __forceinline__ void block_count(bool flag, int* __restrict__ count) {
+    __shared__ int sh_cnt[32];
+    const unsigned ballot = __ballot_sync(0xffffffffu, flag);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sh_cnt[w] = __popc(ballot);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int k = 0; k < (int)((blockDim.x + 31) >> 5); ++k) c += sh_cnt[k];
+        if (c) atomicAdd(count, c);
+    }
+}
+
 // Closest point on triangle (a,b,c) to p: reference geometry.py:10-79.
 // Returns distance; u, v = barycentric weights of b and c; q = closest point.
 __device__ __forceinline__ double pt_tri_closest(d3 p, d3 a, d3 b, d3 c, double& u, double& v, d3& q) {

@@ -149,19 +149,10 @@ __device__ __forceinline__ bool separated_sides(int kd, const Corners& a, const 
     return gap > bound * (1.0 + 1e-6) + 1e-9 * mag;
 }
 
-__global__ void k_full_ccd(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
-                           const double* __restrict__ x0, const double* __restrict__ x1, int64_t P,
-                           int single, double tol, double* __restrict__ toi_out) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= P) return;
-    const int kd = kind[i];
-    const int4 id = idx[i];
-    Corners a = gather4(x0, id), b = gather4(x1, id);
+// full_ccd for one pair (ccd.py:138-196); NaN = miss
+__device__ double full_ccd_pair(int kd, const Corners& a, const Corners& b, int single, double tol) {
     const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
-    if (separated_sides(kd, a, b, tol)) {
-        toi_out[i] = NaN;
-        return;
-    }
+    if (separated_sides(kd, a, b, tol)) return NaN;
 
     // coplanarity samples at t = 0, 1/3, 2/3, 1 and the monomial fit (ccd.py:36-44)
     const double nodes[4] = {0.0, 1.0 / 3.0, 2.0 / 3.0, 1.0};
@@ -299,7 +290,16 @@ __global__ void k_full_ccd(const int8_t* __restrict__ kind, const int4* __restri
             }
         }
     }
-    toi_out[i] = toi;
+    return toi;
+}
+
+__global__ void k_full_ccd(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+                           const double* __restrict__ x0, const double* __restrict__ x1, int64_t P,
+                           int single, double tol, double* __restrict__ toi_out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const int4 id = idx[i];
+    toi_out[i] = full_ccd_pair(kind[i], gather4(x0, id), gather4(x1, id), single, tol);
 }
 
 // gap between the boxes of the two sides at the start positions, minus a
@@ -334,14 +334,8 @@ __device__ __forceinline__ double start_gap(int kd, const Corners& a) {
     return gap - 1e-9 * mag;
 }
 
-__global__ void k_distance_toi(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
-                               const double* __restrict__ x0, const double* __restrict__ x1, int64_t P,
-                               double floor_frac, int max_iter, double* __restrict__ out) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= P) return;
-    const int kd = kind[i];
-    const int4 id = idx[i];
-    Corners a = gather4(x0, id), b = gather4(x1, id);
+// distance_toi for one pair (ccd.py:221-266)
+__device__ double distance_toi_pair(int kd, const Corners& a, const Corners& b, double floor_frac, int max_iter) {
     d3 dp[4];
     double mv[4];
 #pragma unroll
@@ -364,10 +358,7 @@ __global__ void k_distance_toi(const int8_t* __restrict__ kind, const int4* __re
     // whenever the start-box gap bounds d from below well enough (ccd.py:251-255)
     if (L > 0.0 && floor_frac < 1.0) {
         const double g = start_gap(kd, a);
-        if (g > 0.0 && g * (1.0 - floor_frac) * (1.0 - 1e-9) > L * (1.0 + 1e-9)) {
-            out[i] = NaN;
-            return;
-        }
+        if (g > 0.0 && g * (1.0 - floor_frac) * (1.0 - 1e-9) > L * (1.0 + 1e-9)) return NaN;
     }
     double d = pair_distance(kd, a.p[0], a.p[1], a.p[2], a.p[3]);
     const double goal = floor_frac * d;
@@ -394,7 +385,154 @@ __global__ void k_distance_toi(const int8_t* __restrict__ kind, const int4* __re
         }
         if (alive) toi = t;  // unresolved: safe time reached so far
     }
-    out[i] = toi;
+    return toi;
+}
+
+__global__ void k_distance_toi(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+                               const double* __restrict__ x0, const double* __restrict__ x1, int64_t P,
+                               double floor_frac, int max_iter, double* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const int4 id = idx[i];
+    out[i] = distance_toi_pair(kind[i], gather4(x0, id), gather4(x1, id), floor_frac, max_iter);
+}
+
+// One CCD site's narrow phase (stepper.py:436-441) as filter + worklists.
+// k_site_filter settles every pair whose results are provably NaN (the full_ccd
+// bound of separated_sides; the distance march's first advance leaving [0, 1],
+// or L == 0 where the reference returns 0 only for d <= 0); the rest go to two
+// worklists (warp-aggregated appends; results are written by pair index, so
+// worklist order is irrelevant).  The heavy kernels then run only over the
+// worklists, grid-striding over the device-side counts.
+__device__ __forceinline__ void wl_append(bool want, int64_t i, int* __restrict__ wl, int* __restrict__ n) {
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(n, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (want) wl[base + __popc(m & ((1u << lane) - 1u))] = (int)i;
+}
+
+// Settling works from the broad phase's primitive data of the same site (no
+// per-pair corner gathers): margin-inflated swept boxes (vertex / triangle / edge)
+// and per-primitive max displacement norms.  Removing the margin from both boxes
+// widens their gap by 2 x margin; the 1e-9 x |coordinate| slack covers the
+// rounding of the inflation, so g below is a lower bound on the true gap between
+// the two sides' swept (and hence start) positions.
+struct SiteBoxes {
+    const double* __restrict__ vlo;    // (n_w,3) vertex boxes
+    const double* __restrict__ vhi;
+    const double* __restrict__ vdisp;  // (n_w) |x_end - x_start| per vertex
+    const double* __restrict__ tbox;   // (tris,6)
+    const double* __restrict__ tdisp;  // (tris) max vertex displacement
+    const double* __restrict__ ebox;   // (edges,6)
+    const double* __restrict__ edisp;
+    double margin;
+};
+
+__global__ void __launch_bounds__(256) k_site_filter(const unsigned long long* __restrict__ keys, int64_t P,
+                                                     SiteBoxes B, double tol, double floor_frac,
+                                                     double* __restrict__ toi_out, double* __restrict__ filt_out,
+                                                     int* __restrict__ wl_full, int* __restrict__ wl_dist,
+                                                     int* __restrict__ counts) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool need_full = false, need_dist = false;
+    if (i < P) {
+        const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
+        const unsigned long long k = keys[i];
+        const int p = (int)((k >> 32) & 0x7fffffffu), q = (int)(k & 0xffffffffu);
+        double alo[3], ahi[3], blo[3], bhi[3], LA, LB;
+        if (k >> 63) {
+            load_box(B.ebox, p, alo, ahi);
+            load_box(B.ebox, q, blo, bhi);
+            LA = B.edisp[p];
+            LB = B.edisp[q];
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                alo[c] = B.vlo[3 * (int64_t)p + c];
+                ahi[c] = B.vhi[3 * (int64_t)p + c];
+            }
+            load_box(B.tbox, q, blo, bhi);
+            LA = B.vdisp[p];
+            LB = B.tdisp[q];
+        }
+        double gm = -INFINITY, e2 = 0.0, mag = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            gm = fmax(gm, fmax(blo[c] - ahi[c], alo[c] - bhi[c]));
+            const double lo = fmin(alo[c], blo[c]), hi = fmax(ahi[c], bhi[c]);
+            e2 += (hi - lo) * (hi - lo);
+            mag = fmax(mag, fmax(fabs(lo), fabs(hi)));
+        }
+        const double g = (gm + 2.0 * B.margin) - 1e-9 * mag;
+        const double ext = sqrt(e2);
+        const double bound = fmax(tol * fmax(2.0 * ext, 1.0), 1e-9 * fmax(ext, 1.0));
+        need_full = !(g > bound * (1.0 + 1e-6));
+        if (!need_full) toi_out[i] = NaN;
+        const double L = LA + LB;
+        bool settled = false;
+        if (g > 0.0) {
+            if (!(L > 0.0)) settled = L == 0.0;  // d > 0 and L == 0: never alive
+            else if (floor_frac < 1.0) settled = g * (1.0 - floor_frac) * (1.0 - 1e-9) > L * (1.0 + 1e-9);
+        }
+        need_dist = !settled;
+        if (settled) filt_out[i] = NaN;
+    }
+    wl_append(need_full, i, wl_full, counts);
+    wl_append(need_dist, i, wl_dist, counts + 1);
+}
+
+__global__ void __launch_bounds__(128) k_full_ccd_wl(const int* __restrict__ wl, const int* __restrict__ count,
+                                                     const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+                                                     const double* __restrict__ x0, const double* __restrict__ x1,
+                                                     int single, double tol, double* __restrict__ toi_out) {
+    const int n = count[0];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int i = wl[k];
+        const int4 id = idx[i];
+        toi_out[i] = full_ccd_pair(kind[i], gather4(x0, id), gather4(x1, id), single, tol);
+    }
+}
+
+// distance march over its worklist + the minimum folded with one atomicMin on the
+// (non-negative) fp64 bit pattern per block - exact and order independent.
+// min_slot must hold +inf before the launch.
+__global__ void __launch_bounds__(128) k_distance_toi_wl(const int* __restrict__ wl, const int* __restrict__ count,
+                                                         const int8_t* __restrict__ kind,
+                                                         const int4* __restrict__ idx, const double* __restrict__ x0,
+                                                         const double* __restrict__ x1, double floor_frac,
+                                                         int max_iter, double* __restrict__ out,
+                                                         unsigned long long* __restrict__ min_slot) {
+    const int n = count[0];
+    double m = __longlong_as_double(0x7ff0000000000000ULL);
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int i = wl[k];
+        const int4 id = idx[i];
+        const double f = distance_toi_pair(kind[i], gather4(x0, id), gather4(x1, id), floor_frac, max_iter);
+        out[i] = f;
+        if (f == f) m = fmin(m, f);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_down_sync(0xffffffffu, m, o));
+    __shared__ double sm[4];
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, sm[w]);
+        if (m < __longlong_as_double(0x7ff0000000000000ULL))
+            atomicMin(min_slot, (unsigned long long)__double_as_longlong(m));
+    }
+}
+
+// clamp factor from the folded minimum (stepper.py:445-452)
+__global__ void k_clamp_from_min(const unsigned long long* __restrict__ min_slot, double alpha,
+                                 double* __restrict__ out) {
+    const double t = __longlong_as_double((long long)min_slot[0]);
+    const bool none = isinf(t);
+    out[0] = t;
+    out[1] = none ? 1.0 : alpha * t;
+    out[2] = (!none && t <= 0.0) ? 1.0 : 0.0;
 }
 
 // Witness refresh: bary/params, distance and separating normal (stepper.py:194-216).
@@ -522,10 +660,7 @@ __global__ void k_partial_ndb(const int8_t* __restrict__ kind, const int4* __res
     weight[i] = eng ? ndb_weight(lf, k_ndb, base) : 0.0;
     if (write_active) active_out[i] = act;
     }
-    if (eng_count != nullptr) {
-        const unsigned ballot = __ballot_sync(0xffffffffu, eng);
-        if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(eng_count, __popc(ballot));
-    }
+    if (eng_count != nullptr) block_count(eng, eng_count);
 }
 
 // Engaged set and weights after a full-CCD site (stepper.py:483-487, 564-565).
@@ -540,10 +675,7 @@ __global__ void k_engage_init(const double* __restrict__ toi, const double* __re
         engaged[i] = eng;
         weight[i] = eng ? ndb_weight(life[i], k_ndb, base) : 0.0;
     }
-    if (eng_count != nullptr) {
-        const unsigned ballot = __ballot_sync(0xffffffffu, eng);
-        if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(eng_count, __popc(ballot));
-    }
+    if (eng_count != nullptr) block_count(eng, eng_count);
 }
 
 // Per engaged pair: 4 positional targets (stepper.py:238-285).  Entries for

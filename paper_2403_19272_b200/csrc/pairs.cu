@@ -70,22 +70,19 @@ __global__ void k_flag_engaged(const uint8_t* __restrict__ engaged, const double
         f = engaged[i] && (weight[i] > 0.0);
         flags[i] = f;
     }
-    const unsigned ballot = __ballot_sync(0xffffffffu, f);
-    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(count, __popc(ballot));
+    block_count(f, count);
 }
 
 __global__ void k_count_nonzero(const int* __restrict__ v, int64_t P, int* __restrict__ count) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool f = i < P && v[i] != 0;
-    const unsigned ballot = __ballot_sync(0xffffffffu, f);
-    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(count, __popc(ballot));
+    block_count(f, count);
 }
 
 __global__ void k_count_true(const uint8_t* __restrict__ v, int64_t P, int* __restrict__ count) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool f = i < P && v[i];
-    const unsigned ballot = __ballot_sync(0xffffffffu, f);
-    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(count, __popc(ballot));
+    block_count(f, count);
 }
 
 // sorted keys (free row, or 0x7fffffff for dropped) -> seg_beg/seg_end per row,

@@ -303,3 +303,42 @@ class Simulation:
         kind = kind[:P].cpu().numpy()
         idx = idx[:P].cpu().numpy().astype(np.int64)
         return PairSet(kind=kind, idx=idx, life_span=np.zeros(P, np.int64), weight=np.zeros(P))
+
+    def _full_ccd_site(self, x_from_w, x_to_w, report=None):
+        """Broad phase + full CCD + distance march of one CCD site on the device
+        (reference stepper.py:426-443); returns (pairs, toi, toi_filter) as numpy.
+        The clamp of stepper.py:445-452 is applied by ``_clamp``."""
+        import torch
+
+        a, b = self._dbuf(x_from_w), self._dbuf(x_to_w)
+        count = ctypes.c_longlong(0)
+        clamp = ctypes.c_double(1.0)
+        rc = self._lib.cs_ccd_site(self._scene, a.data_ptr(), b.data_ptr(), ctypes.byref(count), ctypes.byref(clamp),
+                                   self._stream())
+        if rc not in (_lib.CS_OK, _lib.CS_PENETRATION):
+            _lib.check(rc, "cs_ccd_site")
+        P = count.value
+        n = max(P, 1)
+        kind = torch.empty(n, dtype=torch.int8, device="cuda")
+        idx = torch.empty((n, 4), dtype=torch.int32, device="cuda")
+        toi = torch.empty(n, dtype=torch.float64, device="cuda")
+        filt = torch.empty(n, dtype=torch.float64, device="cuda")
+        _lib.check(self._lib.cs_scene_pairs(self._scene, kind.data_ptr(), idx.data_ptr(), self._stream()),
+                   "cs_scene_pairs")
+        _lib.check(self._lib.cs_scene_pair_results(self._scene, toi.data_ptr(), filt.data_ptr(), self._stream()),
+                   "cs_scene_pair_results")
+        if report is not None:
+            report.full_ccd_calls += 1
+        pairs = PairSet(kind=kind[:P].cpu().numpy(), idx=idx[:P].cpu().numpy().astype(np.int64),
+                        life_span=np.zeros(P, np.int64), weight=np.zeros(P))
+        return pairs, toi[:P].cpu().numpy(), filt[:P].cpu().numpy()
+
+    def _clamp(self, toi: np.ndarray) -> float:
+        """stepper.py:445-452."""
+        finite = toi[~np.isnan(toi)]
+        if finite.size == 0:
+            return 1.0
+        t = float(finite.min())
+        if t <= 0.0:
+            raise PenetrationError("impact at t<=0: step began in contact")
+        return self.config.alpha * t

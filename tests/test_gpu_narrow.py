@@ -143,3 +143,32 @@ def test_pair_witness_degenerate(cuda):
     pr = Pairs(kind, idx)
     OracleSimulation.witness_into(None, pr, x)
     assert np.array_equal(nrm, pr.normal) and np.array_equal(bary, pr.bary) and np.array_equal(dist, pr.dist)
+
+
+def _same(a, b):
+    return np.array_equal(np.isnan(a), np.isnan(b)) and np.array_equal(a[~np.isnan(a)], b[~np.isnan(b)])
+
+
+@pytest.mark.parametrize("steps,jitter,move", [(0, 0.0, 2e-3), (12, 0.0, 1e-3), (6, 2e-4, 5e-4), (3, 0.0, 0.0)])
+def test_ccd_site_matches_oracle(cuda, rng, steps, jitter, move):
+    """The step's CCD site (broad phase + filter/worklist narrow phase) returns, pair for
+    pair, exactly the oracle's full_ccd and distance_toi values (bitwise, NaN-aware),
+    including motion-free sites (exit line search) and grazing contact."""
+    import paper_2403_19272_b200 as P
+    from oracle import narrow
+
+    sim = P.build_scene("sphere_drape", resolution=14, size=0.2, config=P.StepConfig())
+    for _ in range(steps):
+        sim.step()
+    x0 = sim.world(sim.state.x)
+    x0 = x0 + jitter * rng.normal(size=x0.shape)
+    x1 = x0 + move * rng.normal(size=x0.shape)
+    x1[len(sim.state.x):] = x0[len(sim.state.x):]
+    pairs, toi, filt = sim._full_ccd_site(x0, x1)
+    assert len(pairs) > 0
+    ref_toi = narrow.full_ccd(pairs.kind, pairs.idx, x0, x1)
+    ref_filt = narrow.distance_toi(pairs.kind, pairs.idx, x0, x1, floor_frac=1.0 - sim.config.alpha)
+    assert _same(toi, ref_toi)
+    assert _same(filt, ref_filt)
+    if steps == 12 or move == 0.0:
+        assert (~np.isnan(ref_filt)).any() or move == 0.0

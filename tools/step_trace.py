@@ -17,6 +17,7 @@ if which == "skirt":
 else:
     sim = P.build_scene(which, resolution=int(sys.argv[3]) if len(sys.argv) > 3 else 64, config=cfg)
 for i in range(steps):
+    print(f"--- step {i}", file=sys.stderr, flush=True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     r = sim.step()

@@ -1,0 +1,58 @@
+"""Device timeline of a few steps via torch.profiler (CUPTI): busy vs idle time,
+largest idle gaps and what precedes them (diagnostic, GPU box)."""
+import json
+import sys
+
+import torch
+from torch.profiler import ProfilerActivity, profile
+
+sys.path.insert(0, ".")
+import paper_2403_19272_b200 as P  # noqa: E402
+from paper_2403_19272_b200 import scenes as S  # noqa: E402
+
+cfg = P.StepConfig(h=1.0 / 200.0)
+sim = S.skirt_scene(cfg, around=584, down=584, eigensolver="device")
+for _ in range(4):
+    sim.step()
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+    for _ in range(2):
+        sim.step()
+    torch.cuda.synchronize()
+prof.export_chrome_trace("gpurun_out/timeline.json")
+ev = json.load(open("gpurun_out/timeline.json"))["traceEvents"]
+dev = [e for e in ev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
+dev.sort(key=lambda e: e["ts"])
+t0, t1 = dev[0]["ts"], max(e["ts"] + e["dur"] for e in dev)
+busy = sum(e["dur"] for e in dev)
+print(f"window {(t1 - t0) / 1e3:.2f} ms, device busy {busy / 1e3:.2f} ms, events {len(dev)}")
+by = {}
+for e in dev:
+    k = e["cat"] + ":" + e["name"][:60]
+    by.setdefault(k, [0, 0.0])
+    by[k][0] += 1
+    by[k][1] += e["dur"]
+for k, (c, d) in sorted(by.items(), key=lambda x: -x[1][1])[:25]:
+    print(f"{d / 1e3:8.3f} ms {c:5d}  {k}")
+gaps = []
+end = dev[0]["ts"] + dev[0]["dur"]
+prev = dev[0]
+for e in dev[1:]:
+    if e["ts"] > end:
+        gaps.append((e["ts"] - end, prev["name"][:50], e["name"][:50]))
+    if e["ts"] + e["dur"] > end:
+        end = e["ts"] + e["dur"]
+        prev = e
+gaps.sort(reverse=True)
+print(f"idle total {sum(g[0] for g in gaps) / 1e3:.2f} ms in {len(gaps)} gaps; largest:")
+for g in gaps[:25]:
+    print(f"  {g[0]:8.1f} us after {g[1]} -> before {g[2]}")
+cpu = [e for e in ev if e.get("ph") == "X" and e.get("cat") == "cuda_runtime"]
+byc = {}
+for e in cpu:
+    byc.setdefault(e["name"], [0, 0.0])
+    byc[e["name"]][0] += 1
+    byc[e["name"]][1] += e["dur"]
+print("host CUDA runtime calls:")
+for k, (c, d) in sorted(byc.items(), key=lambda x: -x[1][1])[:12]:
+    print(f"{d / 1e3:8.3f} ms {c:5d}  {k}")
