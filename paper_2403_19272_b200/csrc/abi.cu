@@ -204,7 +204,7 @@ struct cs_scene {
     DBuf<double> sw, stt;
     DBuf<unsigned long long> hkeys;
     DBuf<int> hvals;
-    DBuf<double> part, part2, rhs_red, gram_red, q, Xred, beta_red, norms;
+    DBuf<double> part, part2, spart, rhs_red, gram_red, q, Xred, beta_red, norms;
     int pending_checks = 0;
     DBuf<int> fallback;
     DBuf<int> wl_full, wl_dist;
@@ -280,25 +280,62 @@ struct cs_scene {
     // rank-2 A-Jacobi on x (nf,3) in place (smoothing.py:23-66).  The residual
     // norms at k = 0, 10, 20, ... are kept on device and compared at the next
     // host sync (check_divergence): a diverging step is discarded either way.
+    // The 2 x 16 SpMV passes (+ norm checks) of one smoothing call are captured once
+    // per distinct argument set into a CUDA graph and replayed: back-to-back
+    // dependent launches without per-launch host overhead or launch gaps.
+    struct SmoothGraph {
+        const double* bb;
+        const double* xx;
+        const double* dl;
+        const double* part;
+        const double* norms;
+        int steps;
+        double c;
+        cudaGraphExec_t exec;
+    };
+    std::vector<SmoothGraph> smooth_graphs;
+    cudaStream_t cap_stream = nullptr;
+
+    void smooth_launch(cudaStream_t st, const double* bb, double* xx, int steps, double c, const double* dl) {
+        const int g = grid(nf);
+        for (int k = 0; k < steps; ++k) {
+            const bool chk = (k % 10) == 0;
+            k_jacobi_a<<<g, 256, 0, st>>>(sell(), diag.p, dl, bb, xx, t.p, chk ? spart.p : nullptr);
+            if (chk) k_norm_final<<<1, 256, 0, st>>>(spart.p, g, norms.p + k / 10);
+            k_jacobi_b<<<g, 256, 0, st>>>(sell(), diag.p, dl, t.p, c, xx);
+        }
+    }
+
     int smooth(const double* bb, double* xx, int iterations, double omega, const double* dl) {
         const int steps = (iterations + 1) / 2;
         const double c = 1.0 - omega;
         const int g = grid(nf);
-        CS_RET(part.ensure(g));
+        CS_RET(spart.ensure(g));
         const int nchk = (steps + 9) / 10;
         CS_RET(norms.ensure(std::max(nchk, 1)));
-        for (int k = 0; k < steps; ++k) {
-            const bool chk = (k % 10) == 0;
-            k_jacobi_a<<<g, 256, 0, s>>>(sell(), diag.p, dl, bb, xx, t.p, chk ? part.p : nullptr);
-            if (chk) {
-                k_norm_final<<<1, 256, 0, s>>>(part.p, g, norms.p + k / 10);
-                ++launches;
-            }
-            k_jacobi_b<<<g, 256, 0, s>>>(sell(), diag.p, dl, t.p, c, xx);
-            launches += 2;
-            CS_CHECK_LAUNCH();
-        }
+        launches += 2LL * steps + nchk;
         pending_checks = nchk;
+        for (auto& sg : smooth_graphs)
+            if (sg.bb == bb && sg.xx == xx && sg.dl == dl && sg.part == spart.p && sg.norms == norms.p &&
+                sg.steps == steps && sg.c == c) {
+                CS_TRY(cudaGraphLaunch(sg.exec, s));
+                return 0;
+            }
+        if (!cap_stream) CS_TRY(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+        cudaGraph_t graph;
+        CS_TRY(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+        smooth_launch(cap_stream, bb, xx, steps, c, dl);
+        CS_TRY(cudaStreamEndCapture(cap_stream, &graph));
+        cudaGraphExec_t exec;
+        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CS_TRY(e);
+        if (smooth_graphs.size() >= 8) {
+            cudaGraphExecDestroy(smooth_graphs.front().exec);
+            smooth_graphs.erase(smooth_graphs.begin());
+        }
+        smooth_graphs.push_back(SmoothGraph{bb, xx, dl, spart.p, norms.p, steps, c, exec});
+        CS_TRY(cudaGraphLaunch(exec, s));
         return 0;
     }
 
@@ -894,6 +931,10 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
 }
 
 void cs_scene::release() {
+    for (auto& sg : smooth_graphs) cudaGraphExecDestroy(sg.exec);
+    smooth_graphs.clear();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    cap_stream = nullptr;
     for (auto e : ev_pool) cudaEventDestroy(e);
     ev_pool.clear();
     if (h_scal) cudaFreeHost(h_scal);
@@ -909,7 +950,7 @@ void cs_scene::release() {
     DBuf<double>* dbl[] = {&mass, &fext, &mh2, &erest, &ew, &bk, &bw, &sell_val, &diag, &hfp_val, &U, &V, &lam,
                            &x, &v, &xprev, &df, &obs, &z, &xs_w, &xc_w, &anchor_w, &tmp_w, &xf, &xf0, &b, &t,
                            &delta, &prev_outer, &grad, &fr, &pins_next_d, &obs_next_d, &vlo, &vhi, &vdisp, &tdisp, &edisp, &sw, &stt,
-                           &part, &part2, &rhs_red, &gram_red, &q, &Xred, &beta_red, &d_scal, &norms};
+                           &part, &part2, &spart, &rhs_red, &gram_red, &q, &Xred, &beta_red, &d_scal, &norms};
     for (auto* p : dbl) p->release();
     tri_static.release();
     vert_static.release();

@@ -30,20 +30,50 @@ struct Sell {
     const double* __restrict__ val;
 };
 
-// y_row = H[row, :] @ x (3 right-hand sides), scipy csr_matvecs order
+// y_row = H[row, :] @ x (3 right-hand sides), scipy csr_matvecs order.
+// Padding sits only at the end of a row (col = -1), so skipping it keeps the
+// sequential CSR summation order.  The (col, val) stream is read 4 slots at a time
+// with all loads issued before the dependent x gathers (memory-level parallelism
+// instead of a load-use chain per nonzero).
 __device__ __forceinline__ d3 sell_row(const Sell& H, int row, const double* __restrict__ x) {
     const int s = row >> 5, lane = row & 31;
     const int beg = H.slice_ptr[s], width = (H.slice_ptr[s + 1] - beg) >> 5;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     const int* cp = H.col + beg + lane;
     const double* vp = H.val + beg + lane;
-    for (int k = 0; k < width; ++k) {
+    int k = 0;
+    for (; k + 4 <= width; k += 4) {
+        int c[4];
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            c[u] = __ldg(cp + 32 * (k + u));
+            v[u] = __ldg(vp + 32 * (k + u));
+        }
+        double g[4][3];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int cc = c[u] < 0 ? 0 : c[u];
+            g[u][0] = __ldg(x + 3 * cc);
+            g[u][1] = __ldg(x + 3 * cc + 1);
+            g[u][2] = __ldg(x + 3 * cc + 2);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (c[u] >= 0) {
+                a0 = a0 + v[u] * g[u][0];
+                a1 = a1 + v[u] * g[u][1];
+                a2 = a2 + v[u] * g[u][2];
+            }
+        }
+    }
+    for (; k < width; ++k) {
         const int c = __ldg(cp + 32 * k);
         if (c < 0) break;
         const double v = __ldg(vp + 32 * k);
-        a0 = a0 + v * x[3 * c];
-        a1 = a1 + v * x[3 * c + 1];
-        a2 = a2 + v * x[3 * c + 2];
+        a0 = a0 + v * __ldg(x + 3 * c);
+        a1 = a1 + v * __ldg(x + 3 * c + 1);
+        a2 = a2 + v * __ldg(x + 3 * c + 2);
     }
     return d3{a0, a1, a2};
 }
