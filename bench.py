@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--workload", default="skirt", choices=["skirt", "batch", "small"])
     ap.add_argument("--resolution", type=int, default=584)
     ap.add_argument("--batch-scenes", type=int, default=64)
+    ap.add_argument("--streams", type=int, default=8, help="worker streams for multi-scene workloads")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -111,8 +112,13 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
+        # one process per GPU; BENCH_DIST_BACKEND=gloo lets the N>1 plumbing be
+        # exercised with several ranks sharing one device (collectives are only the
+        # barrier and the max-over-ranks timing reduction - nothing on the hot path)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     return ws, rank, local
 
 
@@ -122,7 +128,8 @@ def max_over_ranks(v: float, ws: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -144,8 +151,9 @@ def make_scenes(args, rank: int, ws: int):
             f"skirt_{args.resolution}x{args.resolution} (config 4)"
     if args.workload == "small":
         return [P.build_scene("sphere_drape", resolution=64, size=0.5, config=cfg)], "sphere_drape_64 (smoke)"
-    per = args.batch_scenes // ws
-    ids = range(rank * per, (rank + 1) * per)
+    from paper_2403_19272_b200.batch import scene_shard
+
+    ids = scene_shard(args.batch_scenes, ws, rank)
     return [S.drape_scene(i, resolution=317, config=cfg, eigensolver="device") for i in ids], \
         f"drape_batch {args.batch_scenes}x317^2 (config 5)"
 
@@ -280,6 +288,65 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+class Stepper:
+    """Steps a list of scenes, optionally over K worker streams (one host thread per
+    stream; the C ABI releases the GIL, so independent scenes overlap on the GPU).
+    Device time is bracketed by events on the caller's stream, which the workers
+    wait on / join back into."""
+
+    def __init__(self, sims, n_streams: int):
+        import torch
+
+        self.sims = sims
+        self.k = max(1, min(n_streams, len(sims)))
+        self.streams = [torch.cuda.Stream() for _ in range(self.k)] if self.k > 1 else []
+
+    def run(self, steps: int, record=None, on_step=None):
+        import threading
+
+        import torch
+
+        main = torch.cuda.current_stream()
+        if self.k == 1:
+            for _ in range(steps):
+                for s in self.sims:
+                    rep = s.step()
+                    if record is not None:
+                        record.append((rep, s.last_report_c))
+                    if on_step is not None:
+                        on_step(s)
+            return
+        start = torch.cuda.Event()
+        start.record(main)
+        errs, lock = [], threading.Lock()
+
+        def work(w):
+            try:
+                st = self.streams[w]
+                st.wait_event(start)
+                with torch.cuda.stream(st):
+                    for _ in range(steps):
+                        for s in self.sims[w::self.k]:
+                            rep = s.step()
+                            if record is not None:
+                                with lock:
+                                    record.append((rep, s.last_report_c))
+                            if on_step is not None:
+                                on_step(s)
+            except BaseException as e:  # surface worker errors
+                errs.append(e)
+
+        th = [threading.Thread(target=work, args=(w,)) for w in range(self.k)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+        for st in self.streams:
+            main.wait_stream(st)
+
+
 def run_ours(args, ws, rank, local):
     import torch
 
@@ -293,18 +360,15 @@ def run_ours(args, ws, rank, local):
     sims, workload = make_scenes(args, rank, ws)
     setup_s = time.time() - t_setup
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        for s in sims:
-            s.step()
+    stepper = Stepper(sims, args.streams)
+    stepper.run(args.warmup)
     barrier(ws)
     torch.cuda.synchronize()
     reps = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
-            for s in sims:
-                reps.append((s.step(), s.last_report_c))
+        stepper.run(args.steps, record=reps)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier(ws)
@@ -322,10 +386,7 @@ def run_ours(args, ws, rank, local):
         barrier(ws)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(k_e2e):
-            for s in sims:
-                s.step()
-                _ = s.state.x          # D2H of the step's result
+        stepper.run(k_e2e, on_step=lambda s: s.state.x)   # D2H of each step's result
         torch.cuda.synchronize()
         wall = max_over_ranks(time.perf_counter() - t0, ws)
         e2e = {"value": scenes_total * k_e2e / wall, "unit": "FPS", "h2d_bytes_per_step": int(h2d),

@@ -11,7 +11,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:k_|Device|cu
     --log-file "$OUT/launches.csv" python bench.py $ARGS > "$OUT/ncu_launches.log" 2>&1
 echo "launch list rc=$?"
 for K in ${KERNELS:-k_query_ee k_jacobi_a}; do
-  ncu --set full --clock-control none --import-source on -k "regex:${K}" --launch-skip ${SKIP:-3} -c 1 \
+  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:${K}" --launch-skip ${SKIP:-3} -c 1 \
       -o "$OUT/full_${K}" -f python bench.py $ARGS > "$OUT/ncu_full_${K}.log" 2>&1
   echo "full $K rc=$?"
 done
