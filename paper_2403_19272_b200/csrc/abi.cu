@@ -643,6 +643,13 @@ struct cs_scene {
                                                  1.0 - cfg.alpha, 64, pr.filt.p, min_slot);
             k_clamp_from_min<<<1, 1, 0, s>>>(min_slot, cfg.alpha, d_scal.p + S_CLAMP_MIN);
             launches += 5;
+            static const bool trace_sites = std::getenv("CS_TRACE_SITES") != nullptr;
+            if (trace_sites) {
+                int wl[2];
+                cudaMemcpyAsync(wl, d_iscal.p + I_WLF, sizeof(wl), cudaMemcpyDeviceToHost, s);
+                cudaStreamSynchronize(s);
+                std::fprintf(stderr, "[cs site] pairs %lld full-ccd worklist %d march worklist %d\n", P, wl[0], wl[1]);
+            }
             CS_CHECK_LAUNCH();
             CS_RET(sync_scalars());
             if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;
@@ -735,11 +742,18 @@ struct cs_scene {
         launches += 2;
         // stable sort of the 4A entries by free row keeps np.add.at's per-vertex order
         bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey.p, skey_s.p, ssrc.p, ssrc_s.p, (int)m, 0, 31, s);
+        // keys are free rows < nf or the 0x7fffffff sentinel: sort only the bits a row needs,
+        // with the sentinel clamped to 2^bits - 1 (still after every real row)
+        int bits = 1;
+        while ((1LL << bits) <= (long long)nf) ++bits;
+        k_clamp_keys<<<grid(m), 256, 0, s>>>(skey.p, (int)m, (1 << bits) - 1);
+        ++launches;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey.p, skey_s.p, ssrc.p, ssrc_s.p, (int)m, 0, bits, s);
         CS_RET(cub_tmp.ensure(bytes));
-        CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, skey.p, skey_s.p, ssrc.p, ssrc_s.p, (int)m, 0, 31, s));
+        CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, skey.p, skey_s.p, ssrc.p, ssrc_s.p, (int)m, 0, bits,
+                                               s));
         CS_TRY(cudaMemsetAsync(rowflag.p, 0, sizeof(int) * m, s));
-        k_mark_segments<<<grid(m), 256, 0, s>>>(skey_s.p, (int)m, seg_beg.p, seg_end.p, rowflag.p);
+        k_mark_segments<<<grid(m), 256, 0, s>>>(skey_s.p, (int)m, nf, seg_beg.p, seg_end.p, rowflag.p);
         ++launches;
         bytes = 0;
         cub::DeviceSelect::Flagged(nullptr, bytes, skey_s.p, rowflag.p, rows_act.p, d_iscal.p + I_ROWS, (int)m, s);
@@ -1422,7 +1436,7 @@ int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const int* c
         CS_TRY(cub::DeviceRadixSort::SortPairs(sc->cub_tmp.p, bytes, sc->skey.p, sc->skey_s.p, sc->ssrc.p,
                                                sc->ssrc_s.p, m, 0, 31, s));
         CS_TRY(cudaMemsetAsync(sc->rowflag.p, 0, sizeof(int) * m, s));
-        k_mark_segments<<<sc->grid(m), 256, 0, s>>>(sc->skey_s.p, m, sc->seg_beg.p, sc->seg_end.p, sc->rowflag.p);
+        k_mark_segments<<<sc->grid(m), 256, 0, s>>>(sc->skey_s.p, m, sc->nf, sc->seg_beg.p, sc->seg_end.p, sc->rowflag.p);
         CS_CHECK_LAUNCH();
         with = true;
     }
@@ -1506,7 +1520,7 @@ int cs_energy_gradient(cs_scene* sc, const double* x, const double* z, const int
         CS_TRY(cub::DeviceRadixSort::SortPairs(sc->cub_tmp.p, bytes, sc->skey.p, sc->skey_s.p, sc->ssrc.p,
                                                sc->ssrc_s.p, m, 0, 31, s));
         CS_TRY(cudaMemsetAsync(sc->rowflag.p, 0, sizeof(int) * m, s));
-        k_mark_segments<<<sc->grid(m), 256, 0, s>>>(sc->skey_s.p, m, sc->seg_beg.p, sc->seg_end.p, sc->rowflag.p);
+        k_mark_segments<<<sc->grid(m), 256, 0, s>>>(sc->skey_s.p, m, sc->nf, sc->seg_beg.p, sc->seg_end.p, sc->rowflag.p);
         with = true;
     }
     k_energy_grad<<<sc->grid(sc->n), 256, 0, s>>>(sc->n, x, z, sc->mass.p, sc->cfg.h, sc->edges(), sc->ginc_ptr.p,

@@ -236,10 +236,12 @@ __global__ void k_cell_fill(BoxSrc S, const double* __restrict__ inv_cell, unsig
     double lo[3], hi[3];
     S.load(p, lo, hi);
     const CellRange r = cell_range(lo, hi, inv_cell[0]);
-    const long long sx = r.hi[0] - r.lo[0] + 1, sy = r.hi[1] - r.lo[1] + 1;
+    // n <= kMaxCellsPerPrim, so the per-axis spans fit 32-bit arithmetic
+    const int sx = (int)(r.hi[0] - r.lo[0] + 1), sxy = sx * (int)(r.hi[1] - r.lo[1] + 1);
     const int o = offset[p];
     for (int k = k0; k < n; k += 8) {
-        const long long x = r.lo[0] + k % sx, y = r.lo[1] + (k / sx) % sy, z = r.lo[2] + k / (sx * sy);
+        const int kz = k / sxy, rem = k - kz * sxy, ky = rem / sx, kx = rem - ky * sx;
+        const long long x = r.lo[0] + kx, y = r.lo[1] + ky, z = r.lo[2] + kz;
         const unsigned long long c = cell_code(x, y, z);
         key[o + k] = bucket_of(c, mask);
         prim[o + k] = p;
@@ -585,14 +587,53 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
     }
 }
 
-// EE: one warp per edge-table bucket run; all entry pairs i < j of the run.
+// Round-robin enumeration of the m(m-1)/2 unordered entry pairs of a run: k ->
+// (offset d, i), j = (i + d) mod m; offsets 1 .. ceil(m/2)-1 take all m rows, and
+// for even m the offset m/2 takes rows i < m/2 only.  Division by m via a float
+// reciprocal with one correction (k < 2^13, exact).  The hit test is symmetric, so
+// (i, j) orientation does not matter; pass 1 replays the same mapping.
+__device__ __forceinline__ void rr_index(int k, int m, float inv_m, int& i, int& j) {
+    const int half = m >> 1;
+    const int full = (m & 1) ? m * half : m * (half - 1);
+    int d;
+    if (k < full) {
+        int q = (int)((float)k * inv_m);
+        int r = k - q * m;
+        if (r < 0) {
+            --q;
+            r += m;
+        } else if (r >= m) {
+            ++q;
+            r -= m;
+        }
+        d = q + 1;
+        i = r;
+    } else {
+        d = half;
+        i = k - full;
+    }
+    j = i + d;
+    if (j >= m) j -= m;
+}
+
+// EE per-warp staging, structure of arrays (conflict-free lane access); the static
+// flag rides in bit 3 of the low-corner byte
+struct EeStage {
+    double lo[3][kRunCap], hi[3][kRunCap];
+    unsigned long long code[kRunCap];
+    int a[kRunCap], b[kRunCap];
+    unsigned char zs[kRunCap];
+};
+
+// EE: one warp per edge-table bucket run; all unordered entry pairs of the run.
 template <int PASS>
 __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_ee(EntryTable E, const double* __restrict__ ebox,
                                                               const double* __restrict__ inv_cell, WorldTopo W,
                                                               const long long* __restrict__ iter_off,
                                                               unsigned* __restrict__ masks, PairOut O) {
-    __shared__ SmEntry sme[kPairWarps][kRunCap];
+    __shared__ EeStage sme[kPairWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    EeStage& S = sme[w];
     const int nr = E.n_run[0];
     const double inv = inv_cell[0];
     for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nr; r += (gridDim.x * blockDim.x) >> 5) {
@@ -603,34 +644,39 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_ee(EntryTable E, cons
         if (m <= kRunCap) {
             if (PASS == 0) {
                 for (int k = lane; k < m; k += 32) {
-                    SmEntry& e = sme[w][k];
                     const int q = E.prim[eb + k];
-                    e.prim = q;
-                    e.code = E.code[eb + k];
-                    e.z = E.zb[eb + k];
-                    e.a = W.edges[2 * q];
-                    e.b = W.edges[2 * q + 1];
-                    e.stat = W.edge_static[q];
-                    load_box(ebox, q, e.lo, e.hi);
+                    S.code[k] = E.code[eb + k];
+                    S.a[k] = W.edges[2 * q];
+                    S.b[k] = W.edges[2 * q + 1];
+                    S.zs[k] = (unsigned char)(E.zb[eb + k] | (W.edge_static[q] ? 8 : 0));
+                    double lo[3], hi[3];
+                    load_box(ebox, q, lo, hi);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        S.lo[c][k] = lo[c];
+                        S.hi[c][k] = hi[c];
+                    }
                 }
                 __syncwarp();
             }
             const int np = m * (m - 1) / 2;
+            const float inv_m = 1.0f / (float)m;
             for (int k0 = 0; k0 < np; k0 += 32, ++it) {
                 const int k = k0 + lane;
                 bool hit = false;
                 if (PASS == 0 && k < np) {
                     int i, j;
-                    tri_index(k, m, i, j);
-                    const SmEntry& x = sme[w][i];
-                    const SmEntry& y = sme[w][j];
-                    hit = (x.z | y.z) == 7 && x.code == y.code && !(x.stat && y.stat) && x.a != y.a &&
-                          x.a != y.b && x.b != y.a && x.b != y.b && sm_overlap(x, y);
+                    rr_index(k, m, inv_m, i, j);
+                    const int zi = S.zs[i], zj = S.zs[j];
+                    hit = ((zi | zj) & 7) == 7 && !(zi & zj & 8) && S.code[i] == S.code[j] && S.a[i] != S.a[j] &&
+                          S.a[i] != S.b[j] && S.b[i] != S.a[j] && S.b[i] != S.b[j] && S.lo[0][i] <= S.hi[0][j] &&
+                          S.lo[0][j] <= S.hi[0][i] && S.lo[1][i] <= S.hi[1][j] && S.lo[1][j] <= S.hi[1][i] &&
+                          S.lo[2][i] <= S.hi[2][j] && S.lo[2][j] <= S.hi[2][i];
                 }
                 const unsigned msk = warp_hits<PASS>(hit, masks, it);
                 if (PASS == 1 && ((msk >> lane) & 1u)) {
                     int i, j;
-                    tri_index(k, m, i, j);
+                    rr_index(k, m, inv_m, i, j);
                     write_ee(O, base + lane_rank(msk), E.prim[eb + i], E.prim[eb + j], W);
                 }
                 base += __popc(msk);

@@ -85,19 +85,24 @@ __global__ void k_count_true(const uint8_t* __restrict__ v, int64_t P, int* __re
     block_count(f, count);
 }
 
-// sorted keys (free row, or 0x7fffffff for dropped) -> seg_beg/seg_end per row,
-// plus the ascending list of distinct rows (collided vertices for the reduced update)
-__global__ void k_mark_segments(const int* __restrict__ skey, int m, int* __restrict__ seg_beg,
+// sorted keys (free row < nrows, or a sentinel >= nrows for dropped) -> seg_beg/seg_end
+// per row, plus the ascending list of distinct rows (collided vertices for the reduced update)
+__global__ void k_mark_segments(const int* __restrict__ skey, int m, int nrows, int* __restrict__ seg_beg,
                                 int* __restrict__ seg_end, int* __restrict__ rows_out_flag) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     const int k = skey[j];
-    if (k == 0x7fffffff) return;
+    if (k >= nrows) return;
     if (j == 0 || skey[j - 1] != k) {
         seg_beg[k] = j;
         rows_out_flag[j] = 1;
     }
     if (j == m - 1 || skey[j + 1] != k) seg_end[k] = j + 1;
+}
+
+__global__ void k_clamp_keys(int* __restrict__ k, int m, int cap) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m && k[i] > cap) k[i] = cap;
 }
 
 __global__ void k_iota(int* __restrict__ a, int64_t m) {

@@ -100,6 +100,33 @@ def test_distance_toi_bitwise(cuda, rng, floor):
         assert _same(got, ref)
 
 
+def _comoving_pairs(n, rng, scale=0.002, shift=0.003, twist=0.02):
+    """Pairs a few mm apart carried along by a common rigid motion (rotation about z
+    + translation) plus a small relative jitter: the cloth-riding-the-body regime."""
+    kind = (rng.random(n) < 0.5).astype(np.int8)
+    c = rng.uniform(-0.3, 0.3, size=(n, 1, 3))
+    base = c + rng.normal(size=(n, 4, 3)) * scale
+    ang = twist * rng.uniform(0.5, 1.0, size=(n, 1))
+    ca, sa = np.cos(ang), np.sin(ang)
+    x, y = base[..., 0], base[..., 1]
+    end = np.stack([ca * x - sa * y, sa * x + ca * y, base[..., 2]], axis=-1)
+    end = end + shift * rng.normal(size=(n, 1, 3)) + 1e-5 * rng.normal(size=(n, 4, 3))
+    return kind, np.arange(4 * n).reshape(n, 4), base.reshape(-1, 3), end.reshape(-1, 3)
+
+
+@pytest.mark.parametrize("floor", [0.2, 0.5])
+def test_distance_toi_comoving_bitwise(cuda, rng, floor):
+    """Exercises the march's relative-motion shortcut (narrow.cu march_never_reaches):
+    results must stay bitwise the oracle's, NaN or not."""
+    import paper_2403_19272_b200 as P
+
+    kind, idx, x0, x1 = _comoving_pairs(20000, rng)
+    got = P.distance_toi(kind, idx, x0, x1, floor_frac=floor)
+    ref = O.distance_toi(kind, idx, x0, x1, floor_frac=floor)
+    assert np.isnan(ref).mean() > 0.3 and (~np.isnan(ref)).any()
+    assert _same(got, ref)
+
+
 @pytest.mark.parametrize("count", [1, 3, 6])
 def test_partial_ccd_bitwise(cuda, rng, count):
     """reference tests/test_partial_ccd.py:68-88 population."""
@@ -143,10 +170,6 @@ def test_pair_witness_degenerate(cuda):
     pr = Pairs(kind, idx)
     OracleSimulation.witness_into(None, pr, x)
     assert np.array_equal(nrm, pr.normal) and np.array_equal(bary, pr.bary) and np.array_equal(dist, pr.dist)
-
-
-def _same(a, b):
-    return np.array_equal(np.isnan(a), np.isnan(b)) and np.array_equal(a[~np.isnan(a)], b[~np.isnan(b)])
 
 
 @pytest.mark.parametrize("steps,jitter,move", [(0, 0.0, 2e-3), (12, 0.0, 1e-3), (6, 2e-4, 5e-4), (3, 0.0, 0.0)])
