@@ -36,6 +36,68 @@ def _rms(v: np.ndarray) -> float:
     return float(np.linalg.norm(v)) / max(np.sqrt(v.size), 1.0)
 
 
+class _Tracked(np.ndarray):
+    """ndarray that records writes through item assignment (``a[...] = v``, also on
+    views) so only modified state fields are written back to the device."""
+
+    def __array_finalize__(self, obj):
+        root = getattr(obj, "_root", None)
+        self._root = root if root is not None else self
+        self._dirty = False
+
+    def __setitem__(self, key, value):
+        self._root._dirty = True
+        super().__setitem__(key, value)
+
+    def __array_ufunc__(self, ufunc, method, *inputs, out=None, **kw):
+        # arithmetic yields plain arrays; in-place ufuncs (out=state field) mark dirty
+        plain = tuple(np.asarray(a) if isinstance(a, _Tracked) else a for a in inputs)
+        if out is not None:
+            for o in out:
+                if isinstance(o, _Tracked):
+                    o._root._dirty = True
+            kw["out"] = tuple(np.asarray(o) if isinstance(o, _Tracked) else o for o in out)
+        return getattr(ufunc, method)(*plain, **kw)
+
+
+class DeviceSimState:
+    """SimState (reference mesh.py:55-73) backed by the device state: fields download
+    lazily and are cached; in-place edits of a cached field (the reference tests do
+    ``sim.state.x_dot[:] = ...``) are written back before the next device call."""
+
+    FIELDS = ("x", "x_dot", "x_prev", "delta_f")
+
+    def __init__(self, sim, step_index=None):
+        self._sim = sim
+        self._cache = {}
+        self.step_index = sim._step_index if step_index is None else step_index
+
+    def _field(name):
+        def get(self):
+            a = self._cache.get(name)
+            if a is None:
+                a = self._cache[name] = self._sim._download(name).view(_Tracked)
+                a._dirty = False
+            return a
+
+        def put(self, value):
+            a = np.array(value, dtype=np.float64).view(_Tracked)
+            a._dirty = True
+            self._cache[name] = a
+
+        return property(get, put)
+
+    def dirty(self, name) -> bool:
+        a = self._cache.get(name)
+        return a is not None and bool(a._dirty)
+
+    x = _field("x")
+    x_dot = _field("x_dot")
+    x_prev = _field("x_prev")
+    delta_f = _field("delta_f")
+    del _field
+
+
 class Simulation:
     """One cloth plus optional obstacle meshes, stepped on the GPU under a StepConfig."""
 
@@ -88,6 +150,7 @@ class Simulation:
         self._n_obs = len(obstacle_x)
         self._host_state = None
         self._host_obstacles = None
+        self._obs_dirty = False
         self._step_index = 0
 
     def __del__(self):
@@ -101,53 +164,70 @@ class Simulation:
         return _lib.stream_handle()
 
     def _flush(self):
-        """Write back host-mirror edits before the device uses the state."""
+        """Write back host-mirror edits (fields that were read or assigned) before
+        the device uses the state."""
         st = self._host_state
-        if st is None:
+        obs = self._host_obstacles
+        if st is None and obs is None:
             return
-        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (st.x, st.x_dot, st.x_prev, st.delta_f)]
-        obs = np.ascontiguousarray(self._host_obstacles, dtype=np.float64) if self._n_obs else None
-        _lib.check(self._lib.cs_set_state(self._scene, *[a.ctypes.data for a in arrs],
-                                          obs.ctypes.data if obs is not None else None, int(st.step_index),
+        ptrs = []
+        keep = []
+        for name in DeviceSimState.FIELDS:
+            if st is None or not st.dirty(name):
+                ptrs.append(None)
+                continue
+            a = np.ascontiguousarray(np.asarray(st._cache[name]), dtype=np.float64)
+            keep.append(a)
+            ptrs.append(a.ctypes.data)
+        o = np.ascontiguousarray(obs, dtype=np.float64) if (obs is not None and self._n_obs and self._obs_dirty) else None
+        step = int(st.step_index) if st is not None else -1
+        _lib.check(self._lib.cs_set_state(self._scene, *ptrs, o.ctypes.data if o is not None else None, step,
                                           self._stream()), "cs_set_state")
-        self._step_index = int(st.step_index)
+        self._obs_dirty = False
+        if st is not None:
+            self._step_index = step
+            for name in DeviceSimState.FIELDS:
+                if st.dirty(name):
+                    st._cache[name]._dirty = False
+
+    def _download(self, name: str) -> np.ndarray:
+        """One state field (n, 3) from the device (cs_get_state with only that pointer)."""
+        out = np.empty((self.mesh.vertex_count, 3)) if name != "obstacle_x" else np.empty((self._n_obs, 3))
+        ptrs = [None] * 5
+        ptrs[(*DeviceSimState.FIELDS, "obstacle_x").index(name)] = out.ctypes.data if out.size else None
+        idx = ctypes.c_int(0)
+        _lib.check(self._lib.cs_get_state(self._scene, *ptrs, ctypes.byref(idx), self._stream()), "cs_get_state")
+        return out
 
     def host_state(self) -> SimState:
-        n = self.mesh.vertex_count
-        bufs = [np.empty((n, 3)) for _ in range(4)]
-        obs = np.empty((self._n_obs, 3))
-        idx = ctypes.c_int(0)
-        _lib.check(self._lib.cs_get_state(self._scene, *[b.ctypes.data for b in bufs],
-                                          obs.ctypes.data if self._n_obs else None, ctypes.byref(idx),
-                                          self._stream()), "cs_get_state")
-        self._host_obstacles = obs
-        return SimState(x=bufs[0], x_dot=bufs[1], x_prev=bufs[2], delta_f=bufs[3], step_index=self._step_index)
+        """Full host copy of the device state (all fields)."""
+        return SimState(**{k: self._download(k) for k in DeviceSimState.FIELDS}, step_index=self._step_index)
 
     @property
-    def state(self) -> SimState:
+    def state(self):
+        """``SimState`` view of the device state; each field downloads on first access,
+        so reading ``sim.state.x`` moves only the positions."""
         if self._host_state is None:
-            self._host_state = self.host_state()
+            self._host_state = DeviceSimState(self)
         return self._host_state
 
     @state.setter
-    def state(self, st: SimState):
-        self._host_state = SimState(x=np.array(st.x, dtype=np.float64), x_dot=np.array(st.x_dot, dtype=np.float64),
-                                    x_prev=np.array(st.x_prev, dtype=np.float64),
-                                    delta_f=np.array(st.delta_f, dtype=np.float64), step_index=int(st.step_index))
-        if self._host_obstacles is None:
-            self.host_state()
+    def state(self, st):
+        ds = DeviceSimState(self, step_index=int(st.step_index))
+        for k in DeviceSimState.FIELDS:
+            setattr(ds, k, getattr(st, k))
+        self._host_state = ds
 
     @property
     def obstacle_x(self) -> np.ndarray:
-        if self._host_state is not None and self._host_obstacles is not None:
-            return self._host_obstacles
-        self.host_state()
+        if self._host_obstacles is None:
+            self._host_obstacles = self._download("obstacle_x")
         return self._host_obstacles
 
     @obstacle_x.setter
     def obstacle_x(self, value):
-        _ = self.state
         self._host_obstacles = np.array(value, dtype=np.float64).reshape(-1, 3)
+        self._obs_dirty = True
 
     # ------------------------------------------------------------ reference helpers
     def world(self, cloth_x: np.ndarray, obstacle_x: np.ndarray | None = None) -> np.ndarray:
@@ -179,6 +259,7 @@ class Simulation:
                                obs.ctypes.data if obs is not None else None, ctypes.byref(rep), self._stream())
         # a failed step leaves the state untouched (the reference raises before assigning)
         self._host_state = None
+        self._host_obstacles = None
         _lib.check(rc, "cs_step")
         self._step_index += 1
         self.last_report_c = rep
