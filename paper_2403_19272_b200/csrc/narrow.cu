@@ -365,6 +365,129 @@ __device__ __forceinline__ bool march_never_reaches(int kd, const Corners& a, co
     return step * 60.0 > 1.0 + 1e-9;
 }
 
+// ---- fp32 closest-point directions for the march's relative-motion shortcut.
+// Only the DIRECTION of the witness is taken from fp32; the bounds below are
+// evaluated in fp64 and are valid for any unit direction n:
+//     dist(A, B) >= min_{a in A, b in B} (a - b) . n = min over vertex pairs,
+// and dist(A, B) <= |pA - pB| for any pair of points taken on A and B.
+struct f3 {
+    float x, y, z;
+};
+__device__ __forceinline__ f3 fsub(f3 a, f3 b) { return f3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ float fdot(f3 a, f3 b) { return fmaf(a.x, b.x, fmaf(a.y, b.y, a.z * b.z)); }
+__device__ __forceinline__ float fclip(float v) { return fminf(fmaxf(v, 0.0f), 1.0f); }
+
+// barycentric weights (u of b, v of c) of the closest point of triangle abc to p
+__device__ __forceinline__ void pt_tri_weights_f(f3 p, f3 a, f3 b, f3 c, float& u, float& v) {
+    const f3 ab = fsub(b, a), ac = fsub(c, a), ap = fsub(p, a), bp = fsub(p, b), cp = fsub(p, c);
+    const float d1 = fdot(ab, ap), d2 = fdot(ac, ap), d3v = fdot(ab, bp), d4 = fdot(ac, bp);
+    const float d5 = fdot(ab, cp), d6 = fdot(ac, cp);
+    u = 0.0f;
+    v = 0.0f;
+    if (d1 <= 0.0f && d2 <= 0.0f) return;
+    if (d3v >= 0.0f && d4 <= d3v) { u = 1.0f; return; }
+    if (d6 >= 0.0f && d5 <= d6) { v = 1.0f; return; }
+    const float vc = d1 * d4 - d3v * d2;
+    if (vc <= 0.0f && d1 >= 0.0f && d3v <= 0.0f) { u = fclip(d1 / (d1 - d3v)); return; }
+    const float vb = d5 * d2 - d1 * d6;
+    if (vb <= 0.0f && d2 >= 0.0f && d6 <= 0.0f) { v = fclip(d2 / (d2 - d6)); return; }
+    const float va = d3v * d6 - d5 * d4;
+    const float g1 = d4 - d3v, g2 = d5 - d6;
+    if (va <= 0.0f && g1 >= 0.0f && g2 >= 0.0f) {
+        const float w = fclip(g1 / (g1 + g2));
+        u = 1.0f - w;
+        v = w;
+        return;
+    }
+    const float inv = 1.0f / (va + vb + vc);
+    u = fclip(vb * inv);
+    v = fclip(vc * inv);
+    if (u + v > 1.0f) {
+        const float sum = u + v;
+        u /= sum;
+        v /= sum;
+    }
+}
+
+__device__ __forceinline__ void seg_seg_params_f(f3 a0, f3 a1, f3 b0, f3 b1, float& s, float& t) {
+    const f3 da = fsub(a1, a0), db = fsub(b1, b0), r = fsub(a0, b0);
+    const float aa = fdot(da, da), ee = fdot(db, db), f = fdot(db, r), c = fdot(da, r), bb = fdot(da, db);
+    const float den = aa * ee - bb * bb;
+    s = den > 1e-20f ? fclip((bb * f - c * ee) / den) : 0.0f;
+    const float traw = ee > 1e-20f ? (bb * s + f) / ee : 0.0f;
+    t = fclip(traw);
+    if (traw != t) s = aa > 1e-20f ? fclip((bb * t - c) / aa) : 0.0f;
+}
+
+// The march's NaN proven without the fp64 witness distance: as march_never_reaches,
+// with d0 bracketed by [lower, upper] from an fp32-chosen direction (see above).
+__device__ __forceinline__ bool march_never_reaches_f32(int kd, const Corners& a, const Corners& b, double floor_frac,
+                                                        int max_iter) {
+    if (max_iter < 60 || !(floor_frac < 1.0) || !(floor_frac >= 0.0)) return false;
+    d3 r[4], dp[4];
+    double mag = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        r[k] = a.p[k] - a.p[0];  // relative start positions (fp64)
+        dp[k] = b.p[k] - a.p[k];
+        mag = fmax(mag, fmax(fmax(fabs(a.p[k].x), fabs(a.p[k].y)), fabs(a.p[k].z)));
+        mag = fmax(mag, fmax(fmax(fabs(b.p[k].x), fabs(b.p[k].y)), fabs(b.p[k].z)));
+    }
+    f3 rf[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rf[k] = f3{(float)r[k].x, (float)r[k].y, (float)r[k].z};
+    d3 pa, pb;  // fp64 points on side A and side B (valid convex combinations)
+    if (kd == CS_VT) {
+        float u, v;
+        pt_tri_weights_f(rf[0], rf[1], rf[2], rf[3], u, v);
+        double ud = u, vd = v;
+        const double sum = ud + vd;
+        if (sum > 1.0) {  // keep the point inside the triangle (fp32 rounding)
+            ud /= sum;
+            vd /= sum;
+            if (ud + vd > 1.0) vd = 1.0 - ud;
+        }
+        pa = r[0];
+        pb = r[1] + ud * (r[2] - r[1]) + vd * (r[3] - r[1]);
+    } else {
+        float sp, tp;
+        seg_seg_params_f(rf[0], rf[1], rf[2], rf[3], sp, tp);
+        pa = r[0] + (double)sp * (r[1] - r[0]);
+        pb = r[2] + (double)tp * (r[3] - r[2]);
+    }
+    const d3 nv = pa - pb;
+    const double len = norm3(nv);
+    if (!(len > 0.0)) return false;
+    const d3 n = (1.0 / len) * nv;
+    const int na = kd == CS_VT ? 1 : 2;
+    double lb = INFINITY;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 1; j < 4; ++j)
+            if (i < na && j >= na) lb = fmin(lb, dot3(r[i] - r[j], n));
+    const double slack = 1e-12 * mag;
+    const double d_lo = lb * (1.0 - 1e-12) - slack, d_hi = len * (1.0 + 1e-12) + slack;
+    double ra = 0.0, rb = 0.0, la = 0.0, lbm = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double rel = norm3(dp[k] - dp[0]), mvk = norm3(dp[k]);
+        if (k < na) {
+            ra = fmax(ra, rel);
+            la = fmax(la, mvk);
+        } else {
+            rb = fmax(rb, rel);
+            lbm = fmax(lbm, mvk);
+        }
+    }
+    const double L = (la + lbm) * (1.0 + 1e-12);  // >= the reference's L
+    if (!(L > 0.0)) return false;
+    const double dmin = d_lo - (ra + rb) * (1.0 + 1e-12) - slack;
+    const double goal_hi = floor_frac * d_hi;
+    if (!(dmin > goal_hi * (1.0 + 2e-9))) return false;
+    return ((dmin - goal_hi) / L) * 60.0 > 1.0 + 1e-9;
+}
+
 __device__ double distance_toi_pair(int kd, const Corners& a, const Corners& b, double floor_frac, int max_iter) {
     d3 dp[4];
     double mv[4];
@@ -541,7 +664,11 @@ __global__ void __launch_bounds__(128) k_distance_toi_wl(const int* __restrict__
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const int i = wl[k];
         const int4 id = idx[i];
-        const double f = distance_toi_pair(kind[i], gather4(x0, id), gather4(x1, id), floor_frac, max_iter);
+        const int kd = kind[i];
+        const Corners a = gather4(x0, id), b = gather4(x1, id);
+        const double f = march_never_reaches_f32(kd, a, b, floor_frac, max_iter)
+                             ? __longlong_as_double(0x7ff8000000000000ULL)
+                             : distance_toi_pair(kd, a, b, floor_frac, max_iter);
         out[i] = f;
         if (f == f) m = fmin(m, f);
     }
