@@ -11,6 +11,7 @@
  *   CS_DIVERGENCE   (3)  smoother blew up      -> clothsim.SmootherDivergence (smoothing.py:55-62)
  *   CS_BAD_DIAGONAL (4)  nonpositive diagonal  -> ValueError                  (smoothing.py:39-40)
  *   CS_BAD_ARGUMENT (5)  invalid size/argument -> ValueError
+ *   CS_INTERNAL     (6)  internal consistency check failed (test hooks) -> RuntimeError
  *   >= 1000              CUDA runtime error (1000 + cudaError_t)
  *
  * Which reference interface each entry point replaces is cited per function;
@@ -31,6 +32,7 @@ extern "C" {
 #define CS_DIVERGENCE 3
 #define CS_BAD_DIAGONAL 4
 #define CS_BAD_ARGUMENT 5
+#define CS_INTERNAL 6
 
 typedef struct cs_scene cs_scene;
 
@@ -95,6 +97,7 @@ typedef struct {
     long long pairs_last_site, pairs_max_site;
     int reduced_fallbacks;
     long long gpu_launches;
+    int static_sites;           /* motion-free CCD sites served from the previous site's pairs */
 } cs_step_report;
 
 /* ---- scene lifetime ---------------------------------------------------- */

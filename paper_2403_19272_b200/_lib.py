@@ -59,10 +59,10 @@ class StepReportC(ctypes.Structure):
             "t_narrow_full", "t_rf")] + [
         ("n_outer_deltas", ctypes.c_int), ("outer_deltas", ctypes.c_double * 64),
         ("pairs_last_site", ctypes.c_longlong), ("pairs_max_site", ctypes.c_longlong),
-        ("reduced_fallbacks", ctypes.c_int), ("gpu_launches", ctypes.c_longlong)]
+        ("reduced_fallbacks", ctypes.c_int), ("gpu_launches", ctypes.c_longlong), ("static_sites", ctypes.c_int)]
 
 
-CS_OK, CS_PENETRATION, CS_NONFINITE, CS_DIVERGENCE, CS_BAD_DIAGONAL, CS_BAD_ARGUMENT = range(6)
+CS_OK, CS_PENETRATION, CS_NONFINITE, CS_DIVERGENCE, CS_BAD_DIAGONAL, CS_BAD_ARGUMENT, CS_INTERNAL = range(7)
 
 # every symbol include/clothsim_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
@@ -143,6 +143,8 @@ def check(rc: int, what: str = "clothsim_b200") -> None:
         raise ValueError("nonpositive diagonal entry")
     if rc == CS_BAD_ARGUMENT:
         raise ValueError(f"{what}: invalid argument")
+    if rc == CS_INTERNAL:
+        raise RuntimeError(f"{what}: internal consistency check failed")
     raise RuntimeError(f"{what}: CUDA error {rc - 1000}")
 
 

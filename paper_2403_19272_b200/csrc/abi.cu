@@ -161,7 +161,8 @@ struct PairBuf {
 // scalar slots (doubles) read back in one D2H copy
 enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_NORM1 = 5, S_NORM_F = 6,
        S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_MINBITS = 10, S_COUNT = 16 };
-enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_WLF = 8, I_COUNT = 10 };
+enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_FLAG = 7, I_WLF = 8,
+       I_COUNT = 10 };
 
 const int kStages = 8;
 enum { T_WARM = 0, T_LOCAL, T_GLOBAL, T_SMOOTH, T_BROAD, T_PARTIAL, T_FULL, T_RF };
@@ -208,6 +209,7 @@ struct cs_scene {
     int pending_checks = 0;
     DBuf<int> fallback;
     DBuf<int> wl_full, wl_dist;
+    DBuf<uint8_t> keep_flag;
     DBuf<char> cub_tmp;
     DBuf<double> d_scal;
     DBuf<int> d_iscal;
@@ -620,9 +622,89 @@ struct cs_scene {
     }
 
     // broad -> full CCD -> distance march -> clamp factor (stepper.py:426-452)
-    int ccd_site(const double* xa, const double* xb, PairBuf& pr, cs_step_report* rep, double& clamp) {
+    // Motion-free site (xa == xb) right after a site whose pairs are in `prev`: when
+    // the static boxes stay inside that site's boxes, the candidate set is the
+    // subset of `prev` that still overlaps (order preserved).  ok = false -> caller
+    // runs the full broad phase.  Two small host syncs instead of three.
+    int broad_phase_static(const double* x, double margin, PairBuf& prev, PairBuf& pr, bool& ok) {
+        ok = false;
+        if (margin != bmargin || prev.P == 0) return 0;
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_FLAG, 0, sizeof(int), s));
+        k_box_contained<<<grid(3LL * nw), 256, 0, s>>>(x, 3 * nw, margin, vlo.p, vhi.p, d_iscal.p + I_FLAG);
+        ++launches;
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_FLAG], d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        if (h_iscal[I_FLAG]) return 0;
+        // boxes of this site (static), then the surviving subset of prev
+        k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(x, x, nw, margin, vlo.p, vhi.p);
+        k_vertex_disp<<<grid(nw), 256, 0, s>>>(x, x, nw, vdisp.p);
+        const int gt = grid(ntw), ge = grid(new_);
+        k_prim_boxes<3><<<gt, 256, 0, s>>>(wtris.p, ntw, tri_static.p, vlo.p, vhi.p, vdisp.p, ttab.box.p, tdisp.p,
+                                           ttab.part.p);
+        k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, vdisp.p, etab.box.p, edisp.p,
+                                           etab.part.p);
+        const long long P0 = prev.P;
+        CS_RET(keep_flag.ensure(P0));
+        CS_RET(sel.ensure(P0));
+        k_pair_keep<<<grid(P0), 256, 0, s>>>(prev.keys.p, P0, vlo.p, vhi.p, ttab.box.p, etab.box.p, keep_flag.p);
+        launches += 5;
+        size_t bytes = 0;
+        cub::CountingInputIterator<int> it(0);
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, keep_flag.p, sel.p, d_iscal.p + I_FLAG, (int)P0, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, keep_flag.p, sel.p, d_iscal.p + I_FLAG, (int)P0, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_FLAG], d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        const long long P = h_iscal[I_FLAG];
+        CS_RET(pr.reserve(std::max<long long>(P, 1)));
+        if (P) {
+            k_gather_pairs<<<std::max(1, std::min(grid(P), 16 * sm_count)), 256, 0, s>>>(
+                sel.p, d_iscal.p + I_FLAG, prev.kind.p, prev.idx.p, prev.keys.p, pr.kind.p, pr.idx.p, pr.keys.p);
+            ++launches;
+        }
+        CS_CHECK_LAUNCH();
+        pr.P = P;
+        ok = true;
+        return 0;
+    }
+
+    // test hook (CS_VERIFY_STATIC_SITE): the subset path must give exactly the full
+    // broad phase's key set; returns CS_INTERNAL on any difference
+    int verify_static_site(const double* x, PairBuf& got) {
+        PairBuf full;
+        CS_RET(broad_phase(x, x, cfg.d_hat, full));
+        int rc = 0;
+        if (full.P != got.P) {
+            rc = CS_INTERNAL;
+        } else if (full.P > 0) {
+            DBuf<unsigned long long> a, b;
+            CS_RET(a.ensure(full.P));
+            CS_RET(b.ensure(full.P));
+            size_t bytes = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, bytes, full.keys.p, a.p, (int)full.P, 0, 64, s);
+            CS_RET(cub_tmp.ensure(bytes));
+            CS_TRY(cub::DeviceRadixSort::SortKeys(cub_tmp.p, bytes, full.keys.p, a.p, (int)full.P, 0, 64, s));
+            CS_TRY(cub::DeviceRadixSort::SortKeys(cub_tmp.p, bytes, got.keys.p, b.p, (int)full.P, 0, 64, s));
+            std::vector<unsigned long long> ha(full.P), hb(full.P);
+            CS_TRY(cudaMemcpyAsync(ha.data(), a.p, sizeof(unsigned long long) * full.P, cudaMemcpyDeviceToHost, s));
+            CS_TRY(cudaMemcpyAsync(hb.data(), b.p, sizeof(unsigned long long) * full.P, cudaMemcpyDeviceToHost, s));
+            CS_TRY(cudaStreamSynchronize(s));
+            if (ha != hb) rc = CS_INTERNAL;
+            a.release();
+            b.release();
+        }
+        full.release();
+        return rc;
+    }
+
+    int ccd_site(const double* xa, const double* xb, PairBuf& pr, cs_step_report* rep, double& clamp,
+                 PairBuf* prev_site = nullptr) {
         stage(T_BROAD);
-        CS_RET(broad_phase(xa, xb, cfg.d_hat, pr));
+        bool done = false;
+        if (prev_site != nullptr && xa == xb) CS_RET(broad_phase_static(xa, cfg.d_hat, *prev_site, pr, done));
+        if (done && std::getenv("CS_VERIFY_STATIC_SITE")) CS_RET(verify_static_site(xa, pr));
+        if (done && rep) rep->static_sites += 1;
+        if (!done) CS_RET(broad_phase(xa, xb, cfg.d_hat, pr));
         stage(T_FULL);
         const long long P = pr.P;
         if (P > 0) {
@@ -971,6 +1053,7 @@ void cs_scene::release() {
     vert_used.release();
     edge_static.release();
     eflip.release();
+    keep_flag.release();
     hkeys.release();
     cub_tmp.release();
     pa.release();
@@ -1115,7 +1198,9 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     // ---- exit line search (stepper.py:580-592)
     const long long active_pairs = cur->P ? A : 0;
     double tfin = 1.0;
-    CS_RET(ccd_site(anchor_w.p, xc_w.p, *nxt, rep, tfin));
+    // anchor_w == xc_w here (the last outer site set the anchor to the clamped
+    // candidate): a motion-free site whose pairs are a subset of that site's (*cur)
+    CS_RET(ccd_site(anchor_w.p, anchor_w.p, *nxt, rep, tfin, cur));
     CS_RET(set_clamp_value(tfin));
     CS_RET(lerp_world(anchor_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));  // tmp_w = x_final_w
     toi_exit = std::min(toi_exit, tfin);

@@ -777,4 +777,56 @@ __global__ void k_over_ee(const int* __restrict__ over_e, int n_oe, const uint8_
     if (PASS == 0) O.counts[t] = cnt;
 }
 
+// ------------------------------------------------------------------ motion-free sites
+// A site with x_start == x_end (the exit line search: the anchor was just set to
+// the clamped candidate) has static boxes x -/+ margin.  When every such vertex box
+// lies inside the vertex box of the previous site (both with the same margin), every
+// primitive box does too, so the new candidate set is exactly the previous set's
+// pairs whose new boxes still overlap (pair conditions other than overlap are
+// topological and unchanged).  flag != 0: some box escaped -> full broad phase.
+__global__ void k_box_contained(const double* __restrict__ x, int n3, double margin,
+                                const double* __restrict__ vlo, const double* __restrict__ vhi,
+                                int* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n3) return;
+    const double a = x[i];
+    const double lo = np_min(a, a) - margin, hi = np_max(a, a) + margin;
+    if (!(lo >= vlo[i] && hi <= vhi[i])) atomicOr(flag, 1);
+}
+
+__global__ void k_pair_keep(const unsigned long long* __restrict__ keys, int64_t P, const double* __restrict__ vlo,
+                            const double* __restrict__ vhi, const double* __restrict__ tbox,
+                            const double* __restrict__ ebox, uint8_t* __restrict__ keep) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const unsigned long long k = keys[i];
+    const int p = (int)((k >> 32) & 0x7fffffffu), q = (int)(k & 0xffffffffu);
+    double alo[3], ahi[3], blo[3], bhi[3];
+    if (k >> 63) {
+        load_box(ebox, p, alo, ahi);
+        load_box(ebox, q, blo, bhi);
+    } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            alo[c] = vlo[3 * (int64_t)p + c];
+            ahi[c] = vhi[3 * (int64_t)p + c];
+        }
+        load_box(tbox, q, blo, bhi);
+    }
+    keep[i] = overlap6(alo, ahi, blo, bhi) ? 1 : 0;
+}
+
+__global__ void k_gather_pairs(const int* __restrict__ sel, const int* __restrict__ count,
+                               const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+                               const unsigned long long* __restrict__ keys, int8_t* __restrict__ kind_o,
+                               int4* __restrict__ idx_o, unsigned long long* __restrict__ keys_o) {
+    const int n = count[0];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int i = sel[k];
+        kind_o[k] = kind[i];
+        idx_o[k] = idx[i];
+        keys_o[k] = keys[i];
+    }
+}
+
 }  // namespace cs
