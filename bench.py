@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--streams", type=int, default=8, help="worker streams for multi-scene workloads")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--verify-steps", type=int, default=5,
+                    help="untimed steps with the device intersection check after the timed region")
     return ap.parse_args()
 
 
@@ -396,6 +398,33 @@ def run_ours(args, ws, rank, local):
         e2e = {"value": scenes_total * k_e2e / wall, "unit": "FPS", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": k_e2e}
 
+    # penetration-free invariant (untimed): further steps in verify mode, where cs_step
+    # runs the device intersection check on every new state (reference stepper.py:614-621)
+    pen = None
+    if args.verify_steps > 0:
+        import dataclasses
+
+        from paper_2403_19272_b200 import PenetrationError
+
+        bad_steps, checked = 0, 0
+        for s in sims[:2]:
+            s.config = dataclasses.replace(s.config, verify=True)
+            for _ in range(args.verify_steps):
+                try:
+                    s.step()
+                except PenetrationError:
+                    bad_steps += 1
+                    break
+                checked += 1
+            s.config = dataclasses.replace(s.config, verify=False)
+        torch.cuda.synchronize()
+        ta = time.perf_counter()
+        n_pairs = len(sims[0].intersecting_pairs())
+        t_check = time.perf_counter() - ta
+        pen = {"verified_steps": checked, "steps_with_intersections": bad_steps,
+               "intersecting_pairs_final": n_pairs, "device_check_ms": round(1e3 * t_check, 2),
+               "check": "all non-adjacent world-triangle pairs, 17-axis SAT (reference oracles.py:83-131)"}
+
     if rank != 0:
         return
     # per-stage ms/frame and counters
@@ -455,6 +484,7 @@ def run_ours(args, ws, rank, local):
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "penetration_free": pen,
     }
     print(json.dumps(line), flush=True)
 

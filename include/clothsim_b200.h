@@ -165,6 +165,17 @@ int cs_warmstart_correction(cs_scene *scene, const double *b, double *x, void *s
 int cs_energy_gradient(cs_scene *scene, const double *x, const double *z, const int *q_ids, const double *q_w,
                        const double *q_t, int n_q, double *grad, void *stream);
 
+/* ---- penetration-free invariant ----------------------------------------- */
+/* oracle_intersect (oracles.py:83-131): intersecting non-adjacent world-triangle pairs at
+ * x_world (DEVICE, n_world*3; NULL = current state).  count = all pairs; the first
+ * min(count, cap) are written to `pairs` (HOST, (cap,2) rows (lo, hi), unordered). */
+int cs_intersections(cs_scene *scene, const double *x_world, long long *count, int *pairs, int cap, void *stream);
+/* verify mode (stepper.py:614-621): with on != 0, cs_step checks x_final before committing
+ * the state and returns CS_PENETRATION (state untouched) when triangles intersect;
+ * cs_last_intersections reports that check (pairs HOST (cap,2), x_final HOST n_cloth*3). */
+int cs_scene_set_verify(cs_scene *scene, int on);
+int cs_last_intersections(cs_scene *scene, long long *count, int *pairs, int cap, double *x_final);
+
 const char *cs_version(void);
 
 #ifdef __cplusplus

@@ -24,6 +24,7 @@
 #include "solver.cu"
 #include "broad.cu"
 #include "pairs.cu"
+#include "intersect.cu"
 #include "../../include/clothsim_b200.h"
 
 using namespace cs;
@@ -697,6 +698,49 @@ struct cs_scene {
         return rc;
     }
 
+    // ---------------------------------------------------------- intersection check
+    // all intersecting non-adjacent world-triangle pairs at positions xw (device)
+    // (reference oracles.py:83-131); pairs: first `cap` as (lo, hi) rows, unsorted
+    DBuf<int> isect_out;
+    bool verify_on = false;
+    long long last_isect = 0;
+    std::vector<int> last_isect_pairs;
+
+    int intersections(const double* xw, long long& count, int cap) {
+        k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(xw, xw, nw, 0.0, vlo.p, vhi.p);
+        const int gt = grid(ntw);
+        CS_RET(ttab.part.ensure(4LL * gt));
+        k_prim_boxes<3><<<gt, 256, 0, s>>>(wtris.p, ntw, tri_static.p, vlo.p, vhi.p, vdisp.p, ttab.box.p, tdisp.p,
+                                           ttab.part.p);
+        k_cell_size<<<1, 256, 0, s>>>(ttab.part.p, gt, ttab.inv.p);
+        launches += 3;
+        bmargin = -1.0;  // the site boxes are gone: no motion-free site may reuse them
+        const BoxSrc ts{ttab.box.p, nullptr, nullptr, nullptr, ntw};
+        CS_RET(table_count(ttab, ts, ttab.inv.p));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], ttab.offset.p + ttab.np, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], ttab.n_over.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        ttab.m = h_iscal[I_COUNT];
+        ttab.n_over_h = h_iscal[I_COUNT + 1];
+        ttab.set_buckets(ttab.m);
+        CS_RET(table_build(ttab, ts, ttab.inv.p, false));
+        CS_RET(isect_out.ensure(2LL * std::max(cap, 1)));
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_FLAG, 0, sizeof(int), s));
+        if (ttab.m)
+            k_tri_intersect<<<run_blocks(ttab.m), 128, 0, s>>>(ttab.view(), ttab.box.p, wtris.p, xw,
+                                                               d_iscal.p + I_FLAG, isect_out.p, cap);
+        if (ttab.n_over_h)
+            k_tri_intersect_over<<<grid(ttab.n_over_h, 64), 64, 0, s>>>(ttab.over.p, ttab.n_over_h, ttab.is_over.p,
+                                                                         ttab.box.p, ntw, wtris.p, xw,
+                                                                         d_iscal.p + I_FLAG, isect_out.p, cap);
+        launches += 2;
+        CS_CHECK_LAUNCH();
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_FLAG], d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        count = h_iscal[I_FLAG];
+        return 0;
+    }
+
     int ccd_site(const double* xa, const double* xb, PairBuf& pr, cs_step_report* rep, double& clamp,
                  PairBuf* prev_site = nullptr) {
         stage(T_BROAD);
@@ -1054,6 +1098,7 @@ void cs_scene::release() {
     edge_static.release();
     eflip.release();
     keep_flag.release();
+    isect_out.release();
     hkeys.release();
     cub_tmp.release();
     pa.release();
@@ -1205,6 +1250,20 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     CS_RET(lerp_world(anchor_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));  // tmp_w = x_final_w
     toi_exit = std::min(toi_exit, tfin);
     stage(-1);
+    // ---- verify mode (stepper.py:614-621): the device intersection check replaces the
+    // injected oracle; a failing step leaves the state untouched
+    if (verify_on) {
+        long long bad = 0;
+        const int cap = 1024;
+        CS_RET(intersections(tmp_w.p, bad, cap));
+        last_isect = bad;
+        last_isect_pairs.assign(2 * (size_t)std::min<long long>(bad, cap), 0);
+        if (bad) {
+            CS_TRY(cudaMemcpy(last_isect_pairs.data(), isect_out.p, sizeof(int) * last_isect_pairs.size(),
+                              cudaMemcpyDeviceToHost));
+            return CS_PENETRATION;
+        }
+    }
     // ---- new state (stepper.py:594-602)
     CS_TRY(cudaMemcpyAsync(xprev.p, x.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
     k_velocity_update<<<grid(3LL * n), 256, 0, s>>>(tmp_w.p, x.p, v.p, 3LL * n, h);
@@ -1481,6 +1540,43 @@ int cs_scene_pair_results(cs_scene* sc, double* toi, double* toi_filter, void* s
     if (P == 0) return 0;
     if (toi) CS_TRY(cudaMemcpyAsync(toi, sc->cur->toi.p, sizeof(double) * P, cudaMemcpyDeviceToDevice, s));
     if (toi_filter) CS_TRY(cudaMemcpyAsync(toi_filter, sc->cur->filt.p, sizeof(double) * P, cudaMemcpyDeviceToDevice, s));
+    return 0;
+}
+
+int cs_scene_set_verify(cs_scene* sc, int on) {
+    if (!sc) return CS_BAD_ARGUMENT;
+    sc->verify_on = on != 0;
+    return 0;
+}
+
+int cs_intersections(cs_scene* sc, const double* x_world, long long* count, int* pairs, int cap, void* stream) {
+    if (!sc || cap < 0) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    const double* xw = x_world;
+    if (!xw) {  // current world state
+        CS_TRY(cudaMemcpyAsync(sc->tmp_w.p, sc->x.p, sizeof(double) * 3 * sc->n, cudaMemcpyDeviceToDevice, sc->s));
+        if (sc->nobs)
+            CS_TRY(cudaMemcpyAsync(sc->tmp_w.p + 3LL * sc->n, sc->obs.p, sizeof(double) * 3 * sc->nobs,
+                                   cudaMemcpyDeviceToDevice, sc->s));
+        xw = sc->tmp_w.p;
+    }
+    long long bad = 0;
+    CS_RET(sc->intersections(xw, bad, cap));
+    if (count) *count = bad;
+    if (pairs && bad)
+        CS_TRY(cudaMemcpy(pairs, sc->isect_out.p, sizeof(int) * 2 * std::min<long long>(bad, cap),
+                          cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int cs_last_intersections(cs_scene* sc, long long* count, int* pairs, int cap, double* x_final) {
+    if (!sc || cap < 0) return CS_BAD_ARGUMENT;
+    if (count) *count = sc->last_isect;
+    if (pairs) {
+        const size_t k = std::min<size_t>(sc->last_isect_pairs.size() / 2, (size_t)cap);
+        std::memcpy(pairs, sc->last_isect_pairs.data(), sizeof(int) * 2 * k);
+    }
+    if (x_final) CS_TRY(cudaMemcpy(x_final, sc->tmp_w.p, sizeof(double) * 3 * sc->n, cudaMemcpyDeviceToHost));
     return 0;
 }
 

@@ -135,6 +135,7 @@ class Simulation:
         self.kappa = config.dbb_kappa if config.dbb_kappa > 0 else self.k / ((config.d_hat / 2.0) ** 2 * np.log(2.0))
         self.gravity_force = mesh.vertex_mass[:, None] * np.asarray(config.gravity)
         self._verify_oracle = None
+        self._device_verify = False
         self.last_outer_deltas = []
         self.last_report_c = None
 
@@ -255,11 +256,29 @@ class Simulation:
         pins = self._pin_targets(t_now + cfg.h)
         obs = self._obstacle_targets(t_now + cfg.h)
         rep = _lib.StepReportC()
+        # verify mode without an injected host oracle: the device intersection check
+        # (csrc/intersect.cu, reference oracles.py:83-131) runs inside cs_step on x_final
+        device_verify = bool(cfg.verify and self._verify_oracle is None)
+        if device_verify != self._device_verify:
+            _lib.check(self._lib.cs_scene_set_verify(self._scene, int(device_verify)), "cs_scene_set_verify")
+            self._device_verify = device_verify
         rc = self._lib.cs_step(self._scene, pins.ctypes.data if pins is not None else None,
                                obs.ctypes.data if obs is not None else None, ctypes.byref(rep), self._stream())
         # a failed step leaves the state untouched (the reference raises before assigning)
         self._host_state = None
         self._host_obstacles = None
+        if rc == _lib.CS_PENETRATION and device_verify:
+            count = ctypes.c_longlong(0)
+            self._lib.cs_last_intersections(self._scene, ctypes.byref(count), None, 0, None)
+            if count.value:
+                k = min(count.value, 1024)
+                pairs = np.zeros((k, 2), np.int32)
+                x_final = np.empty((self.mesh.vertex_count, 3))
+                self._lib.cs_last_intersections(self._scene, None, pairs.ctypes.data, k, x_final.ctypes.data)
+                pairs = pairs.astype(np.int64)
+                pairs = pairs[np.lexsort((pairs[:, 1], pairs[:, 0]))]
+                raise PenetrationError(f"step {self._step_index}: {count.value} intersecting triangle pairs",
+                                       state_dump={"x": x_final, "pairs": pairs})
         _lib.check(rc, "cs_step")
         self._step_index += 1
         self.last_report_c = rep
@@ -271,7 +290,9 @@ class Simulation:
             timings={"warm_start": rep.t_warm_start, "local": rep.t_local, "global": rep.t_global,
                      "smoothing": rep.t_smoothing, "broad": rep.t_broad, "narrow_partial": rep.t_narrow_partial,
                      "narrow_full": rep.t_narrow_full, "rf": rep.t_rf})
-        if cfg.verify and self._verify_oracle is not None:
+        if device_verify:
+            report.penetration_free = True
+        elif cfg.verify and self._verify_oracle is not None:
             st = self.state
             xw = self.world(st.x)
             bad = self._verify_oracle(xw, self.bvh.triangles)
@@ -423,3 +444,19 @@ class Simulation:
         if t <= 0.0:
             raise PenetrationError("impact at t<=0: step began in contact")
         return self.config.alpha * t
+
+    def intersecting_pairs(self, x_world=None) -> np.ndarray:
+        """All intersecting non-adjacent world-triangle pairs as sorted (k, 2) rows,
+        computed on the device (reference oracles.py:83-131); x_world None = current state."""
+        cap = 4096
+        while True:
+            count = ctypes.c_longlong(0)
+            pairs = np.zeros((cap, 2), np.int32)
+            xd = self._dbuf(x_world) if x_world is not None else None
+            _lib.check(self._lib.cs_intersections(self._scene, xd.data_ptr() if xd is not None else None,
+                                                  ctypes.byref(count), pairs.ctypes.data, cap, self._stream()),
+                       "cs_intersections")
+            if count.value <= cap:
+                out = pairs[:count.value].astype(np.int64)
+                return out[np.lexsort((out[:, 1], out[:, 0]))]
+            cap = int(count.value)
