@@ -179,8 +179,10 @@ def scene_parts(kind: str, resolution: int = 32, size: float = 1.0, density: flo
         v, t = grid_cloth(resolution, size, height=radius + 2.0 * cfg.d_hat + 0.01 * size)
         v[:, :2] -= size / 2.0
         out["mesh"] = build_mesh(v, t, density, pins=[])
+        # ground slab top 5 mm below the sphere's south pole (a touching slab would count
+        # as an obstacle-obstacle intersection in the penetration check)
         out["obstacles"] = [icosphere(3, radius),
-                            box_mesh(center=(0.0, 0.0, -(radius + 0.01 * size)),
+                            box_mesh(center=(0.0, 0.0, -(radius + 0.005 + 0.01 * size)),
                                      extents=(2.0 * size, 2.0 * size, 0.02 * size), divisions=4)]
     elif kind == "stacked_twist":
         sheets = int(kw.pop("sheets", 2))
