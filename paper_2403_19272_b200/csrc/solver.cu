@@ -42,6 +42,37 @@ __device__ __forceinline__ d3 sell_row(const Sell& H, int row, const double* __r
     const int* cp = H.col + beg + lane;
     const double* vp = H.val + beg + lane;
     int k = 0;
+    if (width <= 16) {
+        // whole row in flight: 16 (col, val) loads, then 16 x gathers, then the ordered sum
+        int c[16];
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            c[u] = u < width ? __ldg(cp + 32 * u) : -1;
+            v[u] = u < width ? __ldg(vp + 32 * u) : 0.0;
+        }
+        double g[16][3];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int cc = c[u] < 0 ? 0 : c[u];
+            if (c[u] >= 0) {
+                g[u][0] = __ldg(x + 3 * cc);
+                g[u][1] = __ldg(x + 3 * cc + 1);
+                g[u][2] = __ldg(x + 3 * cc + 2);
+            } else {
+                g[u][0] = g[u][1] = g[u][2] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            if (c[u] >= 0) {
+                a0 = a0 + v[u] * g[u][0];
+                a1 = a1 + v[u] * g[u][1];
+                a2 = a2 + v[u] * g[u][2];
+            }
+        }
+        return d3{a0, a1, a2};
+    }
     for (; k + 4 <= width; k += 4) {
         int c[4];
         double v[4];
