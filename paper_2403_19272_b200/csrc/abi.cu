@@ -300,20 +300,19 @@ struct cs_scene {
     cudaStream_t cap_stream = nullptr;
 
     void smooth_launch(cudaStream_t st, const double* bb, double* xx, int steps, double c, const double* dl) {
-        const int g = grid(nf);
+        const int g2 = grid(nf, 128);
         for (int k = 0; k < steps; ++k) {
             const bool chk = (k % 10) == 0;
-            k_jacobi_a<<<g, 256, 0, st>>>(sell(), diag.p, dl, bb, xx, t.p, chk ? spart.p : nullptr);
-            if (chk) k_norm_final<<<1, 256, 0, st>>>(spart.p, g, norms.p + k / 10);
-            k_jacobi_b<<<g, 256, 0, st>>>(sell(), diag.p, dl, t.p, c, xx);
+            k_jacobi_a<<<g2, 128, 0, st>>>(sell(), diag.p, dl, bb, xx, t.p, chk ? spart.p : nullptr);
+            if (chk) k_norm_final<<<1, 256, 0, st>>>(spart.p, g2, norms.p + k / 10);
+            k_jacobi_b<<<g2, 128, 0, st>>>(sell(), diag.p, dl, t.p, c, xx);
         }
     }
 
     int smooth(const double* bb, double* xx, int iterations, double omega, const double* dl) {
         const int steps = (iterations + 1) / 2;
         const double c = 1.0 - omega;
-        const int g = grid(nf);
-        CS_RET(spart.ensure(g));
+        CS_RET(spart.ensure(grid(nf, 128)));
         const int nchk = (steps + 9) / 10;
         CS_RET(norms.ensure(std::max(nchk, 1)));
         launches += 2LL * steps + nchk;
