@@ -153,6 +153,15 @@ int cs_scene_pair_results(cs_scene *scene, double *toi, double *toi_filter, void
  * (ids, weights, targets) of Simulation._collision_terms in order; ids are cloth ids. */
 int cs_assemble_rhs(cs_scene *scene, const double *z, const double *x, const int *coll_ids, const double *coll_w,
                     const double *coll_t, int n_coll, double *b, double *delta, void *stream);
+/* Simulation._collision_terms (stepper.py:238-285): per engaged pair with weight > 0, its
+ * movable cloth vertices' (ids, weights, targets) in pair-then-slot order; DEVICE arrays
+ * (ids/w capacity 4P, targets 4P*3); count = entries written */
+int cs_collision_terms(cs_scene *scene, const int8_t *kind, const int *idx4, const double *bary, const double *normal,
+                       const double *weight, const uint8_t *engaged, long long P, const double *x_world, int *ids,
+                       double *w, double *targets, long long *count, void *stream);
+/* r = b - H x - delta x over the free rows (the residual of reduced_correction /
+ * residual_forward, subspace.py:179, stepper.py:663) */
+int cs_residual(cs_scene *scene, const double *b, const double *x, const double *delta, double *r, void *stream);
 /* ajacobi_smooth (smoothing.py:23-66), x (n_free*3) updated in place; delta may be NULL */
 int cs_ajacobi_smooth(cs_scene *scene, const double *b, double *x, int iterations, double omega,
                       const double *delta, void *stream);

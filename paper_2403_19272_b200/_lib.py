@@ -69,7 +69,7 @@ EXPORTED = (
     "cs_scene_create", "cs_scene_destroy", "cs_scene_set_config", "cs_step", "cs_get_state", "cs_set_state",
     "cs_state_device", "cs_full_ccd", "cs_distance_toi", "cs_partial_ccd", "cs_pair_witness", "cs_broad_phase",
     "cs_scene_pairs", "cs_ccd_site", "cs_scene_pair_results", "cs_assemble_rhs", "cs_ajacobi_smooth", "cs_reduced_correction", "cs_warmstart_correction",
-    "cs_energy_gradient", "cs_intersections", "cs_scene_set_verify", "cs_last_intersections", "cs_version",
+    "cs_energy_gradient", "cs_collision_terms", "cs_residual", "cs_intersections", "cs_scene_set_verify", "cs_last_intersections", "cs_version",
 )
 
 _lib = None
@@ -107,6 +107,8 @@ def load(path: str = LIB_PATH):
         "cs_reduced_correction": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, vp]),
         "cs_warmstart_correction": (ctypes.c_int, [vp, vp, vp, vp]),
         "cs_energy_gradient": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp]),
+        "cs_collision_terms": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, ll, vp, vp, vp, vp, ctypes.POINTER(ll), vp]),
+        "cs_residual": (ctypes.c_int, [vp, vp, vp, vp, vp, vp]),
         "cs_intersections": (ctypes.c_int, [vp, vp, ctypes.POINTER(ll), vp, ctypes.c_int, vp]),
         "cs_scene_set_verify": (ctypes.c_int, [vp, ctypes.c_int]),
         "cs_last_intersections": (ctypes.c_int, [vp, ctypes.POINTER(ll), vp, ctypes.c_int, vp]),

@@ -1629,6 +1629,63 @@ int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const int* c
     return 0;
 }
 
+int cs_collision_terms(cs_scene* sc, const int8_t* kind, const int* idx4, const double* bary, const double* normal,
+                       const double* weight, const uint8_t* engaged, long long P, const double* x_world, int* ids,
+                       double* w, double* targets, long long* count, void* stream) {
+    if (!sc || P < 0) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    cudaStream_t s = sc->s;
+    if (count) *count = 0;
+    if (P == 0) return 0;
+    // engaged & weight > 0, in pair order (stepper.py:245)
+    CS_RET(sc->keep_flag.ensure(P));
+    CS_TRY(cudaMemsetAsync(sc->d_iscal.p + I_FLAG, 0, sizeof(int), s));
+    k_flag_engaged<<<sc->grid(P), 256, 0, s>>>(engaged, weight, P, sc->keep_flag.p, sc->d_iscal.p + I_FLAG);
+    CS_RET(sc->sel.ensure(P));
+    size_t bytes = 0;
+    cub::CountingInputIterator<int> it(0);
+    cub::DeviceSelect::Flagged(nullptr, bytes, it, sc->keep_flag.p, sc->sel.p, sc->d_iscal.p + I_FLAG, (int)P, s);
+    CS_RET(sc->cub_tmp.ensure(bytes));
+    CS_TRY(cub::DeviceSelect::Flagged(sc->cub_tmp.p, bytes, it, sc->keep_flag.p, sc->sel.p, sc->d_iscal.p + I_FLAG,
+                                      (int)P, s));
+    CS_TRY(cudaMemcpyAsync(&sc->h_iscal[I_FLAG], sc->d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CS_TRY(cudaStreamSynchronize(s));
+    const long long A = sc->h_iscal[I_FLAG];
+    if (A == 0) return 0;
+    const long long m = 4 * A;
+    CS_RET(sc->skey.ensure(m));
+    CS_RET(sc->sw.ensure(m));
+    CS_RET(sc->stt.ensure(3 * m));
+    CS_RET(sc->rowflag.ensure(m));
+    CS_RET(sc->rows_act.ensure(m));
+    k_collision_terms<<<sc->grid(A), 256, 0, s>>>(sc->sel.p, A, kind, (const int4*)idx4, x_world, bary, normal, weight,
+                                                  sc->cfg.d_hat, sc->n, sc->free_index.p, 0, sc->skey.p, sc->sw.p,
+                                                  sc->stt.p);
+    CS_RET(sc->keep_flag.ensure(m));
+    k_key_kept<<<sc->grid(m), 256, 0, s>>>(sc->skey.p, (int)m, sc->nf, sc->keep_flag.p);
+    bytes = 0;
+    cub::DeviceSelect::Flagged(nullptr, bytes, it, sc->keep_flag.p, sc->rows_act.p, sc->d_iscal.p + I_FLAG, (int)m, s);
+    CS_RET(sc->cub_tmp.ensure(bytes));
+    CS_TRY(cub::DeviceSelect::Flagged(sc->cub_tmp.p, bytes, it, sc->keep_flag.p, sc->rows_act.p,
+                                      sc->d_iscal.p + I_FLAG, (int)m, s));
+    k_gather_terms<<<std::max(1, std::min(sc->grid(m), 16 * sc->sm_count)), 256, 0, s>>>(
+        sc->rows_act.p, sc->d_iscal.p + I_FLAG, sc->sel.p, (const int4*)idx4, sc->sw.p, sc->stt.p, ids, w, targets);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaMemcpyAsync(&sc->h_iscal[I_FLAG], sc->d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CS_TRY(cudaStreamSynchronize(s));
+    if (count) *count = sc->h_iscal[I_FLAG];
+    return 0;
+}
+
+int cs_residual(cs_scene* sc, const double* b, const double* x, const double* delta, double* r, void* stream) {
+    if (!sc || !delta) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    k_residual<<<sc->grid(sc->nf), 256, 0, sc->s>>>(sc->sell(), b, x, delta, r);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaStreamSynchronize(sc->s));
+    return 0;
+}
+
 int cs_ajacobi_smooth(cs_scene* sc, const double* b, double* x, int iterations, double omega, const double* delta,
                       void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;

@@ -100,6 +100,28 @@ __global__ void k_mark_segments(const int* __restrict__ skey, int m, int nrows, 
     if (j == m - 1 || skey[j + 1] != k) seg_end[k] = j + 1;
 }
 
+// compaction helpers for the per-stage collision-terms entry point
+__global__ void k_key_kept(const int* __restrict__ key, int m, int nf, uint8_t* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) flag[i] = key[i] < nf ? 1 : 0;
+}
+__global__ void k_gather_terms(const int* __restrict__ pick, const int* __restrict__ count,
+                               const int* __restrict__ sel, const int4* __restrict__ idx,
+                               const double* __restrict__ w, const double* __restrict__ t, int* __restrict__ ids_out,
+                               double* __restrict__ w_out, double* __restrict__ t_out) {
+    const int n = count[0];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int o = pick[k];
+        const int4 id = idx[sel[o >> 2]];
+        const int slot = o & 3;
+        ids_out[k] = slot == 0 ? id.x : (slot == 1 ? id.y : (slot == 2 ? id.z : id.w));
+        w_out[k] = w[o];
+        t_out[3 * k] = t[3 * o];
+        t_out[3 * k + 1] = t[3 * o + 1];
+        t_out[3 * k + 2] = t[3 * o + 2];
+    }
+}
+
 __global__ void k_clamp_keys(int* __restrict__ k, int m, int cap) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m && k[i] > cap) k[i] = cap;

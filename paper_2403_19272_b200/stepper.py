@@ -460,3 +460,87 @@ class Simulation:
                 out = pairs[:count.value].astype(np.int64)
                 return out[np.lexsort((out[:, 1], out[:, 0]))]
             cap = int(count.value)
+
+    # ------------------------------------------------------------ contact helpers (device)
+    def _witness(self, pairs: PairSet, x_ref) -> None:
+        """Refresh bary / distance / separating normal at x_ref (reference stepper.py:194-216)."""
+        from .collision import witness_normals
+
+        pairs.bary, pairs.distance, pairs.normal = witness_normals(pairs.kind, pairs.idx, x_ref)
+
+    def _collision_terms(self, pairs: PairSet, engaged, x_cand):
+        """(ids, weights, targets) of the engaged pairs at x_cand, computed by the device
+        kernel the step uses (reference stepper.py:238-285); None when nothing engages."""
+        import torch
+
+        P = len(pairs)
+        if P == 0:
+            return None
+        dev = lambda a, t: torch.as_tensor(np.ascontiguousarray(a, dtype=t), device="cuda")  # noqa: E731
+        k, i = dev(pairs.kind, np.int8), dev(pairs.idx, np.int32)
+        bary, nrm = dev(pairs.bary, np.float64), dev(pairs.normal, np.float64)
+        w, eng = dev(pairs.weight, np.float64), dev(np.asarray(engaged, dtype=bool), np.uint8)
+        xw = dev(x_cand, np.float64)
+        ids = torch.empty(4 * P, dtype=torch.int32, device="cuda")
+        wo = torch.empty(4 * P, dtype=torch.float64, device="cuda")
+        to = torch.empty((4 * P, 3), dtype=torch.float64, device="cuda")
+        count = ctypes.c_longlong(0)
+        _lib.check(self._lib.cs_collision_terms(self._scene, k.data_ptr(), i.data_ptr(), bary.data_ptr(),
+                                                nrm.data_ptr(), w.data_ptr(), eng.data_ptr(), P, xw.data_ptr(),
+                                                ids.data_ptr(), wo.data_ptr(), to.data_ptr(), ctypes.byref(count),
+                                                self._stream()), "cs_collision_terms")
+        m = count.value
+        if m == 0:
+            return None
+        return ids[:m].cpu().numpy().astype(np.int64), wo[:m].cpu().numpy(), to[:m].cpu().numpy()
+
+    def residual_forward(self, x, z, pairs: PairSet, x_world) -> np.ndarray:
+        """Forwarded force from the exit residual (reference stepper.py:626-672), run with
+        the device stages: frozen-weight collision terms, energy gradient, reduced
+        corrections + A-Jacobi smoothing with the residual check on device."""
+        import torch
+
+        mesh, cfg = self.mesh, self.config
+        self._flush()
+        quad = None
+        if len(pairs):
+            engaged = pairs.distance < 2.0 * cfg.d_hat
+            frozen = PairSet(kind=pairs.kind, idx=pairs.idx, life_span=np.zeros(len(pairs), np.int64),
+                             weight=np.where(engaged, self.k, 0.0), bary=pairs.bary, distance=pairs.distance,
+                             normal=pairs.normal)
+            coll = self._collision_terms(frozen, engaged, x_world)
+            if coll is not None:
+                ids, w, tg = coll
+                cl = ids < mesh.vertex_count
+                quad = ("quad", ids[cl], w[cl], tg[cl])
+        _, grad, _ = self.energy(x, z, collision=quad)
+        nf = mesh.free.size
+        f_r = self._dbuf(-grad[mesh.free])
+        delta = torch.zeros(nf, dtype=torch.float64, device="cuda")
+        if quad is not None:
+            ids_d = torch.as_tensor(quad[1].astype(np.int32), device="cuda")
+            w_d, t_d = self._dbuf(quad[2]), self._dbuf(quad[3])
+            b = torch.empty((nf, 3), dtype=torch.float64, device="cuda")
+            zz = self._dbuf(z)
+            _lib.check(self._lib.cs_assemble_rhs(self._scene, zz.data_ptr(), zz.data_ptr(), ids_d.data_ptr(),
+                                                 w_d.data_ptr(), t_d.data_ptr(), len(quad[1]), b.data_ptr(),
+                                                 delta.data_ptr(), self._stream()), "cs_assemble_rhs")
+        dx = torch.zeros((nf, 3), dtype=torch.float64, device="cuda")
+        r = torch.empty_like(dx)
+        fnorm = float(torch.linalg.vector_norm(f_r))
+        for it in range(cfg.rf_iterations):
+            _lib.check(self._lib.cs_reduced_correction(self._scene, f_r.data_ptr(), dx.data_ptr(), delta.data_ptr(),
+                                                       int(it > 0), self._stream()), "cs_reduced_correction")
+            _lib.check(self._lib.cs_ajacobi_smooth(self._scene, f_r.data_ptr(), dx.data_ptr(),
+                                                   cfg.smoothing_iterations, cfg.omega, delta.data_ptr(),
+                                                   self._stream()), "cs_ajacobi_smooth")
+            _lib.check(self._lib.cs_residual(self._scene, f_r.data_ptr(), dx.data_ptr(), delta.data_ptr(),
+                                             r.data_ptr(), self._stream()), "cs_residual")
+            if float(torch.linalg.vector_norm(r)) <= cfg.rf_tolerance * max(fnorm, 1e-30):
+                break
+        delta_f = np.zeros_like(np.asarray(x, dtype=np.float64))
+        delta_f[mesh.free] = 2.0 * mesh.vertex_mass[mesh.free, None] * dx.cpu().numpy() / (cfg.h * cfg.h)
+        norm = float(np.linalg.norm(delta_f))
+        if norm > cfg.delta_f_cap:
+            delta_f *= cfg.delta_f_cap / norm
+        return delta_f
