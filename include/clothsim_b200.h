@@ -77,12 +77,19 @@ typedef struct {
     const double *obstacle_x0;  /* (n_obstacle*3) */
 } cs_scene_desc;
 
-/* Mirrors reference StepConfig (stepper.py:43-79); NDB barrier mode. */
+#define CS_BARRIER_NDB 0
+#define CS_BARRIER_DBB 1
+
+/* Mirrors reference StepConfig (stepper.py:43-79).  barrier_mode: CS_BARRIER_NDB
+ * (non-distance barrier, the paper's method) or CS_BARRIER_DBB (log-barrier baseline,
+ * stepper.py:524-538); dbb_kappa is the resolved kappa (stepper.py:165-169). */
 typedef struct {
     double h, eps_initial, eps_inner, eps_outer, eps_toi, alpha;
     double ndb_k, ndb_base, d_hat, omega, rf_tolerance, delta_f_cap;
     int iteration_cap, samples, smoothing_iterations;
     int warm_start_cap, inner_cap, outer_cap, rf_iterations;
+    double dbb_kappa;
+    int barrier_mode;
 } cs_step_config;
 
 /* Mirrors reference StepReport (stepper.py:81-92) + device-side diagnostics. */

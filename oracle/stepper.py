@@ -59,6 +59,18 @@ def rms(v) -> float:
     return float(np.linalg.norm(v)) / max(np.sqrt(v.size), 1.0)   # stepper.py:96-98
 
 
+def dbb_weight(d, d_hat, kappa):
+    """Log barrier -kappa (d - d_hat)^2 ln(d / d_hat) below d_hat, else 0 (pairs.py:83-99)."""
+    d = np.asarray(d, dtype=np.float64)
+    if (d <= 0).any():
+        raise FloatingPointError("nonpositive pair distance: infeasible state")
+    out = np.zeros_like(d)
+    near = d < d_hat
+    dn = d[near]
+    out[near] = -kappa * (dn - d_hat) ** 2 * np.log(dn / d_hat)
+    return out
+
+
 def ndb_weight(life, k, base):
     return k * np.power(base, np.minimum(life, LIFE_CAP).astype(np.float64))   # pairs.py:65-70
 
@@ -98,6 +110,8 @@ class OracleSimulation:
         self.mesh, self.cfg = mesh, config
         self.el, self.sys, self.sub = elastic, system, subspace
         self.k = k
+        # stepper.py:165-169: kappa matched to the NDB mode's initial weight at d_hat / 2
+        self.kappa = config.dbb_kappa if config.dbb_kappa > 0 else k / ((config.d_hat / 2.0) ** 2 * np.log(2.0))
         self.obstacle_x = np.asarray(obstacles_x, dtype=np.float64).reshape(-1, 3)
         self.topo = WorldTopology.build(world_tris, tri_static)
         self.pin_motion, self.obstacle_motion = pin_motion, obstacle_motion
@@ -279,8 +293,7 @@ class OracleSimulation:
     # ------------------------------------------------------------ step
     def step(self):
         cfg, mesh, st = self.cfg, self.mesh, self.state
-        if cfg.barrier_mode != "ndb":
-            raise NotImplementedError("oracle covers the NDB barrier mode")
+        dbb = cfg.barrier_mode == "dbb"
         rep = {"timings": {k: 0.0 for k in ("warm_start", "local", "global", "smoothing", "broad",
                                              "narrow_partial", "narrow_full")},
                "lg_iterations": 0, "outer_loops": 0, "full_ccd_calls": 0, "partial_ccd_calls": 0,
@@ -310,7 +323,11 @@ class OracleSimulation:
         self.witness_into(pr, anchor_w)
         engaged = ~np.isnan(toi) | (pr.dist < 2.0 * cfg.d_hat)
         pr.life = np.zeros(len(pr), np.int64)
-        pr.weight = np.where(engaged, ndb_weight(pr.life, self.k, cfg.ndb_base), 0.0)
+        if dbb:                                          # stepper.py:489-491
+            pr.weight = dbb_weight(np.maximum(pr.dist, 1e-12), 2.0 * cfg.d_hat, self.kappa)
+            engaged = pr.weight > 0
+        else:
+            pr.weight = np.where(engaged, ndb_weight(pr.life, self.k, cfg.ndb_base), 0.0)
 
         xc = x_acc_w[:nc].copy()
         obs_c = x_acc_w[nc:]
@@ -329,15 +346,29 @@ class OracleSimulation:
                 xc = xn
                 rep["lg_iterations"] += 1
                 xc_w = self.world(xc, obs_c)
-                t0 = time.perf_counter()
-                active = narrow.partial_ccd(pr.kind, pr.idx, anchor_w, xc_w, cfg.samples)
-                rep["timings"]["narrow_partial"] += time.perf_counter() - t0
                 rep["partial_ccd_calls"] += 1
-                gap = self.gaps(pr, xc_w)
-                active = active | (gap < cfg.d_hat)
-                pr.life = np.where(active, np.minimum(pr.life + 1, LIFE_CAP), 0)
-                engaged = active | (gap < 2.0 * cfg.d_hat)
-                pr.weight = np.where(engaged, ndb_weight(pr.life, self.k, cfg.ndb_base), 0.0)
+                if dbb:
+                    # baseline: the partial-CCD classes are unused (stepper.py:513, 524-538);
+                    # distances refreshed with the full distance march + clamp
+                    toi_in = narrow.distance_toi(pr.kind, pr.idx, anchor_w, xc_w, floor_frac=1.0 - cfg.alpha)
+                    t_in = self.clamp(toi_in)
+                    if t_in < 1.0:
+                        cw = anchor_w + t_in * (xc_w - anchor_w)
+                        xc = cw[:nc].copy()
+                        obs_c = cw[nc:]
+                        pins_c = xc[mesh.pinned] if mesh.pinned.size else pins_c
+                    self.witness_into(pr, self.world(xc, obs_c))
+                    pr.weight = dbb_weight(np.maximum(pr.dist, 1e-12), 2.0 * cfg.d_hat, self.kappa)
+                    engaged = pr.weight > 0
+                else:
+                    t0 = time.perf_counter()
+                    active = narrow.partial_ccd(pr.kind, pr.idx, anchor_w, xc_w, cfg.samples)
+                    rep["timings"]["narrow_partial"] += time.perf_counter() - t0
+                    gap = self.gaps(pr, xc_w)
+                    active = active | (gap < cfg.d_hat)
+                    pr.life = np.where(active, np.minimum(pr.life + 1, LIFE_CAP), 0)
+                    engaged = active | (gap < 2.0 * cfg.d_hat)
+                    pr.weight = np.where(engaged, ndb_weight(pr.life, self.k, cfg.ndb_base), 0.0)
                 if cfg.iteration_cap and rep["lg_iterations"] >= cfg.iteration_cap:
                     cap_hit = True
                     break
@@ -355,9 +386,13 @@ class OracleSimulation:
                 toi_exit = min(toi_exit, tout)
             anchor_w = xc_w.copy()
             self.witness_into(npr, anchor_w)
-            self.carry_life(pr, npr)
-            engaged = ~np.isnan(toi) | (npr.dist < 2.0 * cfg.d_hat)
-            npr.weight = np.where(engaged, ndb_weight(npr.life, self.k, cfg.ndb_base), 0.0)
+            if dbb:
+                npr.weight = dbb_weight(np.maximum(npr.dist, 1e-12), 2.0 * cfg.d_hat, self.kappa)
+                engaged = npr.weight > 0
+            else:
+                self.carry_life(pr, npr)
+                engaged = ~np.isnan(toi) | (npr.dist < 2.0 * cfg.d_hat)
+                npr.weight = np.where(engaged, ndb_weight(npr.life, self.k, cfg.ndb_base), 0.0)
             pr = npr
             d_out = rms(xc[fr] - prev_outer[fr])
             self.last_outer_deltas.append(d_out)

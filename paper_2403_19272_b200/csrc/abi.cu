@@ -803,8 +803,12 @@ struct cs_scene {
     int engage(PairBuf& pr) {
         CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
         if (pr.P == 0) return 0;
-        k_engage_init<<<grid(pr.P), 256, 0, s>>>(pr.toi.p, pr.dist.p, pr.life.p, pr.P, cfg.d_hat, cfg.ndb_k,
-                                                 cfg.ndb_base, pr.engaged.p, pr.weight.p, d_iscal.p + I_ENG);
+        if (cfg.barrier_mode == CS_BARRIER_DBB)  // log barrier of the witness distance (stepper.py:489-491)
+            k_dbb_weights<<<grid(pr.P), 256, 0, s>>>(pr.dist.p, pr.P, 2.0 * cfg.d_hat, cfg.dbb_kappa, pr.engaged.p,
+                                                     pr.weight.p, d_iscal.p + I_ENG);
+        else
+            k_engage_init<<<grid(pr.P), 256, 0, s>>>(pr.toi.p, pr.dist.p, pr.life.p, pr.P, cfg.d_hat, cfg.ndb_k,
+                                                     cfg.ndb_base, pr.engaged.p, pr.weight.p, d_iscal.p + I_ENG);
         ++launches;
         CS_CHECK_LAUNCH();
         return 0;
@@ -1192,6 +1196,44 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             k_scatter_rows<<<grid(nf), 256, 0, s>>>(xf.p, free_ids.p, nf, xcl);
             ++launches;
             ++lg;
+            if (cfg.barrier_mode == CS_BARRIER_DBB) {
+                // DBB baseline (stepper.py:524-538): the partial-CCD classes go unused;
+                // distance march anchor -> candidate, clamp, witness at the candidate,
+                // log-barrier weights
+                ++partial_calls;
+                double t_in = 1.0;
+                stage(T_FULL);
+                if (cur->P) {
+                    k_distance_toi<<<grid(cur->P, 128), 128, 0, s>>>(cur->kind.p, cur->idx.p, anchor_w.p, xc_w.p,
+                                                                     cur->P, 1.0 - cfg.alpha, 64, cur->filt.p);
+                    const int g = std::min(grid(cur->P), 2 * sm_count);
+                    CS_RET(part.ensure(g));
+                    k_min_toi_partial<<<g, 256, 0, s>>>(cur->filt.p, cur->P, part.p);
+                    k_min_toi_final<<<1, 256, 0, s>>>(part.p, g, cfg.alpha, d_scal.p + S_CLAMP_MIN);
+                    launches += 3;
+                    CS_CHECK_LAUNCH();
+                }
+                CS_RET(sync_scalars());
+                dx_last = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
+                if (cur->P) {
+                    if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;
+                    t_in = h_scal[S_CLAMP];
+                }
+                if (t_in < 1.0) {
+                    CS_RET(lerp_world(anchor_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));
+                    CS_TRY(cudaMemcpyAsync(xc_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
+                }
+                CS_RET(witness(*cur, xc_w.p));
+                CS_RET(engage(*cur));
+                CS_RET(sync_scalars());
+                A = h_iscal[I_ENG];
+                if (cfg.iteration_cap && lg >= cfg.iteration_cap) {
+                    cap_hit = true;
+                    break;
+                }
+                if (dx_last <= cfg.eps_inner) break;
+                continue;
+            }
             // partial CCD + NDB life-span update (stepper.py:511-523)
             stage(T_PARTIAL);
             CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
@@ -1226,7 +1268,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         CS_TRY(cudaMemcpyAsync(anchor_w.p, xc_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
         stage(T_FULL);
         CS_RET(witness(*nxt, anchor_w.p));
-        CS_RET(carry(*cur, *nxt));
+        if (cfg.barrier_mode != CS_BARRIER_DBB) CS_RET(carry(*cur, *nxt));
         CS_RET(engage(*nxt));
         std::swap(cur, nxt);
         // outer progress (stepper.py:574-578)

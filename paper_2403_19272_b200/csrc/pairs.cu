@@ -122,6 +122,26 @@ __global__ void k_gather_terms(const int* __restrict__ pick, const int* __restri
     }
 }
 
+// DBB baseline weights (pairs.py:83-99): -kappa (d - dh)^2 ln(d / dh) for d < dh, d =
+// max(dist, 1e-12) (stepper.py:490); engaged = weight > 0.  numpy order: ((-kappa) sq) ln.
+__global__ void k_dbb_weights(const double* __restrict__ dist, int64_t P, double dh, double kappa,
+                              uint8_t* __restrict__ engaged, double* __restrict__ weight, int* __restrict__ count) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool e = false;
+    if (i < P) {
+        const double d = np_max(dist[i], 1e-12);
+        double w = 0.0;
+        if (d < dh) {
+            const double dd = d - dh;
+            w = ((-kappa) * (dd * dd)) * log(d / dh);
+        }
+        weight[i] = w;
+        e = w > 0.0;
+        engaged[i] = e;
+    }
+    block_count(e, count);
+}
+
 __global__ void k_clamp_keys(int* __restrict__ k, int m, int cap) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m && k[i] > cap) k[i] = cap;

@@ -63,7 +63,7 @@ class _Keep:
         return a.ctypes.data_as(ctypes.POINTER(ctype))
 
 
-def step_config_c(cfg, k: float) -> _lib.StepConfigC:
+def step_config_c(cfg, k: float, kappa: float = 0.0) -> _lib.StepConfigC:
     c = _lib.StepConfigC()
     for name in ("h", "eps_initial", "eps_inner", "eps_outer", "eps_toi", "alpha", "ndb_base", "d_hat", "omega",
                  "rf_tolerance", "delta_f_cap"):
@@ -72,6 +72,8 @@ def step_config_c(cfg, k: float) -> _lib.StepConfigC:
     for name in ("iteration_cap", "samples", "smoothing_iterations", "warm_start_cap", "inner_cap", "outer_cap",
                  "rf_iterations"):
         setattr(c, name, int(getattr(cfg, name)))
+    c.dbb_kappa = float(kappa)
+    c.barrier_mode = 1 if cfg.barrier_mode == "dbb" else 0
     return c
 
 

@@ -104,8 +104,6 @@ class Simulation:
     def __init__(self, mesh: ClothMesh, config: StepConfig, stretch_stiffness: float = 160.0,
                  bend_stiffness: float = 3e-4, obstacles=None, pin_motion=None, obstacle_motion=None,
                  eigensolver: str = "host"):
-        if config.barrier_mode != "ndb":
-            raise NotImplementedError("the GPU pipeline implements the NDB barrier mode (DBB: SURVEY.md section 8f #3)")
         self.mesh = mesh
         self.config = config
         self.elastic = build_elastic(mesh, stretch_stiffness, bend_stiffness)
@@ -142,7 +140,7 @@ class Simulation:
         self._lib = _lib.load()
         desc, keep = scene_desc(mesh, self.elastic, self.system, self.subspace, self.bvh, obstacle_x,
                                 self.gravity_force, mesh.rest_positions)
-        self._cfg_c = step_config_c(config, self.k)
+        self._cfg_c = step_config_c(config, self.k, self.kappa)
         status = ctypes.c_int(0)
         self._scene = self._lib.cs_scene_create(ctypes.byref(desc), ctypes.byref(self._cfg_c), ctypes.byref(status))
         del keep

@@ -172,6 +172,11 @@ def contact_state_fixture(steps=25):
          rf=np.array(rf), intersections=np.array(bad))
 
 
+def dbb_fixture(steps=18):
+    """sphere_drape res 14 in the DBB baseline mode (barrier_mode="dbb")."""
+    traj_fixture("sphere14_dbb", "sphere_drape", steps, {"barrier_mode": "dbb"}, resolution=14, size=0.2)
+
+
 def two_corner_fixture(steps=3):
     """BASELINE config 1: 64x64 grid pinned at two corners, h = 1/200."""
     v, t = grid_cloth(64, 1.0)
@@ -198,3 +203,4 @@ if __name__ == "__main__":
     traj_fixture("twist10", "twist", 6, {}, resolution=10, size=0.3)
     two_corner_fixture()
     contact_state_fixture()
+    dbb_fixture()

@@ -122,6 +122,7 @@ def test_solver_stages_golden():
 @pytest.mark.parametrize("tag,kind,cfg_kw,scene_kw", [
     ("hanging10", "hanging", dict(h=1.0 / 200.0), dict(resolution=10)),
     ("sphere14", "sphere_drape", {}, dict(resolution=14, size=0.2)),
+    ("sphere14_dbb", "sphere_drape", {"barrier_mode": "dbb"}, dict(resolution=14, size=0.2)),
     ("twist10", "twist", {}, dict(resolution=10, size=0.3)),
     ("two_corner64", "two_corner", dict(h=1.0 / 200.0), dict(resolution=64)),
 ])
