@@ -203,7 +203,7 @@ struct cs_scene {
     PairBuf* cur = &pa;
     PairBuf* nxt = &pb;
     DBuf<int> sel, skey, ssrc, skey_s, ssrc_s, seg_beg, seg_end, rowflag, rows_act;
-    DBuf<double> sw, stt;
+    DBuf<double4> stamp;  // collision stamps: target xyz + weight
     DBuf<unsigned long long> hkeys;
     DBuf<int> hvals;
     DBuf<double> part, part2, spart, rhs_red, gram_red, q, Xred, beta_red, norms;
@@ -274,7 +274,7 @@ struct cs_scene {
         const int* sb = with_stamps ? seg_beg.p : nullptr;
         k_assemble_rhs<<<grid(nf), 256, 0, s>>>(nf, free_ids.p, xcl, zc, mh2.p, edges(), rinc_ptr.p, rinc.p,
                                                 has_fp ? hfp_ptr.p : nullptr, hfp_col.p, hfp_val.p, xcl, sb,
-                                                seg_end.p, ssrc_s.p, sw.p, stt.p, b.p, delta.p);
+                                                seg_end.p, ssrc_s.p, stamp.p, b.p, delta.p);
         ++launches;
         CS_CHECK_LAUNCH();
         return 0;
@@ -855,8 +855,7 @@ struct cs_scene {
         CS_RET(ssrc.ensure(m));
         CS_RET(skey_s.ensure(m));
         CS_RET(ssrc_s.ensure(m));
-        CS_RET(sw.ensure(m));
-        CS_RET(stt.ensure(3 * m));
+        CS_RET(stamp.ensure(m));
         CS_RET(rowflag.ensure(m));
         CS_RET(rows_act.ensure(m));
         // compact engaged pair ids in pair order
@@ -866,7 +865,7 @@ struct cs_scene {
         CS_RET(cub_tmp.ensure(bytes));
         CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, pr.engaged.p, sel.p, d_iscal.p + I_BAD, (int)pr.P, s));
         k_collision_terms<<<grid(A), 256, 0, s>>>(sel.p, A, pr.kind.p, pr.idx.p, xw, pr.bary.p, pr.normal.p,
-                                                  pr.weight.p, cfg.d_hat, n, free_index.p, 0, skey.p, sw.p, stt.p);
+                                                  pr.weight.p, cfg.d_hat, n, free_index.p, 0, skey.p, stamp.p);
         k_iota<<<grid(m), 256, 0, s>>>(ssrc.p, m);
         launches += 2;
         // stable sort of the 4A entries by free row keeps np.add.at's per-vertex order
@@ -1092,7 +1091,7 @@ void cs_scene::release() {
     for (auto* p : ints) p->release();
     DBuf<double>* dbl[] = {&mass, &fext, &mh2, &erest, &ew, &bk, &bw, &sell_val, &diag, &hfp_val, &U, &V, &lam,
                            &x, &v, &xprev, &df, &obs, &z, &xs_w, &xc_w, &anchor_w, &tmp_w, &xf, &xf0, &b, &t,
-                           &delta, &prev_outer, &grad, &fr, &pins_next_d, &obs_next_d, &vlo, &vhi, &vdisp, &tdisp, &edisp, &sw, &stt,
+                           &delta, &prev_outer, &grad, &fr, &pins_next_d, &obs_next_d, &vlo, &vhi, &vdisp, &tdisp, &edisp,
                            &part, &part2, &spart, &rhs_red, &gram_red, &q, &Xred, &beta_red, &d_scal, &norms};
     for (auto* p : dbl) p->release();
     tri_static.release();
@@ -1102,6 +1101,7 @@ void cs_scene::release() {
     eflip.release();
     keep_flag.release();
     isect_out.release();
+    stamp.release();
     hkeys.release();
     cub_tmp.release();
     pa.release();
@@ -1367,10 +1367,10 @@ int cs_scene::residual_forward(const double* xfw, cs_step_report* rep) {
     // f_r = -grad E at x_final (quad collision form), delta from stamps
     k_energy_grad<<<grid(n), 256, 0, s>>>(n, x.p, z.p, mass.p, cfg.h, edges(), ginc_ptr.p, ginc.p,
                                           BendSet{st.p, bk.p, bw.p}, binc_ptr.p, binc.p, free_index.p,
-                                          stamps_valid ? seg_beg.p : nullptr, seg_end.p, ssrc_s.p, sw.p, stt.p,
+                                          stamps_valid ? seg_beg.p : nullptr, seg_end.p, ssrc_s.p, stamp.p,
                                           grad.p);
     k_neg_gather<<<grid(nf), 256, 0, s>>>(grad.p, free_ids.p, nf, fr.p);
-    k_stamp_delta<<<grid(nf), 256, 0, s>>>(nf, stamps_valid ? seg_beg.p : nullptr, seg_end.p, ssrc_s.p, sw.p,
+    k_stamp_delta<<<grid(nf), 256, 0, s>>>(nf, stamps_valid ? seg_beg.p : nullptr, seg_end.p, ssrc_s.p, stamp.p,
                                            delta.p);
     launches += 3;
     CS_CHECK_LAUNCH();
@@ -1645,11 +1645,9 @@ int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const int* c
         CS_RET(sc->ssrc.ensure(m));
         CS_RET(sc->skey_s.ensure(m));
         CS_RET(sc->ssrc_s.ensure(m));
-        CS_RET(sc->sw.ensure(m));
-        CS_RET(sc->stt.ensure(3LL * m));
+        CS_RET(sc->stamp.ensure(m));
         CS_RET(sc->rowflag.ensure(m));
-        CS_TRY(cudaMemcpyAsync(sc->sw.p, coll_w, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
-        CS_TRY(cudaMemcpyAsync(sc->stt.p, coll_t, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, s));
+        k_pack_stamps<<<sc->grid(m), 256, 0, s>>>(coll_w, coll_t, m, sc->stamp.p);
         k_stamp_keys<<<sc->grid(m), 256, 0, s>>>(coll_ids, m, sc->free_index.p, sc->n, sc->skey.p);
         k_iota<<<sc->grid(m), 256, 0, s>>>(sc->ssrc.p, m);
         size_t bytes = 0;
@@ -1665,7 +1663,7 @@ int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const int* c
     k_assemble_rhs<<<sc->grid(sc->nf), 256, 0, s>>>(sc->nf, sc->free_ids.p, x, z, sc->mh2.p, sc->edges(),
                                                     sc->rinc_ptr.p, sc->rinc.p, sc->has_fp ? sc->hfp_ptr.p : nullptr,
                                                     sc->hfp_col.p, sc->hfp_val.p, x, with ? sc->seg_beg.p : nullptr,
-                                                    sc->seg_end.p, sc->ssrc_s.p, sc->sw.p, sc->stt.p, b, delta);
+                                                    sc->seg_end.p, sc->ssrc_s.p, sc->stamp.p, b, delta);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(s));
     return 0;
@@ -1696,13 +1694,12 @@ int cs_collision_terms(cs_scene* sc, const int8_t* kind, const int* idx4, const 
     if (A == 0) return 0;
     const long long m = 4 * A;
     CS_RET(sc->skey.ensure(m));
-    CS_RET(sc->sw.ensure(m));
-    CS_RET(sc->stt.ensure(3 * m));
+    CS_RET(sc->stamp.ensure(m));
     CS_RET(sc->rowflag.ensure(m));
     CS_RET(sc->rows_act.ensure(m));
     k_collision_terms<<<sc->grid(A), 256, 0, s>>>(sc->sel.p, A, kind, (const int4*)idx4, x_world, bary, normal, weight,
-                                                  sc->cfg.d_hat, sc->n, sc->free_index.p, 0, sc->skey.p, sc->sw.p,
-                                                  sc->stt.p);
+                                                  sc->cfg.d_hat, sc->n, sc->free_index.p, 0, sc->skey.p,
+                                                  sc->stamp.p);
     CS_RET(sc->keep_flag.ensure(m));
     k_key_kept<<<sc->grid(m), 256, 0, s>>>(sc->skey.p, (int)m, sc->nf, sc->keep_flag.p);
     bytes = 0;
@@ -1711,7 +1708,7 @@ int cs_collision_terms(cs_scene* sc, const int8_t* kind, const int* idx4, const 
     CS_TRY(cub::DeviceSelect::Flagged(sc->cub_tmp.p, bytes, it, sc->keep_flag.p, sc->rows_act.p,
                                       sc->d_iscal.p + I_FLAG, (int)m, s));
     k_gather_terms<<<std::max(1, std::min(sc->grid(m), 16 * sc->sm_count)), 256, 0, s>>>(
-        sc->rows_act.p, sc->d_iscal.p + I_FLAG, sc->sel.p, (const int4*)idx4, sc->sw.p, sc->stt.p, ids, w, targets);
+        sc->rows_act.p, sc->d_iscal.p + I_FLAG, sc->sel.p, (const int4*)idx4, sc->stamp.p, ids, w, targets);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaMemcpyAsync(&sc->h_iscal[I_FLAG], sc->d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
     CS_TRY(cudaStreamSynchronize(s));
@@ -1786,11 +1783,9 @@ int cs_energy_gradient(cs_scene* sc, const double* x, const double* z, const int
         CS_RET(sc->ssrc.ensure(m));
         CS_RET(sc->skey_s.ensure(m));
         CS_RET(sc->ssrc_s.ensure(m));
-        CS_RET(sc->sw.ensure(m));
-        CS_RET(sc->stt.ensure(3LL * m));
+        CS_RET(sc->stamp.ensure(m));
         CS_RET(sc->rowflag.ensure(m));
-        CS_TRY(cudaMemcpyAsync(sc->sw.p, q_w, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
-        CS_TRY(cudaMemcpyAsync(sc->stt.p, q_t, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, s));
+        k_pack_stamps<<<sc->grid(m), 256, 0, s>>>(q_w, q_t, m, sc->stamp.p);
         k_stamp_keys<<<sc->grid(m), 256, 0, s>>>(q_ids, m, sc->free_index.p, sc->n, sc->skey.p);
         k_iota<<<sc->grid(m), 256, 0, s>>>(sc->ssrc.p, m);
         size_t bytes = 0;
@@ -1805,7 +1800,7 @@ int cs_energy_gradient(cs_scene* sc, const double* x, const double* z, const int
     k_energy_grad<<<sc->grid(sc->n), 256, 0, s>>>(sc->n, x, z, sc->mass.p, sc->cfg.h, sc->edges(), sc->ginc_ptr.p,
                                                   sc->ginc.p, BendSet{sc->st.p, sc->bk.p, sc->bw.p}, sc->binc_ptr.p,
                                                   sc->binc.p, sc->free_index.p, with ? sc->seg_beg.p : nullptr,
-                                                  sc->seg_end.p, sc->ssrc_s.p, sc->sw.p, sc->stt.p, grad);
+                                                  sc->seg_end.p, sc->ssrc_s.p, sc->stamp.p, grad);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(s));
     return 0;

@@ -844,7 +844,7 @@ __global__ void k_collision_terms(const int* __restrict__ sel, int64_t A, const 
                                   const double* __restrict__ bary, const double* __restrict__ normal,
                                   const double* __restrict__ weight, double d_hat, int n_cloth,
                                   const int* __restrict__ free_index, int cloth_only,
-                                  int* __restrict__ key, double* __restrict__ w_out, double* __restrict__ t_out) {
+                                  int* __restrict__ key, double4* __restrict__ stamp_out) {
     int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (a >= A) return;
     const int i = sel[a];
@@ -896,8 +896,7 @@ __global__ void k_collision_terms(const int* __restrict__ sel, int64_t A, const 
         if (cloth_only && ids[k] >= n_cloth) keep = false;
         int64_t o = 4 * a + k;
         key[o] = keep ? free_index[ids[k]] : 0x7fffffff;
-        w_out[o] = w;
-        st3(t_out, o, tg);
+        stamp_out[o] = make_double4(tg.x, tg.y, tg.z, w);
     }
 }
 

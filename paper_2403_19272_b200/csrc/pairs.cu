@@ -107,7 +107,7 @@ __global__ void k_key_kept(const int* __restrict__ key, int m, int nf, uint8_t* 
 }
 __global__ void k_gather_terms(const int* __restrict__ pick, const int* __restrict__ count,
                                const int* __restrict__ sel, const int4* __restrict__ idx,
-                               const double* __restrict__ w, const double* __restrict__ t, int* __restrict__ ids_out,
+                               const double4* __restrict__ stamp, int* __restrict__ ids_out,
                                double* __restrict__ w_out, double* __restrict__ t_out) {
     const int n = count[0];
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -115,10 +115,11 @@ __global__ void k_gather_terms(const int* __restrict__ pick, const int* __restri
         const int4 id = idx[sel[o >> 2]];
         const int slot = o & 3;
         ids_out[k] = slot == 0 ? id.x : (slot == 1 ? id.y : (slot == 2 ? id.z : id.w));
-        w_out[k] = w[o];
-        t_out[3 * k] = t[3 * o];
-        t_out[3 * k + 1] = t[3 * o + 1];
-        t_out[3 * k + 2] = t[3 * o + 2];
+        const double4 st = stamp[o];
+        w_out[k] = st.w;
+        t_out[3 * k] = st.x;
+        t_out[3 * k + 1] = st.y;
+        t_out[3 * k + 2] = st.z;
     }
 }
 
@@ -188,13 +189,21 @@ __global__ void k_velocity_update(const double* __restrict__ xfin, const double*
 
 // delta_i = sum of stamp weights in np.add.at order (stepper.py:653-657)
 __global__ void k_stamp_delta(int nf, const int* __restrict__ seg_beg, const int* __restrict__ seg_end,
-                              const int* __restrict__ src, const double* __restrict__ w, double* __restrict__ delta) {
+                              const int* __restrict__ src, const double4* __restrict__ stamp,
+                              double* __restrict__ delta) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nf) return;
     double d = 0.0;
     if (seg_beg != nullptr)
-        for (int k = seg_beg[i]; k < seg_end[i]; ++k) d = d + w[src[k]];
+        for (int k = seg_beg[i]; k < seg_end[i]; ++k) d = d + stamp[src[k]].w;
     delta[i] = d;
+}
+
+// per-stage inputs (flat weights, targets) -> the driver's stamp records
+__global__ void k_pack_stamps(const double* __restrict__ w, const double* __restrict__ t, int m,
+                              double4* __restrict__ stamp) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) stamp[i] = make_double4(t[3 * i], t[3 * i + 1], t[3 * i + 2], w[i]);
 }
 
 // stamp sort keys from cloth vertex ids: free row or sentinel (constraints.py:252-255)

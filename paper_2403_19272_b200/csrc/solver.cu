@@ -164,8 +164,8 @@ __global__ void k_assemble_rhs(int nf, const int* __restrict__ free_ids, const d
                                const int* __restrict__ fp_ptr, const int* __restrict__ fp_col,
                                const double* __restrict__ fp_val, const double* __restrict__ pins,
                                const int* __restrict__ seg_beg, const int* __restrict__ seg_end,
-                               const int* __restrict__ stamp_src, const double* __restrict__ stamp_w,
-                               const double* __restrict__ stamp_t, double* __restrict__ b,
+                               const int* __restrict__ stamp_src, const double4* __restrict__ stamp,
+                               double* __restrict__ b,
                                double* __restrict__ delta) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nf) return;
@@ -195,10 +195,10 @@ __global__ void k_assemble_rhs(int nf, const int* __restrict__ free_ids, const d
     double dl = 0.0;
     if (seg_beg != nullptr) {
         for (int k = seg_beg[i]; k < seg_end[i]; ++k) {
-            const int src = stamp_src[k];
-            const double w = stamp_w[src];
+            const double4 st = stamp[stamp_src[k]];  // target xyz + weight, one 32-byte sector
+            const double w = st.w;
             dl = dl + w;
-            bi = bi + w * ld3(stamp_t, src);
+            bi = bi + w * d3{st.x, st.y, st.z};
         }
     }
     st3(b, i, bi);
@@ -725,8 +725,7 @@ __global__ void k_energy_grad(int n, const double* __restrict__ x, const double*
                               BendSet Bd, const int* __restrict__ binc_ptr, const int* __restrict__ binc,
                               const int* __restrict__ free_index, const int* __restrict__ seg_beg,
                               const int* __restrict__ seg_end, const int* __restrict__ stamp_src,
-                              const double* __restrict__ stamp_w, const double* __restrict__ stamp_t,
-                              double* __restrict__ grad) {
+                              const double4* __restrict__ stamp, double* __restrict__ grad) {
     int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     const int fi = free_index[v];
@@ -761,8 +760,8 @@ __global__ void k_energy_grad(int n, const double* __restrict__ x, const double*
     }
     if (seg_beg != nullptr) {
         for (int k = seg_beg[fi]; k < seg_end[fi]; ++k) {
-            const int src = stamp_src[k];
-            g = g + stamp_w[src] * (xv - ld3(stamp_t, src));
+            const double4 st = stamp[stamp_src[k]];
+            g = g + st.w * (xv - d3{st.x, st.y, st.z});
         }
     }
     st3(grad, v, g);
