@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(256) k_site_filter(const unsigned long long* _
     wl_append(need_dist, i, wl_dist, counts + 1);
 }
 
-__global__ void __launch_bounds__(128) k_full_ccd_wl(const int* __restrict__ wl, const int* __restrict__ count,
+__global__ void __launch_bounds__(128, 6) k_full_ccd_wl(const int* __restrict__ wl, const int* __restrict__ count,
                                                      const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                                                      const double* __restrict__ x0, const double* __restrict__ x1,
                                                      int single, double tol, double* __restrict__ toi_out) {
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(128) k_full_ccd_wl(const int* __restrict__ wl,
 // distance march over its worklist + the minimum folded with one atomicMin on the
 // (non-negative) fp64 bit pattern per block - exact and order independent.
 // min_slot must hold +inf before the launch.
-__global__ void __launch_bounds__(128) k_distance_toi_wl(const int* __restrict__ wl, const int* __restrict__ count,
+__global__ void __launch_bounds__(128, 6) k_distance_toi_wl(const int* __restrict__ wl, const int* __restrict__ count,
                                                          const int8_t* __restrict__ kind,
                                                          const int4* __restrict__ idx, const double* __restrict__ x0,
                                                          const double* __restrict__ x1, double floor_frac,
@@ -694,7 +694,7 @@ __global__ void k_clamp_from_min(const unsigned long long* __restrict__ min_slot
 }
 
 // Witness refresh: bary/params, distance and separating normal (stepper.py:194-216).
-__global__ void k_witness(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+__global__ void __launch_bounds__(128, 8) k_witness(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                           const double* __restrict__ x, int64_t P, double* __restrict__ bary,
                           double* __restrict__ dist, double* __restrict__ normal, double* __restrict__ p1_out,
                           double* __restrict__ p2_out) {
@@ -753,7 +753,7 @@ struct SamplePattern {
 };
 
 // Partial CCD classifier + NDB update, one pass per inner LG iteration.
-__global__ void k_partial_ndb(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+__global__ void __launch_bounds__(128, 6) k_partial_ndb(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                               const double* __restrict__ xa, const double* __restrict__ xc, int64_t P,
                               SamplePattern pat, const double* __restrict__ bary,
                               const double* __restrict__ normal, double d_hat, double k_ndb, double base,
@@ -839,7 +839,7 @@ __global__ void k_engage_init(const double* __restrict__ toi, const double* __re
 // Per engaged pair: 4 positional targets (stepper.py:238-285).  Entries for
 // immovable or zero-weight endpoints get key 0x7fffffff (sorted to the end).
 // frozen_k >= 0 selects residual forwarding's frozen weights (stepper.py:635-642).
-__global__ void k_collision_terms(const int* __restrict__ sel, int64_t A, const int8_t* __restrict__ kind,
+__global__ void __launch_bounds__(256, 4) k_collision_terms(const int* __restrict__ sel, int64_t A, const int8_t* __restrict__ kind,
                                   const int4* __restrict__ idx, const double* __restrict__ xw,
                                   const double* __restrict__ bary, const double* __restrict__ normal,
                                   const double* __restrict__ weight, double d_hat, int n_cloth,
