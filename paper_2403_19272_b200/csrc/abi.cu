@@ -495,10 +495,11 @@ struct cs_scene {
         CS_RET(etab.part.ensure(4LL * ge));
         k_prim_boxes<3><<<gt, 256, 0, s>>>(wtris.p, ntw, tri_static.p, vlo.p, vhi.p, vdisp.p, ttab.box.p, tdisp.p,
                                            ttab.part.p);
-        k_cell_size<<<1, 256, 0, s>>>(ttab.part.p, gt, ttab.inv.p);
+        static const double cell_scale = std::getenv("CS_CELL_SCALE") ? std::atof(std::getenv("CS_CELL_SCALE")) : 1.0;
+        k_cell_size<<<1, 256, 0, s>>>(ttab.part.p, gt, ttab.inv.p, cell_scale);
         k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, vdisp.p, etab.box.p, edisp.p,
                                            etab.part.p);
-        k_cell_size<<<1, 256, 0, s>>>(etab.part.p, ge, etab.inv.p);
+        k_cell_size<<<1, 256, 0, s>>>(etab.part.p, ge, etab.inv.p, cell_scale);
         launches += 6;
         const BoxSrc vs{nullptr, vlo.p, vhi.p, vert_used.p, nw};
         const BoxSrc ts{ttab.box.p, nullptr, nullptr, nullptr, ntw};

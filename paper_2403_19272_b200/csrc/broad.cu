@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(256) k_prim_boxes(const int* __restrict__ vert
 
 // inv_cell[0] = 1 / mean max-axis box extent of the moving primitives (all
 // primitives if none move); fixed-order reduction of the block partials.
-__global__ void k_cell_size(const double* __restrict__ part, int nparts, double* __restrict__ inv_cell) {
+__global__ void k_cell_size(const double* __restrict__ part, int nparts, double* __restrict__ inv_cell,
+                            double scale = 1.0) {
     __shared__ double sh[4][256];
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int b = threadIdx.x; b < nparts; b += blockDim.x)
@@ -135,6 +136,7 @@ __global__ void k_cell_size(const double* __restrict__ part, int nparts, double*
     }
     if (threadIdx.x == 0) {
         double cell = sh[1][0] > 0.0 ? sh[0][0] / sh[1][0] : (sh[3][0] > 0.0 ? sh[2][0] / sh[3][0] : 1.0);
+        cell *= scale;
         if (!(cell > 1e-12)) cell = 1e-12;
         inv_cell[0] = 1.0 / cell;
     }
