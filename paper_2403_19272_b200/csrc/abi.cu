@@ -198,6 +198,7 @@ struct cs_scene {
     DBuf<double> z, xs_w, xc_w, anchor_w, tmp_w, xf, xf0, b, t, delta, prev_outer, grad, fr;
     DBuf<double> pins_next_d, obs_next_d;
     DBuf<double> vlo, vhi, vdisp, tdisp, edisp;
+    DBuf<float> fvbox, ftbox, febox;  // fp32 outward-rounded copies for the site filter
     double bmargin = 0.0;
     PairBuf pa, pb;  // current and next pair sets
     PairBuf* cur = &pa;
@@ -487,18 +488,18 @@ struct cs_scene {
 
     // broad phase into pr (bvh.py:207-292): entry tables -> bucket-pair count -> scan -> write; two host syncs
     int broad_phase(const double* xa, const double* xb, double margin, PairBuf& pr) {
-        k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(xa, xb, nw, margin, vlo.p, vhi.p);
-        k_vertex_disp<<<grid(nw), 256, 0, s>>>(xa, xb, nw, vdisp.p);
+        k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(xa, xb, nw, margin, vlo.p, vhi.p, fvbox.p);
+        k_vertex_disp<<<grid(nw), 256, 0, s>>>(xa, xb, nw, vdisp.p, fvbox.p);
         bmargin = margin;
         const int gt = grid(ntw), ge = grid(new_);
         CS_RET(ttab.part.ensure(4LL * gt));
         CS_RET(etab.part.ensure(4LL * ge));
         k_prim_boxes<3><<<gt, 256, 0, s>>>(wtris.p, ntw, tri_static.p, vlo.p, vhi.p, vdisp.p, ttab.box.p, tdisp.p,
-                                           ttab.part.p);
+                                           ttab.part.p, ftbox.p);
         static const double cell_scale = std::getenv("CS_CELL_SCALE") ? std::atof(std::getenv("CS_CELL_SCALE")) : 1.0;
         k_cell_size<<<1, 256, 0, s>>>(ttab.part.p, gt, ttab.inv.p, cell_scale);
         k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, vdisp.p, etab.box.p, edisp.p,
-                                           etab.part.p);
+                                           etab.part.p, febox.p);
         k_cell_size<<<1, 256, 0, s>>>(etab.part.p, ge, etab.inv.p, cell_scale);
         launches += 6;
         const BoxSrc vs{nullptr, vlo.p, vhi.p, vert_used.p, nw};
@@ -637,13 +638,13 @@ struct cs_scene {
         CS_TRY(cudaStreamSynchronize(s));
         if (h_iscal[I_FLAG]) return 0;
         // boxes of this site (static), then the surviving subset of prev
-        k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(x, x, nw, margin, vlo.p, vhi.p);
-        k_vertex_disp<<<grid(nw), 256, 0, s>>>(x, x, nw, vdisp.p);
+        k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(x, x, nw, margin, vlo.p, vhi.p, fvbox.p);
+        k_vertex_disp<<<grid(nw), 256, 0, s>>>(x, x, nw, vdisp.p, fvbox.p);
         const int gt = grid(ntw), ge = grid(new_);
         k_prim_boxes<3><<<gt, 256, 0, s>>>(wtris.p, ntw, tri_static.p, vlo.p, vhi.p, vdisp.p, ttab.box.p, tdisp.p,
-                                           ttab.part.p);
+                                           ttab.part.p, ftbox.p);
         k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, vdisp.p, etab.box.p, edisp.p,
-                                           etab.part.p);
+                                           etab.part.p, febox.p);
         const long long P0 = prev.P;
         CS_RET(keep_flag.ensure(P0));
         CS_RET(sel.ensure(P0));
@@ -759,7 +760,7 @@ struct cs_scene {
             CS_RET(wl_full.ensure(P));
             CS_RET(wl_dist.ensure(P));
             CS_TRY(cudaMemsetAsync(d_iscal.p + I_WLF, 0, 2 * sizeof(int), s));
-            const SiteBoxes SB{vlo.p, vhi.p, vdisp.p, ttab.box.p, tdisp.p, etab.box.p, edisp.p, bmargin};
+            const SiteBoxes SB{(const float4*)fvbox.p, (const float4*)ftbox.p, (const float4*)febox.p, bmargin};
             k_site_filter<<<grid(P), 256, 0, s>>>(pr.keys.p, P, SB, 1e-6, 1.0 - cfg.alpha, pr.toi.p, pr.filt.p,
                                                   wl_full.p, wl_dist.p, d_iscal.p + I_WLF);
             const int gw = std::max(1, std::min(grid(P, 128), 16 * sm_count));
@@ -1051,6 +1052,9 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(vlo.ensure(3LL * nw));
     CS_RET(vhi.ensure(3LL * nw));
     CS_RET(vdisp.ensure(nw, true));
+    CS_RET(fvbox.ensure(8LL * nw, true));
+    CS_RET(ftbox.ensure(8LL * ntw, true));
+    CS_RET(febox.ensure(8LL * new_, true));
     CS_RET(tdisp.ensure(ntw, true));
     CS_RET(edisp.ensure(new_, true));
     CS_RET(seg_beg.ensure(nf));
@@ -1102,6 +1106,9 @@ void cs_scene::release() {
     eflip.release();
     keep_flag.release();
     isect_out.release();
+    fvbox.release();
+    ftbox.release();
+    febox.release();
     stamp.release();
     hkeys.release();
     cub_tmp.release();

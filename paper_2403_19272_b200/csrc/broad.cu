@@ -38,21 +38,35 @@ namespace cs {
 
 constexpr long long kMaxCellsPerPrim = 1LL << 15;
 
+// fbox (optional): the same boxes in fp32 rounded outward (lo down, hi up) as 32-byte
+// records {lo.xyz, hi.xyz, max displacement (rounded up), 0} - one sector per
+// primitive for the narrow-phase filter
 __global__ void k_vertex_boxes(const double* __restrict__ x0, const double* __restrict__ x1, int n, double margin,
-                               double* __restrict__ vlo, double* __restrict__ vhi) {
+                               double* __restrict__ vlo, double* __restrict__ vhi, float* __restrict__ fbox = nullptr) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 3 * n) return;
     const double a = x0[i], b = x1[i];
-    vlo[i] = np_min(a, b) - margin;
-    vhi[i] = np_max(a, b) + margin;
+    const double lo = np_min(a, b) - margin, hi = np_max(a, b) + margin;
+    vlo[i] = lo;
+    vhi[i] = hi;
+    if (fbox) {
+        const int v = i / 3, c = i - 3 * v;
+        fbox[8 * (int64_t)v + c] = __double2float_rd(lo);
+        fbox[8 * (int64_t)v + 3 + c] = __double2float_ru(hi);
+    }
 }
 
 // |x_end - x_start| per vertex, as the reference's distance march computes it (ccd.py:240)
 __global__ void k_vertex_disp(const double* __restrict__ x0, const double* __restrict__ x1, int n,
-                              double* __restrict__ vdisp) {
+                              double* __restrict__ vdisp, float* __restrict__ fbox = nullptr) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
-    vdisp[v] = norm3(ld3(x1, v) - ld3(x0, v));
+    const double d = norm3(ld3(x1, v) - ld3(x0, v));
+    vdisp[v] = d;
+    if (fbox) {
+        fbox[8 * (int64_t)v + 6] = __double2float_ru(d);
+        fbox[8 * (int64_t)v + 7] = 0.0f;
+    }
 }
 
 // ------------------------------------------------------------------ boxes + cell size
@@ -64,7 +78,8 @@ __global__ void __launch_bounds__(256) k_prim_boxes(const int* __restrict__ vert
                                                     const uint8_t* __restrict__ is_static,
                                                     const double* __restrict__ vlo, const double* __restrict__ vhi,
                                                     const double* __restrict__ vdisp, double* __restrict__ box,
-                                                    double* __restrict__ pdisp, double* __restrict__ part) {
+                                                    double* __restrict__ pdisp, double* __restrict__ part,
+                                                    float* __restrict__ fbox = nullptr) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     if (p < np) {
@@ -74,6 +89,10 @@ __global__ void __launch_bounds__(256) k_prim_boxes(const int* __restrict__ vert
 #pragma unroll
         for (int k = 1; k < ARITY; ++k) dmax = fmax(dmax, vdisp[verts[ARITY * p + k]]);
         pdisp[p] = dmax;
+        if (fbox) {
+            fbox[8 * (int64_t)p + 6] = __double2float_ru(dmax);
+            fbox[8 * (int64_t)p + 7] = 0.0f;
+        }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             lo[c] = vlo[3 * a + c];
@@ -92,6 +111,10 @@ __global__ void __launch_bounds__(256) k_prim_boxes(const int* __restrict__ vert
         for (int c = 0; c < 3; ++c) {
             box[6 * (int64_t)p + c] = lo[c];
             box[6 * (int64_t)p + 3 + c] = hi[c];
+            if (fbox) {
+                fbox[8 * (int64_t)p + c] = __double2float_rd(lo[c]);
+                fbox[8 * (int64_t)p + 3 + c] = __double2float_ru(hi[c]);
+            }
         }
         const double ext = fmax(fmax(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
         const bool moving = !is_static[p];

@@ -569,21 +569,31 @@ __device__ __forceinline__ void wl_append(bool want, int64_t i, int* __restrict_
 }
 
 // Settling works from the broad phase's primitive data of the same site (no
-// per-pair corner gathers): margin-inflated swept boxes (vertex / triangle / edge)
-// and per-primitive max displacement norms.  Removing the margin from both boxes
+// per-pair corner gathers): margin-inflated swept boxes (vertex / triangle / edge,
+// fp32 copies rounded outward - they contain the fp64 boxes, so every gap below
+// only shrinks) and per-primitive max displacement norms.  Removing the margin from both boxes
 // widens their gap by 2 x margin; the 1e-9 x |coordinate| slack covers the
 // rounding of the inflation, so g below is a lower bound on the true gap between
 // the two sides' swept (and hence start) positions.
 struct SiteBoxes {
-    const double* __restrict__ vlo;    // (n_w,3) vertex boxes
-    const double* __restrict__ vhi;
-    const double* __restrict__ vdisp;  // (n_w) |x_end - x_start| per vertex
-    const double* __restrict__ tbox;   // (tris,6)
-    const double* __restrict__ tdisp;  // (tris) max vertex displacement
-    const double* __restrict__ ebox;   // (edges,6)
-    const double* __restrict__ edisp;
+    const float4* __restrict__ vbox;   // (n_w,2) vertex records {lo.xyz, hi.x}, {hi.yz, disp, 0}
+    const float4* __restrict__ tbox;   // (tris,2)
+    const float4* __restrict__ ebox;   // (edges,2)
     double margin;
 };
+
+// one 32-byte record: conservative box (fp32, rounded outward) + max displacement (rounded up)
+__device__ __forceinline__ void load_frec(const float4* __restrict__ rec, int p, double lo[3], double hi[3],
+                                          double& disp) {
+    const float4 a = rec[2 * (int64_t)p], b = rec[2 * (int64_t)p + 1];
+    lo[0] = a.x;
+    lo[1] = a.y;
+    lo[2] = a.z;
+    hi[0] = a.w;
+    hi[1] = b.x;
+    hi[2] = b.y;
+    disp = b.z;
+}
 
 __global__ void __launch_bounds__(256) k_site_filter(const unsigned long long* __restrict__ keys, int64_t P,
                                                      SiteBoxes B, double tol, double floor_frac,
@@ -598,19 +608,11 @@ __global__ void __launch_bounds__(256) k_site_filter(const unsigned long long* _
         const int p = (int)((k >> 32) & 0x7fffffffu), q = (int)(k & 0xffffffffu);
         double alo[3], ahi[3], blo[3], bhi[3], LA, LB;
         if (k >> 63) {
-            load_box(B.ebox, p, alo, ahi);
-            load_box(B.ebox, q, blo, bhi);
-            LA = B.edisp[p];
-            LB = B.edisp[q];
+            load_frec(B.ebox, p, alo, ahi, LA);
+            load_frec(B.ebox, q, blo, bhi, LB);
         } else {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                alo[c] = B.vlo[3 * (int64_t)p + c];
-                ahi[c] = B.vhi[3 * (int64_t)p + c];
-            }
-            load_box(B.tbox, q, blo, bhi);
-            LA = B.vdisp[p];
-            LB = B.tdisp[q];
+            load_frec(B.vbox, p, alo, ahi, LA);
+            load_frec(B.tbox, q, blo, bhi, LB);
         }
         double gm = -INFINITY, e2 = 0.0, mag = 0.0;
 #pragma unroll
@@ -625,7 +627,7 @@ __global__ void __launch_bounds__(256) k_site_filter(const unsigned long long* _
         const double bound = fmax(tol * fmax(2.0 * ext, 1.0), 1e-9 * fmax(ext, 1.0));
         need_full = !(g > bound * (1.0 + 1e-6));
         if (!need_full) toi_out[i] = NaN;
-        const double L = LA + LB;
+        const double L = (LA + LB) * (1.0 + 1e-12);  // >= the reference's L (records round up)
         bool settled = false;
         if (g > 0.0) {
             if (!(L > 0.0)) settled = L == 0.0;  // d > 0 and L == 0: never alive
