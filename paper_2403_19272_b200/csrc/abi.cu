@@ -54,7 +54,9 @@ struct DBuf {
         // every cudaFree/cudaMalloc of a large buffer stalls the stream
         size_t want = std::max<size_t>(m, 1);
         if (n) want = std::max(2 * want, n + n / 2);
-        else if (!exact && want > (1u << 16)) want *= 2;  // large first sizing: 2x
+        // large first sizing: 3x (per-step sizes grow while the cloth settles; a regrowth
+        // mid-run costs a device-synchronising cudaFree + cudaMalloc)
+        else if (!exact && want > (1u << 16)) want *= 3;
         static const bool trace = std::getenv("CS_TRACE_ALLOC") != nullptr;
         if (trace) std::fprintf(stderr, "[cs alloc] %zu -> %zu bytes\n", n * sizeof(T), want * sizeof(T));
         cudaError_t e = cudaMalloc(&p, want * sizeof(T));
