@@ -15,6 +15,8 @@ import paper_2403_19272_b200 as P  # noqa: E402
 kind, res, steps = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 cfg = P.StepConfig(h=1.0 / 200.0)
 kw = {"sheets": 2, "gap": 0.005} if kind == "stacked_twist" else {}
+if kind == "sphere_drape":      # BASELINE config 5 scene (317^2 drape, material 0)
+    kw = {}
 t0 = time.time()
 sim = P.build_scene(kind, resolution=res, config=cfg, eigensolver="device", **kw)
 print("setup_s", round(time.time() - t0, 1), "verts", sim.mesh.vertex_count, flush=True)
