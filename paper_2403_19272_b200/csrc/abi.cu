@@ -503,7 +503,9 @@ struct cs_scene {
         k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, vdisp.p, etab.box.p, edisp.p,
                                            etab.part.p, febox.p);
         k_cell_size<<<1, 256, 0, s>>>(etab.part.p, ge, etab.inv.p, cell_scale);
-        launches += 6;
+        k_prim_motion<3><<<gt, 256, 0, s>>>(wtris.p, ntw, xa, xb, ftbox.p);
+        k_prim_motion<2><<<ge, 256, 0, s>>>(wedges.p, new_, xa, xb, febox.p);
+        launches += 8;
         const BoxSrc vs{nullptr, vlo.p, vhi.p, vert_used.p, nw};
         const BoxSrc ts{ttab.box.p, nullptr, nullptr, nullptr, ntw};
         const BoxSrc es{etab.box.p, nullptr, nullptr, nullptr, new_};
@@ -647,6 +649,8 @@ struct cs_scene {
                                            ttab.part.p, ftbox.p);
         k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, vdisp.p, etab.box.p, edisp.p,
                                            etab.part.p, febox.p);
+        k_prim_motion<3><<<gt, 256, 0, s>>>(wtris.p, ntw, x, x, ftbox.p);
+        k_prim_motion<2><<<ge, 256, 0, s>>>(wedges.p, new_, x, x, febox.p);
         const long long P0 = prev.P;
         CS_RET(keep_flag.ensure(P0));
         CS_RET(sel.ensure(P0));
@@ -763,7 +767,7 @@ struct cs_scene {
             CS_RET(wl_dist.ensure(P));
             CS_TRY(cudaMemsetAsync(d_iscal.p + I_WLF, 0, 2 * sizeof(int), s));
             const SiteBoxes SB{(const float4*)fvbox.p, (const float4*)ftbox.p, (const float4*)febox.p, bmargin};
-            k_site_filter<<<grid(P), 256, 0, s>>>(pr.keys.p, P, SB, 1e-6, 1.0 - cfg.alpha, pr.toi.p, pr.filt.p,
+            k_site_filter<<<grid(P), 256, 0, s>>>(pr.keys.p, P, SB, 1e-6, 1.0 - cfg.alpha, 64, pr.toi.p, pr.filt.p,
                                                   wl_full.p, wl_dist.p, d_iscal.p + I_WLF);
             const int gw = std::max(1, std::min(grid(P, 128), 16 * sm_count));
             k_full_ccd_wl<<<gw, 128, 0, s>>>(wl_full.p, d_iscal.p + I_WLF, pr.kind.p, pr.idx.p, xa, xb,
@@ -1054,9 +1058,9 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(vlo.ensure(3LL * nw));
     CS_RET(vhi.ensure(3LL * nw));
     CS_RET(vdisp.ensure(nw, true));
-    CS_RET(fvbox.ensure(8LL * nw, true));
-    CS_RET(ftbox.ensure(8LL * ntw, true));
-    CS_RET(febox.ensure(8LL * new_, true));
+    CS_RET(fvbox.ensure(16LL * nw, true));
+    CS_RET(ftbox.ensure(16LL * ntw, true));
+    CS_RET(febox.ensure(16LL * new_, true));
     CS_RET(tdisp.ensure(ntw, true));
     CS_RET(edisp.ensure(new_, true));
     CS_RET(seg_beg.ensure(nf));

@@ -51,8 +51,8 @@ __global__ void k_vertex_boxes(const double* __restrict__ x0, const double* __re
     vhi[i] = hi;
     if (fbox) {
         const int v = i / 3, c = i - 3 * v;
-        fbox[8 * (int64_t)v + c] = __double2float_rd(lo);
-        fbox[8 * (int64_t)v + 3 + c] = __double2float_ru(hi);
+        fbox[16 * (int64_t)v + c] = __double2float_rd(lo);
+        fbox[16 * (int64_t)v + 3 + c] = __double2float_ru(hi);
     }
 }
 
@@ -61,11 +61,22 @@ __global__ void k_vertex_disp(const double* __restrict__ x0, const double* __res
                               double* __restrict__ vdisp, float* __restrict__ fbox = nullptr) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
-    const double d = norm3(ld3(x1, v) - ld3(x0, v));
+    const d3 p0 = ld3(x0, v), dp = ld3(x1, v) - p0;
+    const double d = norm3(dp);
     vdisp[v] = d;
     if (fbox) {
-        fbox[8 * (int64_t)v + 6] = __double2float_ru(d);
-        fbox[8 * (int64_t)v + 7] = 0.0f;
+        float* r = fbox + 16 * (int64_t)v;
+        r[6] = __double2float_ru(d);
+        r[7] = 0.0f;
+        // motion part: reference displacement c (= own), deviation 0, start position
+        r[8] = (float)dp.x;
+        r[9] = (float)dp.y;
+        r[10] = (float)dp.z;
+        r[11] = 0.0f;
+        r[12] = (float)p0.x;
+        r[13] = (float)p0.y;
+        r[14] = (float)p0.z;
+        r[15] = 0.0f;
     }
 }
 
@@ -90,8 +101,8 @@ __global__ void __launch_bounds__(256) k_prim_boxes(const int* __restrict__ vert
         for (int k = 1; k < ARITY; ++k) dmax = fmax(dmax, vdisp[verts[ARITY * p + k]]);
         pdisp[p] = dmax;
         if (fbox) {
-            fbox[8 * (int64_t)p + 6] = __double2float_ru(dmax);
-            fbox[8 * (int64_t)p + 7] = 0.0f;
+            fbox[16 * (int64_t)p + 6] = __double2float_ru(dmax);
+            fbox[16 * (int64_t)p + 7] = 0.0f;
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -112,8 +123,8 @@ __global__ void __launch_bounds__(256) k_prim_boxes(const int* __restrict__ vert
             box[6 * (int64_t)p + c] = lo[c];
             box[6 * (int64_t)p + 3 + c] = hi[c];
             if (fbox) {
-                fbox[8 * (int64_t)p + c] = __double2float_rd(lo[c]);
-                fbox[8 * (int64_t)p + 3 + c] = __double2float_ru(hi[c]);
+                fbox[16 * (int64_t)p + c] = __double2float_rd(lo[c]);
+                fbox[16 * (int64_t)p + 3 + c] = __double2float_ru(hi[c]);
             }
         }
         const double ext = fmax(fmax(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
@@ -163,6 +174,34 @@ __global__ void k_cell_size(const double* __restrict__ part, int nparts, double*
         if (!(cell > 1e-12)) cell = 1e-12;
         inv_cell[0] = 1.0 / cell;
     }
+}
+
+// Motion part of a primitive's filter record (floats 8..15): displacement c of its
+// first vertex, max deviation of its vertices' displacements from c (rounded up),
+// start position of its first vertex.  Lets the site filter bound a pair's RELATIVE
+// motion (distances are translation invariant) - cloth riding a moving body.
+template <int ARITY>
+__global__ void k_prim_motion(const int* __restrict__ verts, int np, const double* __restrict__ x0,
+                              const double* __restrict__ x1, float* __restrict__ fbox) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    const int a = verts[ARITY * p];
+    const d3 p0 = ld3(x0, a), c = ld3(x1, a) - p0;
+    double dev = 0.0;
+#pragma unroll
+    for (int k = 1; k < ARITY; ++k) {
+        const int b = verts[ARITY * p + k];
+        dev = fmax(dev, norm3((ld3(x1, b) - ld3(x0, b)) - c));
+    }
+    float* r = fbox + 16 * (int64_t)p;
+    r[8] = (float)c.x;
+    r[9] = (float)c.y;
+    r[10] = (float)c.z;
+    r[11] = __double2float_ru(dev);
+    r[12] = (float)p0.x;
+    r[13] = (float)p0.y;
+    r[14] = (float)p0.z;
+    r[15] = 0.0f;
 }
 
 // ------------------------------------------------------------------ cells

@@ -576,16 +576,18 @@ __device__ __forceinline__ void wl_append(bool want, int64_t i, int* __restrict_
 // rounding of the inflation, so g below is a lower bound on the true gap between
 // the two sides' swept (and hence start) positions.
 struct SiteBoxes {
-    const float4* __restrict__ vbox;   // (n_w,2) vertex records {lo.xyz, hi.x}, {hi.yz, disp, 0}
-    const float4* __restrict__ tbox;   // (tris,2)
-    const float4* __restrict__ ebox;   // (edges,2)
+    // 64-byte records per vertex / triangle / edge: {lo.xyz, hi.x} {hi.yz, disp, 0}
+    // {c.xyz, dev} {p0.xyz, 0} (broad.cu k_vertex_boxes / k_prim_boxes / k_prim_motion)
+    const float4* __restrict__ vbox;
+    const float4* __restrict__ tbox;
+    const float4* __restrict__ ebox;
     double margin;
 };
 
-// one 32-byte record: conservative box (fp32, rounded outward) + max displacement (rounded up)
+// conservative box (fp32, rounded outward) + max displacement (rounded up)
 __device__ __forceinline__ void load_frec(const float4* __restrict__ rec, int p, double lo[3], double hi[3],
                                           double& disp) {
-    const float4 a = rec[2 * (int64_t)p], b = rec[2 * (int64_t)p + 1];
+    const float4 a = rec[4 * (int64_t)p], b = rec[4 * (int64_t)p + 1];
     lo[0] = a.x;
     lo[1] = a.y;
     lo[2] = a.z;
@@ -596,7 +598,7 @@ __device__ __forceinline__ void load_frec(const float4* __restrict__ rec, int p,
 }
 
 __global__ void __launch_bounds__(256) k_site_filter(const unsigned long long* __restrict__ keys, int64_t P,
-                                                     SiteBoxes B, double tol, double floor_frac,
+                                                     SiteBoxes B, double tol, double floor_frac, int max_iter,
                                                      double* __restrict__ toi_out, double* __restrict__ filt_out,
                                                      int* __restrict__ wl_full, int* __restrict__ wl_dist,
                                                      int* __restrict__ counts) {
@@ -632,6 +634,24 @@ __global__ void __launch_bounds__(256) k_site_filter(const unsigned long long* _
         if (g > 0.0) {
             if (!(L > 0.0)) settled = L == 0.0;  // d > 0 and L == 0: never alive
             else if (floor_frac < 1.0) settled = g * (1.0 - floor_frac) * (1.0 - 1e-9) > L * (1.0 + 1e-9);
+        }
+        if (!settled && g > 0.0 && L > 0.0 && floor_frac < 1.0 && floor_frac >= 0.0 && max_iter >= 60) {
+            // relative motion (march_never_reaches with record bounds): c = first-vertex
+            // displacement, dev = spread around it, p0 = first-vertex start position;
+            // d0 <= |pA - pB| (both are points of the pair), every d_k >= g - Lrel
+            const float4* RA = (k >> 63) ? B.ebox : B.vbox;
+            const float4* RB = (k >> 63) ? B.ebox : B.tbox;
+            const float4 ca = RA[4 * (int64_t)p + 2], pa = RA[4 * (int64_t)p + 3];
+            const float4 cb = RB[4 * (int64_t)q + 2], pb = RB[4 * (int64_t)q + 3];
+            const d3 dc{(double)ca.x - (double)cb.x, (double)ca.y - (double)cb.y, (double)ca.z - (double)cb.z};
+            const double cmag = fabs((double)ca.x) + fabs((double)ca.y) + fabs((double)ca.z) + fabs((double)cb.x) +
+                                fabs((double)cb.y) + fabs((double)cb.z);
+            const double lrel = ((double)ca.w + (double)cb.w + norm3(dc)) * (1.0 + 1e-9) + 1e-6 * cmag;
+            const d3 dpp{(double)pa.x - (double)pb.x, (double)pa.y - (double)pb.y, (double)pa.z - (double)pb.z};
+            const double d_hi = norm3(dpp) * (1.0 + 1e-9) + 1e-6 * mag;
+            const double dmin = g - lrel;
+            const double goal_hi = floor_frac * d_hi;
+            settled = dmin > goal_hi * (1.0 + 2e-9) && ((dmin - goal_hi) / L) * 60.0 > 1.0 + 1e-9;
         }
         need_dist = !settled;
         if (settled) filt_out[i] = NaN;

@@ -195,3 +195,25 @@ def test_ccd_site_matches_oracle(cuda, rng, steps, jitter, move):
     assert _same(filt, ref_filt)
     if steps == 12 or move == 0.0:
         assert (~np.isnan(ref_filt)).any() or move == 0.0
+
+
+@pytest.mark.parametrize("angle,shift", [(0.02, 0.003), (0.005, 0.0)])
+def test_ccd_site_rigid_motion_matches_oracle(cuda, rng, angle, shift):
+    """Site filter's relative-motion bound (the whole world riding a rigid motion, like
+    the skirt on its spinning body): every pair's values still equal the oracle's."""
+    import paper_2403_19272_b200 as P
+    from oracle import narrow
+
+    sim = P.build_scene("sphere_drape", resolution=14, size=0.2, config=P.StepConfig())
+    for _ in range(12):
+        sim.step()
+    x0 = sim.world(sim.state.x)
+    ca, sa = np.cos(angle), np.sin(angle)
+    x1 = np.stack([ca * x0[:, 0] - sa * x0[:, 1], sa * x0[:, 0] + ca * x0[:, 1], x0[:, 2]], axis=1)
+    x1 = x1 + shift + 2e-5 * rng.normal(size=x0.shape)
+    pairs, toi, filt = sim._full_ccd_site(x0, x1)
+    assert len(pairs) > 0
+    ref_toi = narrow.full_ccd(pairs.kind, pairs.idx, x0, x1)
+    ref_filt = narrow.distance_toi(pairs.kind, pairs.idx, x0, x1, floor_frac=1.0 - sim.config.alpha)
+    assert _same(toi, ref_toi)
+    assert _same(filt, ref_filt)
