@@ -421,9 +421,12 @@ __device__ __forceinline__ void seg_seg_params_f(f3 a0, f3 a1, f3 b0, f3 b1, flo
 
 // The march's NaN proven without the fp64 witness distance: as march_never_reaches,
 // with d0 bracketed by [lower, upper] from an fp32-chosen direction (see above).
-__device__ __forceinline__ bool march_never_reaches_f32(int kd, const Corners& a, const Corners& b, double floor_frac,
-                                                        int max_iter) {
-    if (max_iter < 60 || !(floor_frac < 1.0) || !(floor_frac >= 0.0)) return false;
+// Lower bound on the pair's witness distance over t in [0, 1] (distances are
+// translation invariant: d(t) >= d(0) - relative motion), d(0) bracketed from an
+// fp32-chosen witness direction; returns -inf when undecided.  d_hi = upper bound on
+// d(0); L = upper bound on the reference's march Lipschitz constant.
+__device__ __forceinline__ double rel_motion_dmin(int kd, const Corners& a, const Corners& b, double& d_hi,
+                                                  double& L) {
     d3 r[4], dp[4];
     double mag = 0.0;
 #pragma unroll
@@ -457,7 +460,9 @@ __device__ __forceinline__ bool march_never_reaches_f32(int kd, const Corners& a
     }
     const d3 nv = pa - pb;
     const double len = norm3(nv);
-    if (!(len > 0.0)) return false;
+    d_hi = INFINITY;
+    L = 0.0;
+    if (!(len > 0.0)) return -INFINITY;
     const d3 n = (1.0 / len) * nv;
     const int na = kd == CS_VT ? 1 : 2;
     double lb = INFINITY;
@@ -467,7 +472,8 @@ __device__ __forceinline__ bool march_never_reaches_f32(int kd, const Corners& a
         for (int j = 1; j < 4; ++j)
             if (i < na && j >= na) lb = fmin(lb, dot3(r[i] - r[j], n));
     const double slack = 1e-12 * mag;
-    const double d_lo = lb * (1.0 - 1e-12) - slack, d_hi = len * (1.0 + 1e-12) + slack;
+    const double d_lo = lb * (1.0 - 1e-12) - slack;
+    d_hi = len * (1.0 + 1e-12) + slack;
     double ra = 0.0, rb = 0.0, la = 0.0, lbm = 0.0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -480,12 +486,30 @@ __device__ __forceinline__ bool march_never_reaches_f32(int kd, const Corners& a
             lbm = fmax(lbm, mvk);
         }
     }
-    const double L = (la + lbm) * (1.0 + 1e-12);  // >= the reference's L
+    L = (la + lbm) * (1.0 + 1e-12);  // >= the reference's L
+    return d_lo - (ra + rb) * (1.0 + 1e-12) - slack;
+}
+
+__device__ __forceinline__ bool march_never_reaches_f32(int kd, const Corners& a, const Corners& b, double floor_frac,
+                                                        int max_iter) {
+    if (max_iter < 60 || !(floor_frac < 1.0) || !(floor_frac >= 0.0)) return false;
+    double d_hi, L;
+    const double dmin = rel_motion_dmin(kd, a, b, d_hi, L);
     if (!(L > 0.0)) return false;
-    const double dmin = d_lo - (ra + rb) * (1.0 + 1e-12) - slack;
     const double goal_hi = floor_frac * d_hi;
     if (!(dmin > goal_hi * (1.0 + 2e-9))) return false;
     return ((dmin - goal_hi) / L) * 60.0 > 1.0 + 1e-9;
+}
+
+// full_ccd is NaN when the witness distance provably stays above every validation
+// threshold over t in [0, 1] (see separated_sides for the thresholds)
+__device__ __forceinline__ bool ccd_never_hits_f32(int kd, const Corners& a, const Corners& b, double tol) {
+    double d_hi, L;
+    const double dmin = rel_motion_dmin(kd, a, b, d_hi, L);
+    if (!(dmin > 0.0)) return false;
+    const double ext = pair_extent(a, b);
+    const double bound = fmax(tol * fmax(2.0 * ext, 1.0), 1e-9 * fmax(ext, 1.0));
+    return dmin > bound * (1.0 + 1e-6) + 1e-12 * (ext + 1.0);
 }
 
 __device__ double distance_toi_pair(int kd, const Corners& a, const Corners& b, double floor_frac, int max_iter) {
@@ -668,7 +692,10 @@ __global__ void __launch_bounds__(128, 6) k_full_ccd_wl(const int* __restrict__ 
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const int i = wl[k];
         const int4 id = idx[i];
-        toi_out[i] = full_ccd_pair(kind[i], gather4(x0, id), gather4(x1, id), single, tol);
+        const int kd = kind[i];
+        const Corners a = gather4(x0, id), b = gather4(x1, id);
+        toi_out[i] = ccd_never_hits_f32(kd, a, b, tol) ? __longlong_as_double(0x7ff8000000000000ULL)
+                                                       : full_ccd_pair(kd, a, b, single, tol);
     }
 }
 
