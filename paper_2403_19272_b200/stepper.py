@@ -40,13 +40,20 @@ class _Tracked(np.ndarray):
     """ndarray that records writes through item assignment (``a[...] = v``, also on
     views) so only modified state fields are written back to the device."""
 
+    # views keep a reference to the root array (never to themselves: a self-cycle would
+    # leave the array to the cyclic GC and delay recycling its pinned buffer)
     def __array_finalize__(self, obj):
-        root = getattr(obj, "_root", None)
-        self._root = root if root is not None else self
+        if isinstance(obj, _Tracked):
+            self._root = obj._root if obj._root is not None else obj
+        else:
+            self._root = None
         self._dirty = False
 
+    def _mark(self):
+        (self._root if self._root is not None else self)._dirty = True
+
     def __setitem__(self, key, value):
-        self._root._dirty = True
+        self._mark()
         super().__setitem__(key, value)
 
     def __array_ufunc__(self, ufunc, method, *inputs, out=None, **kw):
@@ -55,7 +62,7 @@ class _Tracked(np.ndarray):
         if out is not None:
             for o in out:
                 if isinstance(o, _Tracked):
-                    o._root._dirty = True
+                    o._mark()
             kw["out"] = tuple(np.asarray(o) if isinstance(o, _Tracked) else o for o in out)
         return getattr(ufunc, method)(*plain, **kw)
 
@@ -150,6 +157,7 @@ class Simulation:
         self._host_state = None
         self._host_obstacles = None
         self._obs_dirty = False
+        self._pin_pool = {}
         self._step_index = 0
 
     def __del__(self):
@@ -189,9 +197,24 @@ class Simulation:
                 if st.dirty(name):
                     st._cache[name]._dirty = False
 
+    def _pinned(self, rows: int) -> np.ndarray:
+        """A (rows, 3) fp64 array in page-locked memory from a recycling pool: the device
+        copies into it at full DMA rate (no staging memcpy), and the buffer returns to
+        the pool once the last view of the array is garbage collected."""
+        import weakref
+
+        import torch
+
+        pool = self._pin_pool.setdefault(rows, [])
+        buf = pool.pop() if pool else torch.empty((rows, 3), dtype=torch.float64, pin_memory=True)
+        arr = buf.numpy()
+        weakref.finalize(arr, pool.append, buf)
+        return arr
+
     def _download(self, name: str) -> np.ndarray:
         """One state field (n, 3) from the device (cs_get_state with only that pointer)."""
-        out = np.empty((self.mesh.vertex_count, 3)) if name != "obstacle_x" else np.empty((self._n_obs, 3))
+        rows = self.mesh.vertex_count if name != "obstacle_x" else self._n_obs
+        out = self._pinned(rows) if rows else np.empty((0, 3))
         ptrs = [None] * 5
         ptrs[(*DeviceSimState.FIELDS, "obstacle_x").index(name)] = out.ctypes.data if out.size else None
         idx = ctypes.c_int(0)
