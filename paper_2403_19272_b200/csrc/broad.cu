@@ -217,11 +217,24 @@ __device__ __forceinline__ unsigned long long cell_code(long long ix, long long 
     return ((unsigned long long)ix & m) | (((unsigned long long)iy & m) << 21) | (((unsigned long long)iz & m) << 42);
 }
 
+// Bucket = low bits of the cell's Morton code: neighbouring cells get neighbouring
+// buckets, so bucket-ordered runs (and the pair rows they emit) walk space
+// coherently - every later per-pair gather by vertex id hits cache lines its
+// neighbours just touched.  Cells 2^(bits/3) apart share a bucket; the cell-code
+// comparison keeps the set exact.
+__device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
+    v &= 0x1fffff;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
 __device__ __forceinline__ unsigned bucket_of(unsigned long long code, unsigned mask) {
-    unsigned long long h = code * 0x9E3779B97F4A7C15ull;
-    h ^= h >> 29;
-    h *= 0xBF58476D1CE4E5B9ull;
-    h ^= h >> 32;
+    const unsigned long long m = (1ull << 21) - 1;
+    const unsigned long long h =
+        spread3(code & m) | (spread3((code >> 21) & m) << 1) | (spread3((code >> 42) & m) << 2);
     return (unsigned)h & mask;
 }
 
