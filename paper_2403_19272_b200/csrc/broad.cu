@@ -565,6 +565,34 @@ __global__ void k_run_iters(EntryTable R, EntryTable T, int vt, long long* __res
     }
 }
 
+// VT per-warp staging, structure of arrays; static flags ride in bit 3 of the
+// low-corner bytes
+struct VtStage {
+    double vlo[3][kRunCapV], vhi[3][kRunCapV];
+    unsigned long long vcode[kRunCapV];
+    int vprim[kRunCapV];
+    unsigned char vzs[kRunCapV];
+    double tlo[3][kRunCap], thi[3][kRunCap];
+    unsigned long long tcode[kRunCap];
+    int ta[kRunCap], tb[kRunCap], tc[kRunCap];
+    unsigned char tzs[kRunCap];
+};
+
+// k in [0, mv * mt) -> (i, j) = (k / mt, k % mt) via a float reciprocal (k < 2^12)
+__device__ __forceinline__ void vt_index(int k, int mt, float inv_mt, int& i, int& j) {
+    int q = (int)((float)k * inv_mt);
+    int r = k - q * mt;
+    if (r < 0) {
+        --q;
+        r += mt;
+    } else if (r >= mt) {
+        ++q;
+        r -= mt;
+    }
+    i = q;
+    j = r;
+}
+
 // VT: one warp per vertex-table bucket run x the same bucket's triangle entries.
 template <int PASS>
 __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, EntryTable T,
@@ -574,8 +602,9 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
                                                               const double* __restrict__ inv_cell, WorldTopo W,
                                                               const long long* __restrict__ iter_off,
                                                               unsigned* __restrict__ masks, PairOut O) {
-    __shared__ SmEntry smv[kPairWarps][kRunCapV], smt[kPairWarps][kRunCap];
+    __shared__ VtStage smvt[PASS == 0 ? kPairWarps : 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    VtStage& S = smvt[PASS == 0 ? w : 0];
     const int nr = V.n_run[0];
     const double inv = inv_cell[0];
     for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nr; r += (gridDim.x * blockDim.x) >> 5) {
@@ -588,46 +617,52 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
         if (mt > 0 && mv <= kRunCapV && mt <= kRunCap) {
             if (PASS == 0) {
                 for (int k = lane; k < mv; k += 32) {
-                    SmEntry& e = smv[w][k];
                     const int v = V.prim[vb + k];
-                    e.prim = v;
-                    e.code = V.code[vb + k];
-                    e.z = V.zb[vb + k];
-                    e.stat = W.vert_static[v];
+                    S.vprim[k] = v;
+                    S.vcode[k] = V.code[vb + k];
+                    S.vzs[k] = (unsigned char)(V.zb[vb + k] | (W.vert_static[v] ? 8 : 0));
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        e.lo[c] = vlo[3 * (int64_t)v + c];
-                        e.hi[c] = vhi[3 * (int64_t)v + c];
+                        S.vlo[c][k] = vlo[3 * (int64_t)v + c];
+                        S.vhi[c][k] = vhi[3 * (int64_t)v + c];
                     }
                 }
                 for (int k = lane; k < mt; k += 32) {
-                    SmEntry& e = smt[w][k];
                     const int f = T.prim[tb + k];
-                    e.prim = f;
-                    e.code = T.code[tb + k];
-                    e.z = T.zb[tb + k];
-                    e.a = W.tris[3 * f];
-                    e.b = W.tris[3 * f + 1];
-                    e.c = W.tris[3 * f + 2];
-                    e.stat = W.tri_static[f];
-                    load_box(tbox, f, e.lo, e.hi);
+                    S.tcode[k] = T.code[tb + k];
+                    S.tzs[k] = (unsigned char)(T.zb[tb + k] | (W.tri_static[f] ? 8 : 0));
+                    S.ta[k] = W.tris[3 * f];
+                    S.tb[k] = W.tris[3 * f + 1];
+                    S.tc[k] = W.tris[3 * f + 2];
+                    double lo[3], hi[3];
+                    load_box(tbox, f, lo, hi);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        S.tlo[c][k] = lo[c];
+                        S.thi[c][k] = hi[c];
+                    }
                 }
                 __syncwarp();
             }
             const int np = mv * mt;
+            const float inv_mt = 1.0f / (float)mt;
             for (int k0 = 0; k0 < np; k0 += 32, ++it) {
                 const int k = k0 + lane;
                 bool hit = false;
                 if (PASS == 0 && k < np) {
-                    const int i = k / mt, j = k - i * mt;
-                    const SmEntry& x = smv[w][i];
-                    const SmEntry& y = smt[w][j];
-                    hit = (x.z | y.z) == 7 && x.code == y.code && !(x.stat && y.stat) && x.prim != y.a &&
-                          x.prim != y.b && x.prim != y.c && sm_overlap(x, y);
+                    int i, j;
+                    vt_index(k, mt, inv_mt, i, j);
+                    const int zi = S.vzs[i], zj = S.tzs[j];
+                    const int v = S.vprim[i];
+                    hit = ((zi | zj) & 7) == 7 && !(zi & zj & 8) && S.vcode[i] == S.tcode[j] && v != S.ta[j] &&
+                          v != S.tb[j] && v != S.tc[j] && S.vlo[0][i] <= S.thi[0][j] && S.tlo[0][j] <= S.vhi[0][i] &&
+                          S.vlo[1][i] <= S.thi[1][j] && S.tlo[1][j] <= S.vhi[1][i] && S.vlo[2][i] <= S.thi[2][j] &&
+                          S.tlo[2][j] <= S.vhi[2][i];
                 }
                 const unsigned m = warp_hits<PASS>(hit, masks, it);
                 if (PASS == 1 && ((m >> lane) & 1u)) {
-                    const int i = k / mt, j = k - i * mt;
+                    int i, j;
+                    vt_index(k, mt, inv_mt, i, j);
                     write_vt(O, base + lane_rank(m), V.prim[vb + i], T.prim[tb + j], W);
                 }
                 base += __popc(m);
