@@ -105,6 +105,7 @@ typedef struct {
     int reduced_fallbacks;
     long long gpu_launches;
     int static_sites;           /* motion-free CCD sites served from the previous site's pairs */
+    int subset_sites;           /* moving CCD sites served from the step's base site (+ violator queries) */
 } cs_step_report;
 
 /* ---- scene lifetime ---------------------------------------------------- */

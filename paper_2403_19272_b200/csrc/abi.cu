@@ -214,6 +214,13 @@ struct cs_scene {
     DBuf<int> fallback;
     DBuf<int> wl_full, wl_dist;
     DBuf<uint8_t> keep_flag;
+    // subset sites: a moving site served from the step's base site (subset_site)
+    PairBuf basepr;
+    DBuf<double> blo, bhi;
+    DBuf<uint8_t> vviol, tviol, eviol;
+    DBuf<int> vlist, tlist, elist, qcount, qoff;
+    bool base_valid = false;
+    double base_margin = -1.0;
     DBuf<char> cub_tmp;
     DBuf<double> d_scal;
     DBuf<int> d_iscal;
@@ -490,6 +497,7 @@ struct cs_scene {
 
     // broad phase into pr (bvh.py:207-292): entry tables -> bucket-pair count -> scan -> write; two host syncs
     int broad_phase(const double* xa, const double* xb, double margin, PairBuf& pr) {
+        base_valid = false;  // the grid tables are rebuilt below
         k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(xa, xb, nw, margin, vlo.p, vhi.p, fvbox.p);
         k_vertex_disp<<<grid(nw), 256, 0, s>>>(xa, xb, nw, vdisp.p, fvbox.p);
         bmargin = margin;
@@ -526,9 +534,11 @@ struct cs_scene {
         ttab.T = vtab.T;
         ttab.log2T = vtab.log2T;
         etab.set_buckets(etab.m);
-        CS_RET(table_build(vtab, vs, ttab.inv.p, false));
+        // dense bucket ranges: the triangle table for k_pairs_vt, all three for
+        // k_subset_query's cell walks
+        CS_RET(table_build(vtab, vs, ttab.inv.p, true));
         CS_RET(table_build(ttab, ts, ttab.inv.p, true));
-        CS_RET(table_build(etab, es, etab.inv.p, false));
+        CS_RET(table_build(etab, es, etab.inv.p, true));
         // ballot buffers: warp iterations per run, scanned (one more host sync)
         const EntryTable VT = vtab.view(), TT = ttab.view(), ET = etab.view();
         for (EntryBuf* G : {&vtab, &etab}) {
@@ -676,11 +686,153 @@ struct cs_scene {
         return 0;
     }
 
+    // Base site: the step's first moving site runs the full broad phase with its
+    // margin widened by a small slack into basepr and keeps its vertex boxes; the
+    // grid tables stay valid until the next full broad phase.
+    int build_base(const double* xa, const double* xb, double margin) {
+        static const double slack = std::getenv("CS_SITE_SLACK") ? std::atof(std::getenv("CS_SITE_SLACK")) : 0.01;
+        CS_RET(broad_phase(xa, xb, margin + slack * margin, basepr));
+        CS_RET(blo.ensure(3LL * nw));
+        CS_RET(bhi.ensure(3LL * nw));
+        CS_TRY(cudaMemcpyAsync(blo.p, vlo.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
+        CS_TRY(cudaMemcpyAsync(bhi.p, vhi.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
+        base_valid = true;
+        base_margin = margin;
+        return 0;
+    }
+
+    // Subset site: a moving site whose candidate set is taken from the base site.
+    // Pairs are "boxes overlap" (bvh.py:207-292), and every box is the union of its
+    // vertices' boxes, so for primitives whose vertex boxes all lie inside their base
+    // boxes ("non-violators") the pairs are the base pairs that still overlap.  Pairs
+    // with a violator (a vertex box poking out, or left out of the base grid) are
+    // found by k_subset_query: base-grid cell walks for non-violating partners, brute
+    // force among violators.  Exactly the full broad phase's set
+    // (CS_VERIFY_STATIC_SITE checks it); ok = false when violators are too many.
+    int subset_site(const double* xa, const double* xb, double margin, PairBuf& pr, bool& ok) {
+        ok = false;
+        if (!base_valid || margin != base_margin) return 0;
+        // boxes and filter records of this site
+        k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(xa, xb, nw, margin, vlo.p, vhi.p, fvbox.p);
+        k_vertex_disp<<<grid(nw), 256, 0, s>>>(xa, xb, nw, vdisp.p, fvbox.p);
+        const int gt = grid(ntw), ge = grid(new_);
+        k_prim_boxes<3><<<gt, 256, 0, s>>>(wtris.p, ntw, tri_static.p, vlo.p, vhi.p, vdisp.p, ttab.box.p, tdisp.p,
+                                           ttab.part.p, ftbox.p);
+        k_prim_boxes<2><<<ge, 256, 0, s>>>(wedges.p, new_, edge_static.p, vlo.p, vhi.p, vdisp.p, etab.box.p, edisp.p,
+                                           etab.part.p, febox.p);
+        k_prim_motion<3><<<gt, 256, 0, s>>>(wtris.p, ntw, xa, xb, ftbox.p);
+        k_prim_motion<2><<<ge, 256, 0, s>>>(wedges.p, new_, xa, xb, febox.p);
+        bmargin = margin;
+        // violators
+        CS_RET(vviol.ensure(nw));
+        CS_RET(tviol.ensure(std::max(ntw, 1)));
+        CS_RET(eviol.ensure(std::max(new_, 1)));
+        CS_RET(vlist.ensure(nw));
+        CS_RET(tlist.ensure(std::max(ntw, 1)));
+        CS_RET(elist.ensure(std::max(new_, 1)));
+        k_viol_vertices<<<grid(nw), 256, 0, s>>>(vlo.p, vhi.p, blo.p, bhi.p, nw, vert_used.p, vtab.is_over.p,
+                                                vviol.p);
+        k_viol_prims<3><<<gt, 256, 0, s>>>(wtris.p, ntw, vviol.p, ttab.is_over.p, tviol.p);
+        k_viol_prims<2><<<ge, 256, 0, s>>>(wedges.p, new_, vviol.p, etab.is_over.p, eviol.p);
+        launches += 9;
+        cub::CountingInputIterator<int> it(0);
+        size_t bytes = 0;
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, vviol.p, vlist.p, d_iscal.p + I_COUNT, nw, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, vviol.p, vlist.p, d_iscal.p + I_COUNT, nw, s));
+        bytes = 0;
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, tviol.p, tlist.p, d_iscal.p + I_COUNT + 1, ntw, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, tviol.p, tlist.p, d_iscal.p + I_COUNT + 1, ntw, s));
+        bytes = 0;
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, eviol.p, elist.p, d_iscal.p + I_COUNT + 2, new_, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, eviol.p, elist.p, d_iscal.p + I_COUNT + 2, new_, s));
+        // surviving base pairs among non-violators
+        const long long P0 = basepr.P;
+        CS_RET(keep_flag.ensure(std::max<long long>(P0, 1)));
+        CS_RET(sel.ensure(std::max<long long>(P0, 1)));
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_COUNT + 3, 0, sizeof(int), s));
+        if (P0) {
+            k_pair_keep<<<grid(P0), 256, 0, s>>>(basepr.keys.p, P0, vlo.p, vhi.p, ttab.box.p, etab.box.p,
+                                                 keep_flag.p, vviol.p, tviol.p, eviol.p);
+            ++launches;
+            bytes = 0;
+            cub::DeviceSelect::Flagged(nullptr, bytes, it, keep_flag.p, sel.p, d_iscal.p + I_COUNT + 3, (int)P0, s);
+            CS_RET(cub_tmp.ensure(bytes));
+            CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, keep_flag.p, sel.p, d_iscal.p + I_COUNT + 3,
+                                              (int)P0, s));
+        }
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], d_iscal.p + I_COUNT, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        const int nv = h_iscal[I_COUNT], nt = h_iscal[I_COUNT + 1], ne = h_iscal[I_COUNT + 2];
+        const long long Pa = h_iscal[I_COUNT + 3];
+        const long long nq = (long long)nv + nt + ne;
+        // violator x violator work is quadratic: past this the full broad phase is cheaper
+        if ((double)nv * nt + 0.5 * (double)ne * ne > 2e8) return 0;
+        // violator partners: count, scan, write
+        CS_RET(qcount.ensure(nq + 1));
+        CS_RET(qoff.ensure(nq + 1));
+        CS_TRY(cudaMemsetAsync(qcount.p, 0, sizeof(int) * (nq + 1), s));
+        const QueryArgs A{vlist.p, tlist.p, elist.p, nv, nt, ne, vviol.p, tviol.p, eviol.p, vlo.p, vhi.p,
+                          ttab.box.p, etab.box.p, vtab.view(), ttab.view(), etab.view(), ttab.inv.p, etab.inv.p,
+                          (unsigned)(vtab.T - 1), (unsigned)(etab.T - 1), ntw, new_, nullptr};
+        static const bool trace_sites = std::getenv("CS_TRACE_SITES") != nullptr;
+        static DBuf<unsigned long long> dbg;
+        QueryArgs Aq = A;
+        if (trace_sites) {
+            CS_RET(dbg.ensure(4));
+            CS_TRY(cudaMemsetAsync(dbg.p, 0, 4 * sizeof(unsigned long long), s));
+            Aq.big = dbg.p;
+        }
+        const WorldTopo W = world();
+        const int gq = (int)std::max<long long>(1, (32 * nq + 127) / 128);
+        if (nq) {
+            k_subset_query<0><<<gq, 128, 0, s>>>(Aq, W, qcount.p, nullptr, PairOut{});
+            ++launches;
+        }
+        CS_RET(scan(qcount.p, qoff.p, (int)nq + 1));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], qoff.p + nq, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], qoff.p + nv + nt, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaStreamSynchronize(s));
+        const long long Q = h_iscal[I_COUNT], Qvt = h_iscal[I_COUNT + 1];
+        if (trace_sites) {
+            unsigned long long bg[4];
+            CS_TRY(cudaMemcpy(bg, dbg.p, sizeof(bg), cudaMemcpyDeviceToHost));
+            std::fprintf(stderr,
+                         "[cs subset] base pairs %lld kept %lld violators v %d t %d e %d query pairs %lld "
+                         "big v %llu t %llu e %llu max cells %llu\n",
+                         P0, Pa, nv, nt, ne, Q, bg[0], bg[1], bg[2], bg[3]);
+        }
+        CS_RET(pr.reserve(std::max<long long>(Pa + Q, 1)));
+        if (Pa) {
+            k_gather_pairs<<<std::max(1, std::min(grid(Pa), 16 * sm_count)), 256, 0, s>>>(
+                sel.p, d_iscal.p + I_COUNT + 3, basepr.kind.p, basepr.idx.p, basepr.keys.p, pr.kind.p, pr.idx.p,
+                pr.keys.p);
+            ++launches;
+        }
+        if (Q) {
+            k_subset_query<1><<<gq, 128, 0, s>>>(A, W, nullptr, qoff.p,
+                                                PairOut{nullptr, nullptr, pr.kind.p + Pa, pr.idx.p + Pa,
+                                                        pr.keys.p + Pa});
+            ++launches;
+            if (Q > Qvt) {
+                k_ee_orient<<<grid(Q - Qvt), 256, 0, s>>>(pr.keys.p + Pa + Qvt, pr.idx.p + Pa + Qvt, Q - Qvt, W);
+                ++launches;
+            }
+        }
+        CS_CHECK_LAUNCH();
+        pr.P = Pa + Q;
+        ok = true;
+        return 0;
+    }
+
     // test hook (CS_VERIFY_STATIC_SITE): the subset path must give exactly the full
     // broad phase's key set; returns CS_INTERNAL on any difference
-    int verify_static_site(const double* x, PairBuf& got) {
+    int verify_static_site(const double* x, PairBuf& got) { return verify_site(x, x, got); }
+    int verify_site(const double* xa, const double* xb, PairBuf& got) {
         PairBuf full;
-        CS_RET(broad_phase(x, x, cfg.d_hat, full));
+        CS_RET(broad_phase(xa, xb, cfg.d_hat, full));
         int rc = 0;
         if (full.P != got.P) {
             rc = CS_INTERNAL;
@@ -722,6 +874,7 @@ struct cs_scene {
         k_cell_size<<<1, 256, 0, s>>>(ttab.part.p, gt, ttab.inv.p);
         launches += 3;
         bmargin = -1.0;  // the site boxes are gone: no motion-free site may reuse them
+        base_valid = false;
         const BoxSrc ts{ttab.box.p, nullptr, nullptr, nullptr, ntw};
         CS_RET(table_count(ttab, ts, ttab.inv.p));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], ttab.offset.p + ttab.np, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -748,13 +901,29 @@ struct cs_scene {
         return 0;
     }
 
+    // base: 0 full broad phase; 1 subset of the current base site if possible;
+    // 2 this site becomes the base (first moving site of a step)
     int ccd_site(const double* xa, const double* xb, PairBuf& pr, cs_step_report* rep, double& clamp,
-                 PairBuf* prev_site = nullptr) {
+                 PairBuf* prev_site = nullptr, int base = 0) {
         stage(T_BROAD);
         bool done = false;
-        if (prev_site != nullptr && xa == xb) CS_RET(broad_phase_static(xa, cfg.d_hat, *prev_site, pr, done));
-        if (done && std::getenv("CS_VERIFY_STATIC_SITE")) CS_RET(verify_static_site(xa, pr));
-        if (done && rep) rep->static_sites += 1;
+        const bool no_subset = std::getenv("CS_NO_SUBSET_SITES") != nullptr;
+        const bool verify = std::getenv("CS_VERIFY_STATIC_SITE") != nullptr;
+        if (prev_site != nullptr && xa == xb) {
+            CS_RET(broad_phase_static(xa, cfg.d_hat, *prev_site, pr, done));
+            if (done && verify) CS_RET(verify_static_site(xa, pr));
+            if (done && rep) rep->static_sites += 1;
+        } else if (base != 0 && !no_subset) {
+            if (base == 1) {
+                CS_RET(subset_site(xa, xb, cfg.d_hat, pr, done));
+                if (done && rep) rep->subset_sites += 1;
+                if (done && verify) CS_RET(verify_site(xa, xb, pr));
+            }
+            if (!done) {
+                CS_RET(build_base(xa, xb, cfg.d_hat));
+                CS_RET(subset_site(xa, xb, cfg.d_hat, pr, done));
+            }
+        }
         if (!done) CS_RET(broad_phase(xa, xb, cfg.d_hat, pr));
         stage(T_FULL);
         const long long P = pr.P;
@@ -1072,7 +1241,7 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(beta_red.ensure(1));
     CS_RET(fallback.ensure(1));
     CS_RET(d_scal.ensure(S_COUNT));
-    CS_RET(d_iscal.ensure(I_COUNT));
+    CS_RET(d_iscal.ensure(I_COUNT + 8));  // [I_COUNT, +8): subset-site counters
     CS_TRY(cudaMemset(d_scal.p, 0, sizeof(double) * S_COUNT));
     CS_TRY(cudaMemset(d_iscal.p, 0, sizeof(int) * I_COUNT));
     CS_TRY(cudaMallocHost(&h_scal, sizeof(double) * (S_COUNT + 4)));  // [S_COUNT, +4): broad-phase scratch
@@ -1111,6 +1280,13 @@ void cs_scene::release() {
     edge_static.release();
     eflip.release();
     keep_flag.release();
+    basepr.release();
+    blo.release();
+    bhi.release();
+    vviol.release();
+    tviol.release();
+    eviol.release();
+    for (DBuf<int>* b : {&vlist, &tlist, &elist, &qcount, &qoff}) b->release();
     isect_out.release();
     fvbox.release();
     ftbox.release();
@@ -1183,7 +1359,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         CS_TRY(cudaMemcpyAsync(xc_w.p + 3LL * n, obs_next, sizeof(double) * 3 * nobs, cudaMemcpyDeviceToDevice, s));
     }
     double tc = 1.0;
-    CS_RET(ccd_site(xs_w.p, xc_w.p, *cur, rep, tc));
+    CS_RET(ccd_site(xs_w.p, xc_w.p, *cur, rep, tc, nullptr, 2));
     // x_acc = clamp; anchor = x_acc (stepper.py:475-480)
     CS_RET(set_clamp_value(tc));
     CS_RET(lerp_world(xs_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));
@@ -1272,7 +1448,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         ++outer_loops;
         // fresh pair set + line-search filter at the end of every outer loop (stepper.py:547-570)
         double tout = 1.0;
-        CS_RET(ccd_site(anchor_w.p, xc_w.p, *nxt, rep, tout));
+        CS_RET(ccd_site(anchor_w.p, xc_w.p, *nxt, rep, tout, nullptr, 1));
         if (tout < 1.0) {
             CS_RET(set_clamp_value(tout));
             CS_RET(lerp_world(anchor_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));

@@ -357,7 +357,7 @@ struct EntryTable {
     const uint8_t* __restrict__ zb;             // low-corner bits
     const int* __restrict__ run;                // run heads (first entry of each bucket)
     const int* __restrict__ n_run;              // device scalar
-    const int* __restrict__ bstart;             // dense bucket ranges (triangle table only)
+    const int* __restrict__ bstart;             // dense bucket ranges
     const int* __restrict__ bend;
     int m;                                      // entries
 };
@@ -906,13 +906,196 @@ __global__ void k_box_contained(const double* __restrict__ x, int n3, double mar
     if (!(lo >= vlo[i] && hi <= vhi[i])) atomicOr(flag, 1);
 }
 
+// Violators of a base site (subset sites, see abi.cu subset_site): used vertices
+// whose box at this site is not inside their base box, or that the base grid left
+// out (oversize); primitives with a violating vertex or left out themselves.
+__global__ void k_viol_vertices(const double* __restrict__ vlo, const double* __restrict__ vhi,
+                                const double* __restrict__ blo, const double* __restrict__ bhi, int nw,
+                                const uint8_t* __restrict__ used, const uint8_t* __restrict__ over,
+                                uint8_t* __restrict__ viol) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nw) return;
+    bool out = over[v] != 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int64_t i = 3 * (int64_t)v + c;
+        out |= !(vlo[i] >= blo[i] && vhi[i] <= bhi[i]);
+    }
+    viol[v] = used[v] && out ? 1 : 0;
+}
+
+template <int ARITY>
+__global__ void k_viol_prims(const int* __restrict__ verts, int np, const uint8_t* __restrict__ vviol,
+                             const uint8_t* __restrict__ over, uint8_t* __restrict__ viol) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    bool out = over[p] != 0;
+#pragma unroll
+    for (int k = 0; k < ARITY; ++k) out |= vviol[verts[ARITY * p + k]] != 0;
+    viol[p] = out ? 1 : 0;
+}
+
+// Pairs of a subset site with at least one violator.  Thread t takes violator
+// list entry t of [vertices | triangles | edges] and finds its partners at this
+// site's boxes:
+//  * non-violators through the base grid: the cells covering its box, entries with
+//    that cell code, exact box overlap, reported in the cell holding the overlap's
+//    min corner (a non-violator's box lies inside its base box, so it is entered in
+//    that cell) - once;
+//  * violators by brute force over the violator lists (vertex x triangle from the
+//    vertex side, edge x edge from the lower list position).
+// A violator box spanning more cells than the grid enters for one primitive scans
+// every non-violator instead.  PASS 0 counts, PASS 1 writes at the scanned offset (deterministic).
+constexpr long long kQueryCells = kMaxCellsPerPrim;
+
+struct QueryArgs {
+    const int* __restrict__ vlist;
+    const int* __restrict__ tlist;
+    const int* __restrict__ elist;
+    int nv, nt, ne;
+    const uint8_t* __restrict__ vviol;
+    const uint8_t* __restrict__ tviol;
+    const uint8_t* __restrict__ eviol;
+    const double* __restrict__ vlo;
+    const double* __restrict__ vhi;
+    const double* __restrict__ tbox;
+    const double* __restrict__ ebox;
+    EntryTable V, T, E;  // base grid (V/T share cells and buckets)
+    const double* __restrict__ inv_vt;
+    const double* __restrict__ inv_ee;
+    unsigned mask_vt, mask_ee;
+    int ntris, nedges;
+    unsigned long long* big;  // diagnostics (nullable): [class] big-box violators, [3] max cells
+};
+
+__device__ __forceinline__ void vbox(const QueryArgs& A, int v, double lo[3], double hi[3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        lo[c] = A.vlo[3 * (int64_t)v + c];
+        hi[c] = A.vhi[3 * (int64_t)v + c];
+    }
+}
+
+// one warp per violator; hits are ballot-ordered, so both passes emit in the same order
+template <int PASS>
+__global__ void __launch_bounds__(128) k_subset_query(QueryArgs A, WorldTopo W, int* __restrict__ counts,
+                                                      const int* __restrict__ offsets, PairOut O) {
+    const int lane = threadIdx.x & 31;
+    const int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int ntot = A.nv + A.nt + A.ne;
+    if (t >= ntot) return;
+    const int cls = t < A.nv ? 0 : (t < A.nv + A.nt ? 1 : 2);  // 0 vertex, 1 triangle, 2 edge
+    const int li = cls == 0 ? t : (cls == 1 ? t - A.nv : t - A.nv - A.nt);
+    const int p = cls == 0 ? A.vlist[li] : (cls == 1 ? A.tlist[li] : A.elist[li]);
+    int row = PASS == 1 ? offsets[t] : 0, cnt = 0;
+    // one warp step: lanes with hit emit (a, b) in lane order
+    auto step = [&](bool hit, int a, int b) {
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (PASS == 1 && hit) {
+            if (cls == 2) write_ee(O, row + lane_rank(m), a, b, W);
+            else write_vt(O, row + lane_rank(m), a, b, W);
+        }
+        row += __popc(m);
+        cnt += __popc(m);
+    };
+    auto partner_ok = [&](int q) {
+        return cls == 0 ? vt_ok(W, p, q) : (cls == 1 ? vt_ok(W, q, p) : ee_ok(W, p, q));
+    };
+    double lo[3], hi[3];
+    if (cls == 0) vbox(A, p, lo, hi);
+    else load_box(cls == 1 ? A.tbox : A.ebox, p, lo, hi);
+    const double inv = cls == 2 ? A.inv_ee[0] : A.inv_vt[0];
+    const CellRange r = cell_range(lo, hi, inv);
+    const long long nc = r.count();
+    const EntryTable& G = cls == 0 ? A.T : (cls == 1 ? A.V : A.E);
+    const uint8_t* __restrict__ qviol = cls == 0 ? A.tviol : (cls == 1 ? A.vviol : A.eviol);
+    const unsigned mask = cls == 2 ? A.mask_ee : A.mask_vt;
+    if (PASS == 0 && A.big != nullptr && lane == 0) {
+        if (!(nc > 0 && nc <= kQueryCells)) atomicAdd(&A.big[cls], 1ull);
+        atomicMax(&A.big[3], (unsigned long long)nc);
+    }
+    if (nc > 0 && nc <= kQueryCells) {
+        // lanes take cells; each walks its cell's bucket run, one entry per warp step
+        const int sx = (int)(r.hi[0] - r.lo[0] + 1), sxy = sx * (int)(r.hi[1] - r.lo[1] + 1);
+        for (int c0 = 0; c0 < (int)nc; c0 += 32) {
+            const int c = c0 + lane;
+            int beg = 0, end = 0;
+            unsigned long long code = 0;
+            if (c < (int)nc) {
+                const int kz = c / sxy, rem = c - kz * sxy, ky = rem / sx, kx = rem - ky * sx;
+                code = cell_code(r.lo[0] + kx, r.lo[1] + ky, r.lo[2] + kz);
+                const unsigned b = bucket_of(code, mask);
+                beg = G.bstart[b];
+                end = G.bend[b];
+            }
+            const int len = __reduce_max_sync(0xffffffffu, end - beg);
+            for (int k = 0; k < len; ++k) {
+                const int j = beg + k;
+                bool hit = false;
+                int q = -1;
+                if (j < end && G.code[j] == code) {
+                    q = G.prim[j];
+                    if (!qviol[q]) {
+                        double qlo[3], qhi[3];
+                        if (cls == 1) vbox(A, q, qlo, qhi);
+                        else load_box(cls == 0 ? A.tbox : A.ebox, q, qlo, qhi);
+                        hit = overlap6(lo, hi, qlo, qhi) && min_corner_in(lo, qlo, inv, code) && partner_ok(q);
+                    }
+                }
+                if (cls == 1) step(hit, q, p);
+                else step(hit, p, q);
+            }
+        }
+    } else {
+        // box too large for a cell walk: every non-violating partner
+        const int nq = cls == 0 ? A.ntris : (cls == 1 ? W.nw : A.nedges);
+        for (int q0 = 0; q0 < nq; q0 += 32) {
+            const int q = q0 + lane;
+            bool hit = false;
+            if (q < nq && !qviol[q] && (cls != 1 || W.vert_used[q])) {
+                double qlo[3], qhi[3];
+                if (cls == 1) vbox(A, q, qlo, qhi);
+                else load_box(cls == 0 ? A.tbox : A.ebox, q, qlo, qhi);
+                hit = overlap6(lo, hi, qlo, qhi) && partner_ok(q);
+            }
+            if (cls == 1) step(hit, q, p);
+            else step(hit, p, q);
+        }
+    }
+    // violator x violator: vertex side against violating triangles, edges against later ones
+    if (cls != 1) {
+        const int* __restrict__ L = cls == 0 ? A.tlist : A.elist;
+        const int n = cls == 0 ? A.nt : A.ne;
+        for (int k0 = cls == 0 ? 0 : li + 1; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
+            bool hit = false;
+            int f = -1;
+            if (k < n) {
+                f = L[k];
+                double qlo[3], qhi[3];
+                load_box(cls == 0 ? A.tbox : A.ebox, f, qlo, qhi);
+                hit = overlap6(lo, hi, qlo, qhi) && partner_ok(f);
+            }
+            step(hit, p, f);
+        }
+    }
+    if (PASS == 0 && lane == 0) counts[t] = cnt;
+}
+
 __global__ void k_pair_keep(const unsigned long long* __restrict__ keys, int64_t P, const double* __restrict__ vlo,
                             const double* __restrict__ vhi, const double* __restrict__ tbox,
-                            const double* __restrict__ ebox, uint8_t* __restrict__ keep) {
+                            const double* __restrict__ ebox, uint8_t* __restrict__ keep,
+                            const uint8_t* __restrict__ vviol = nullptr, const uint8_t* __restrict__ tviol = nullptr,
+                            const uint8_t* __restrict__ eviol = nullptr) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= P) return;
     const unsigned long long k = keys[i];
     const int p = (int)((k >> 32) & 0x7fffffffu), q = (int)(k & 0xffffffffu);
+    if (vviol != nullptr &&
+        ((k >> 63) ? (eviol[p] | eviol[q]) != 0 : (vviol[p] | tviol[q]) != 0)) {
+        keep[i] = 0;  // re-found by k_subset_query
+        return;
+    }
     double alo[3], ahi[3], blo[3], bhi[3];
     if (k >> 63) {
         load_box(ebox, p, alo, ahi);
