@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -226,6 +227,7 @@ struct cs_scene {
     DBuf<int> d_iscal;
     double* h_scal = nullptr;
     int* h_iscal = nullptr;
+    double* h_stage = nullptr;  // pinned: [pins (3 npin) | obstacles (3 nobs)]
     cudaStream_t s = 0;
     long long launches = 0;
     // timing
@@ -1224,6 +1226,9 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(delta.ensure(nf));
     CS_RET(pins_next_d.ensure(std::max(3 * npin, 1)));
     CS_RET(obs_next_d.ensure(std::max(3 * nobs, 1)));
+    // page-locked staging for the per-step pin / obstacle targets (a pageable
+    // cudaMemcpyAsync stages through the driver and can stall the stream)
+    CS_TRY(cudaMallocHost(&h_stage, sizeof(double) * (3 * npin + 3 * nobs + 1)));
     CS_RET(vlo.ensure(3LL * nw));
     CS_RET(vhi.ensure(3LL * nw));
     CS_RET(vdisp.ensure(nw, true));
@@ -1261,6 +1266,8 @@ void cs_scene::release() {
     ev_pool.clear();
     if (h_scal) cudaFreeHost(h_scal);
     if (h_iscal) cudaFreeHost(h_iscal);
+    if (h_stage) cudaFreeHost(h_stage);
+    h_stage = nullptr;
     h_scal = nullptr;
     h_iscal = nullptr;
     // DBuf members release through their owners
@@ -1310,17 +1317,21 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     active_stage = -1;
     const double h = cfg.h;
     // prescribed geometry at t + h (stepper.py:461-463): host callbacks evaluated by the caller
+    // (the previous step ended with a stream synchronisation, so h_stage is free)
     if (npin) {
-        if (pin_next_h)
-            CS_TRY(cudaMemcpyAsync(pins_next_d.p, pin_next_h, sizeof(double) * 3 * npin, cudaMemcpyHostToDevice, s));
-        else {
+        if (pin_next_h) {
+            std::memcpy(h_stage, pin_next_h, sizeof(double) * 3 * npin);
+            CS_TRY(cudaMemcpyAsync(pins_next_d.p, h_stage, sizeof(double) * 3 * npin, cudaMemcpyHostToDevice, s));
+        } else {
             k_gather_rows<<<grid(npin), 256, 0, s>>>(x.p, pin_ids.p, npin, pins_next_d.p);
             ++launches;
         }
     }
     const double* obs_next = obs.p;
     if (nobs && obs_next_h) {
-        CS_TRY(cudaMemcpyAsync(obs_next_d.p, obs_next_h, sizeof(double) * 3 * nobs, cudaMemcpyHostToDevice, s));
+        std::memcpy(h_stage + 3 * npin, obs_next_h, sizeof(double) * 3 * nobs);
+        CS_TRY(cudaMemcpyAsync(obs_next_d.p, h_stage + 3 * npin, sizeof(double) * 3 * nobs, cudaMemcpyHostToDevice,
+                               s));
         obs_next = obs_next_d.p;
     }
     stage(T_WARM);
@@ -1631,10 +1642,20 @@ int cs_scene_set_config(cs_scene* scene, const cs_step_config* cfg) {
 int cs_step(cs_scene* scene, const double* pin_next, const double* obstacle_next, cs_step_report* report,
             void* stream) {
     if (!scene) return CS_BAD_ARGUMENT;
+    static const bool trace_host = std::getenv("CS_TRACE_HOST") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     if (report) std::memset(report, 0, sizeof(*report));
     scene->s = (cudaStream_t)stream;
     int rc = scene->step(pin_next, obstacle_next, report);
     scene->stage(-1);
+    if (trace_host) {
+        const auto t1 = std::chrono::steady_clock::now();
+        static auto last = t1;
+        std::fprintf(stderr, "[cs host] step %.1f us, since previous exit %.1f us\n",
+                     std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                     std::chrono::duration<double, std::micro>(t0 - last).count());
+        last = t1;
+    }
     return rc;
 }
 
