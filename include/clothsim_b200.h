@@ -128,6 +128,12 @@ int cs_set_state(cs_scene *scene, const double *x, const double *x_dot, const do
                  const double *obstacle_x, int step_index, void *stream);
 /* device pointers of the resident state (n_cloth*3 doubles each) */
 int cs_state_device(cs_scene *scene, double **x, double **x_dot, double **delta_f, double **obstacle_x);
+/* Frame output (reference cli.py:64-98, frame_stride): snapshot x on `stream` and
+ * copy it to the PAGE-LOCKED host array host_x (n_cloth*3) on an internal copy
+ * stream; returns at once with a ticket (two slots, reused alternately).
+ * cs_frame_wait blocks until that frame has landed in host_x. */
+int cs_frame_async(cs_scene *scene, double *host_x, int *ticket, void *stream);
+int cs_frame_wait(cs_scene *scene, int ticket);
 
 /* ---- per-stage entry points (DEVICE pointers) ---------------------------- */
 /* full_ccd (collision/ccd.py:138-196): toi (P) nan = miss */

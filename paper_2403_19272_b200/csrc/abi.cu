@@ -310,6 +310,15 @@ struct cs_scene {
     };
     std::vector<SmoothGraph> smooth_graphs;
     cudaStream_t cap_stream = nullptr;
+    // asynchronous frame snapshots (cs_frame_async): two device slots, a copy stream
+    struct FrameSlot {
+        DBuf<double> x;
+        cudaEvent_t taken = nullptr, done = nullptr;
+        bool used = false;
+    };
+    FrameSlot frame_slots[2];
+    int frame_next = 0;
+    cudaStream_t copy_stream = nullptr;
 
     void smooth_launch(cudaStream_t st, const double* bb, double* xx, int steps, double c, const double* dl) {
         const int g2 = grid(nf, 128);
@@ -1262,6 +1271,15 @@ void cs_scene::release() {
     smooth_graphs.clear();
     if (cap_stream) cudaStreamDestroy(cap_stream);
     cap_stream = nullptr;
+    for (FrameSlot& f : frame_slots) {
+        if (f.used) cudaEventSynchronize(f.done);
+        if (f.taken) cudaEventDestroy(f.taken);
+        if (f.done) cudaEventDestroy(f.done);
+        f.taken = f.done = nullptr;
+        f.x.release();
+    }
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    copy_stream = nullptr;
     for (auto e : ev_pool) cudaEventDestroy(e);
     ev_pool.clear();
     if (h_scal) cudaFreeHost(h_scal);
@@ -1697,6 +1715,42 @@ int cs_state_device(cs_scene* sc, double** x, double** x_dot, double** delta_f, 
     if (x_dot) *x_dot = sc->v.p;
     if (delta_f) *delta_f = sc->df.p;
     if (obstacle_x) *obstacle_x = sc->obs.p;
+    return 0;
+}
+
+// Frame output without stalling the step loop (reference cli.py:64-98 writes a
+// frame every frame_stride steps): the positions are snapshotted on the caller's
+// stream into one of two device slots (an 8 MB D2D at config 4), and the slot is
+// copied to the caller's page-locked buffer on a separate copy stream while the
+// next steps run.  cs_frame_wait(ticket) blocks until that copy has landed.
+int cs_frame_async(cs_scene* sc, double* host_x, int* ticket, void* stream) {
+    if (!sc || !host_x || !ticket) return CS_BAD_ARGUMENT;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!sc->copy_stream) CS_TRY(cudaStreamCreateWithFlags(&sc->copy_stream, cudaStreamNonBlocking));
+    const int k = sc->frame_next;
+    cs_scene::FrameSlot& f = sc->frame_slots[k];
+    if (!f.taken) {
+        CS_TRY(cudaEventCreateWithFlags(&f.taken, cudaEventDisableTiming));
+        CS_TRY(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming));
+    }
+    const size_t nb = sizeof(double) * 3 * sc->n;
+    CS_RET(f.x.ensure(3LL * sc->n, true));
+    if (f.used) CS_TRY(cudaStreamWaitEvent(s, f.done, 0));  // the slot's previous copy has left it
+    CS_TRY(cudaMemcpyAsync(f.x.p, sc->x.p, nb, cudaMemcpyDeviceToDevice, s));
+    CS_TRY(cudaEventRecord(f.taken, s));
+    CS_TRY(cudaStreamWaitEvent(sc->copy_stream, f.taken, 0));
+    CS_TRY(cudaMemcpyAsync(host_x, f.x.p, nb, cudaMemcpyDeviceToHost, sc->copy_stream));
+    CS_TRY(cudaEventRecord(f.done, sc->copy_stream));
+    f.used = true;
+    sc->frame_next = k ^ 1;
+    *ticket = k;
+    return 0;
+}
+
+int cs_frame_wait(cs_scene* sc, int ticket) {
+    if (!sc || ticket < 0 || ticket > 1) return CS_BAD_ARGUMENT;
+    cs_scene::FrameSlot& f = sc->frame_slots[ticket];
+    if (f.used) CS_TRY(cudaEventSynchronize(f.done));
     return 0;
 }
 

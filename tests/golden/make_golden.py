@@ -190,6 +190,41 @@ def two_corner_fixture(steps=3):
     save("traj_two_corner64.npz", x=np.stack(xs), lg=np.array(lg))
 
 
+def io_fixture():
+    """Frame/metrics I/O (cli.py:64-98, config.py): the reference CLI's `simulate` on a
+    small hanging cloth - config text as written, OBJ frames, metrics CSV - plus
+    parse/serialize of a non-default config and save_obj of a fixed array."""
+    import tempfile
+    from pathlib import Path
+
+    from clothsim.cli import main
+    from clothsim.config import parse_config, serialize_config
+    from clothsim.mesh import save_obj
+
+    text = ('name = "io"\nsteps = 4\nseed = 3\n\n[scene]\nkind = "hanging"\nresolution = 10\nsize = 1.0\n\n'
+            '[solver]\nh = 0.005\ngravity = [0.0, -9.8, 0.0]\nsamples = 6\n\n[output]\nframe_stride = 2\n')
+    with tempfile.TemporaryDirectory() as d:
+        out = Path(d) / "out"
+        cfg_path = Path(d) / "io.toml"
+        cfg_path.write_text(text.replace("[output]\n", f'[output]\ndirectory = "{out}"\n'))
+        assert main(["simulate", str(cfg_path)]) == 0
+        frames = sorted(p.name for p in out.glob("frame_*.obj"))
+        objs = [(out / f).read_text() for f in frames]
+        metrics = (out / "metrics.csv").read_text()
+        written = (out / "config.toml").read_text()
+        obj_path = Path(d) / "fixed.obj"
+        rng = np.random.default_rng(5)
+        verts = rng.uniform(-2.0, 2.0, (17, 3))
+        verts[0] = [-0.0, 1e-12, 123.456789012345]
+        tris = rng.integers(0, 17, (9, 3))
+        save_obj(obj_path, verts, tris)
+        fixed_obj = obj_path.read_text()
+    roundtrip = serialize_config(parse_config(text))
+    save("io.npz", config_in=np.array(text), config_roundtrip=np.array(roundtrip), frames=np.array(frames),
+         objs=np.array(objs), metrics=np.array(metrics), config_written=np.array(written),
+         fixed_verts=verts, fixed_tris=tris, fixed_obj=np.array(fixed_obj))
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:          # regenerate selected fixtures only
         for name in sys.argv[1:]:
@@ -204,3 +239,4 @@ if __name__ == "__main__":
     two_corner_fixture()
     contact_state_fixture()
     dbb_fixture()
+    io_fixture()
