@@ -201,6 +201,10 @@ int cs_last_intersections(cs_scene *scene, long long *count, int *pairs, int cap
 
 const char *cs_version(void);
 
+/* Host helper for frame output: the OBJ vertex block "v %.9f %.9f %.9f\n" of n
+ * vertices (reference mesh.py:220-226) into out; returns bytes, -1 if cap is short. */
+long long cs_format_obj_vertices(const double *v, long long n, char *out, long long cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,7 +71,7 @@ EXPORTED = (
     "cs_state_device", "cs_full_ccd", "cs_distance_toi", "cs_partial_ccd", "cs_pair_witness", "cs_broad_phase",
     "cs_scene_pairs", "cs_ccd_site", "cs_scene_pair_results", "cs_assemble_rhs", "cs_ajacobi_smooth", "cs_reduced_correction", "cs_warmstart_correction",
     "cs_energy_gradient", "cs_collision_terms", "cs_residual", "cs_intersections", "cs_scene_set_verify", "cs_last_intersections", "cs_version",
-    "cs_frame_async", "cs_frame_wait",
+    "cs_frame_async", "cs_frame_wait", "cs_format_obj_vertices",
 )
 
 _lib = None
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH):
         "cs_state_device": (ctypes.c_int, [vp, vp, vp, vp, vp]),
         "cs_frame_async": (ctypes.c_int, [vp, vp, c_int_p, vp]),
         "cs_frame_wait": (ctypes.c_int, [vp, ctypes.c_int]),
+        "cs_format_obj_vertices": (ctypes.c_longlong, [vp, ll, vp, ll]),
         "cs_full_ccd": (ctypes.c_int, [vp, vp, vp, vp, ll, ctypes.c_double, vp, vp]),
         "cs_distance_toi": (ctypes.c_int, [vp, vp, vp, vp, ll, ctypes.c_double, ctypes.c_int, vp, vp]),
         "cs_partial_ccd": (ctypes.c_int, [vp, vp, vp, vp, ll, ctypes.c_int, vp, vp]),

@@ -51,9 +51,23 @@ class ObjFormatter:
         self.faces = "".join(f"f {a + 1} {b + 1} {c + 1}\n" for a, b, c in np.asarray(triangles).tolist())
 
     def write(self, path, vertices: np.ndarray) -> None:
+        v = np.ascontiguousarray(vertices, dtype=np.float64)
         with open(path, "w") as fh:
-            fh.write("".join(f"v {a:.9f} {b:.9f} {c:.9f}\n" for a, b, c in np.asarray(vertices).tolist()))
+            fh.write(self.vertex_text(v))
             fh.write(self.faces)
+
+    @staticmethod
+    def vertex_text(v: np.ndarray) -> str:
+        """The vertex block, formatted by the native library (multi-threaded)."""
+        lib = _lib.load()
+        if len(v) == 0:
+            return ""
+        cap = 160 * len(v)
+        buf = ctypes.create_string_buffer(cap)
+        k = lib.cs_format_obj_vertices(v.ctypes.data, len(v), buf, cap)
+        if k < 0:
+            raise RuntimeError("cs_format_obj_vertices: buffer too small")
+        return buf.raw[:k].decode("ascii")
 
 
 class FrameWriter:
@@ -108,8 +122,10 @@ class FrameWriter:
             raise self._err
 
 
-def build_from_config(cfg: SceneConfig, steps=None, verify=False, barrier=None, iteration_cap=None):
-    """cli.py:39-61: overrides applied to the solver section, then build_scene."""
+def build_from_config(cfg: SceneConfig, steps=None, verify=False, barrier=None, iteration_cap=None,
+                      eigensolver: str = "host"):
+    """cli.py:39-61: overrides applied to the solver section, then build_scene
+    (eigensolver "device" = the GPU subspace precompute, for large meshes)."""
     from .scenes import build_scene
 
     solver = cfg.solver
@@ -124,16 +140,17 @@ def build_from_config(cfg: SceneConfig, steps=None, verify=False, barrier=None, 
     cfg.solver = solver
     return build_scene(cfg.scene.kind, resolution=cfg.scene.resolution, size=cfg.scene.size,
                        density=cfg.material.density, stretch_stiffness=cfg.material.stretch_stiffness,
-                       bend_stiffness=cfg.material.bend_stiffness, config=solver)
+                       bend_stiffness=cfg.material.bend_stiffness, config=solver, eigensolver=eigensolver)
 
 
-def simulate(cfg: SceneConfig, steps=None, verify=False, barrier=None, iteration_cap=None, log=sys.stdout) -> int:
+def simulate(cfg: SceneConfig, steps=None, verify=False, barrier=None, iteration_cap=None, log=sys.stdout,
+             eigensolver: str = "host") -> int:
     """cli.py:64-98: frame_000000.obj, metrics.csv (one row per step), a frame every
     frame_stride steps and at the last step; exit code 2 with a state-dump OBJ on a
     penetration-invariant breach."""
     from ._lib import PenetrationError
 
-    sim = build_from_config(cfg, steps, verify, barrier, iteration_cap)
+    sim = build_from_config(cfg, steps, verify, barrier, iteration_cap, eigensolver)
     out = Path(cfg.output.directory)
     out.mkdir(parents=True, exist_ok=True)
     save_config(cfg, out / "config.toml")
@@ -197,6 +214,8 @@ def main(argv=None) -> int:
     common.add_argument("--barrier", choices=("ndb", "dbb"), default=None)
     common.add_argument("--iteration-cap", type=int, default=None, dest="iteration_cap")
     common.add_argument("--seed", type=int, default=0)
+    common.add_argument("--eigensolver", choices=("host", "device"), default="host",
+                        help="subspace precompute: scipy eigsh (reference) or the device solver")
     for name, verify in (("simulate", False), ("verify", True)):
         p = sub.add_parser(name, parents=[common])
         p.add_argument("config")
@@ -207,7 +226,8 @@ def main(argv=None) -> int:
     if args.command == "bench-ccd":
         return bench_ccd(args.pairs, args.seed)
     cfg = load_config(args.config)
-    return simulate(cfg, args.steps, args.verify or args.verify_default, args.barrier, args.iteration_cap)
+    return simulate(cfg, args.steps, args.verify or args.verify_default, args.barrier, args.iteration_cap,
+                    eigensolver=args.eigensolver)
 
 
 if __name__ == "__main__":

@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include <thread>
+#include <string>
 
 #include "common.cuh"
 #include "narrow.cu"
@@ -1630,6 +1632,38 @@ int cs_scene::residual_forward(const double* xfw, cs_step_report* rep) {
 extern "C" {
 
 const char* cs_version(void) { return "clothsim_b200 0.1 sm_100a fp64"; }
+
+// OBJ vertex block "v %.9f %.9f %.9f\n" (reference mesh.py:220-226; glibc printf and
+// Python's float formatting both round correctly, so the text is identical),
+// formatted by up to 16 host threads.  Returns the byte count, or -1 if cap is short.
+long long cs_format_obj_vertices(const double* v, long long n, char* out, long long cap) {
+    if (n < 0 || (n > 0 && (!v || !out))) return -1;
+    const int nt = (int)std::max<long long>(1, std::min<long long>(16, n / 8192));
+    std::vector<std::string> parts(nt);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            const long long a = n * t / nt, b = n * (t + 1) / nt;
+            std::string& o = parts[t];
+            o.reserve((size_t)(b - a) * 48);
+            char line[160];
+            for (long long i = a; i < b; ++i) {
+                const int k = std::snprintf(line, sizeof(line), "v %.9f %.9f %.9f\n", v[3 * i], v[3 * i + 1],
+                                            v[3 * i + 2]);
+                o.append(line, (size_t)std::min<int>(k, (int)sizeof(line) - 1));
+            }
+        });
+    for (auto& t : th) t.join();
+    long long total = 0;
+    for (auto& p : parts) total += (long long)p.size();
+    if (total > cap) return -1;
+    long long o = 0;
+    for (auto& p : parts) {
+        std::memcpy(out + o, p.data(), p.size());
+        o += (long long)p.size();
+    }
+    return total;
+}
 
 cs_scene* cs_scene_create(const cs_scene_desc* desc, const cs_step_config* cfg, int* status) {
     cs_scene* sc = new cs_scene();
