@@ -217,6 +217,8 @@ struct cs_scene {
     DBuf<int> fallback;
     DBuf<int> wl_full, wl_dist;
     DBuf<uint8_t> keep_flag;
+    DBuf<unsigned> keep_bits;
+    DBuf<int> tile_cnt, tile_off;
     // subset sites: a moving site served from the step's base site (subset_site)
     PairBuf basepr;
     DBuf<double> blo, bhi;
@@ -650,6 +652,35 @@ struct cs_scene {
         return 0;
     }
 
+    // fused keep + stable compaction, phase 1: tile bitmasks + counts + scan; the
+    // kept total lands in h_iscal[slot] after the caller's next sync
+    int keep_tiles(const PairBuf& src, const uint8_t* vv, const uint8_t* tv, const uint8_t* ev, int slot) {
+        const long long P0 = src.P;
+        const long long nt = (P0 + kKeepTile - 1) / kKeepTile;
+        CS_RET(keep_bits.ensure(std::max<long long>(nt * (kKeepTile / 32), 1)));
+        CS_RET(tile_cnt.ensure(nt + 1));
+        CS_RET(tile_off.ensure(nt + 1));
+        CS_TRY(cudaMemsetAsync(tile_cnt.p + nt, 0, sizeof(int), s));
+        if (nt) {
+            const KeepArgs A{src.keys.p, P0, vlo.p, vhi.p, ttab.box.p, etab.box.p, vv, tv, ev};
+            k_keep_tiles<<<(int)nt, 256, 0, s>>>(A, keep_bits.p, tile_cnt.p);
+            ++launches;
+        }
+        CS_RET(scan(tile_cnt.p, tile_off.p, (int)nt + 1));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[slot], tile_off.p + nt, sizeof(int), cudaMemcpyDeviceToHost, s));
+        return 0;
+    }
+    // phase 2: the kept rows of src into dst[0, kept) in order
+    int compact_tiles(const PairBuf& src, PairBuf& dst) {
+        const long long nt = (src.P + kKeepTile - 1) / kKeepTile;
+        if (nt) {
+            k_compact_tiles<<<(int)nt, 256, 0, s>>>(keep_bits.p, tile_off.p, src.P, src.kind.p, src.idx.p,
+                                                    src.keys.p, dst.kind.p, dst.idx.p, dst.keys.p);
+            ++launches;
+        }
+        return 0;
+    }
+
     // broad -> full CCD -> distance march -> clamp factor (stepper.py:426-452)
     // Motion-free site (xa == xb) right after a site whose pairs are in `prev`: when
     // the static boxes stay inside that site's boxes, the candidate set is the
@@ -674,25 +705,12 @@ struct cs_scene {
                                            etab.part.p, febox.p);
         k_prim_motion<3><<<gt, 256, 0, s>>>(wtris.p, ntw, x, x, ftbox.p);
         k_prim_motion<2><<<ge, 256, 0, s>>>(wedges.p, new_, x, x, febox.p);
-        const long long P0 = prev.P;
-        CS_RET(keep_flag.ensure(P0));
-        CS_RET(sel.ensure(P0));
-        k_pair_keep<<<grid(P0), 256, 0, s>>>(prev.keys.p, P0, vlo.p, vhi.p, ttab.box.p, etab.box.p, keep_flag.p);
-        launches += 5;
-        size_t bytes = 0;
-        cub::CountingInputIterator<int> it(0);
-        cub::DeviceSelect::Flagged(nullptr, bytes, it, keep_flag.p, sel.p, d_iscal.p + I_FLAG, (int)P0, s);
-        CS_RET(cub_tmp.ensure(bytes));
-        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, keep_flag.p, sel.p, d_iscal.p + I_FLAG, (int)P0, s));
-        CS_TRY(cudaMemcpyAsync(&h_iscal[I_FLAG], d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
+        launches += 4;
+        CS_RET(keep_tiles(prev, nullptr, nullptr, nullptr, I_FLAG));
         CS_TRY(cudaStreamSynchronize(s));
         const long long P = h_iscal[I_FLAG];
         CS_RET(pr.reserve(std::max<long long>(P, 1)));
-        if (P) {
-            k_gather_pairs<<<std::max(1, std::min(grid(P), 16 * sm_count)), 256, 0, s>>>(
-                sel.p, d_iscal.p + I_FLAG, prev.kind.p, prev.idx.p, prev.keys.p, pr.kind.p, pr.idx.p, pr.keys.p);
-            ++launches;
-        }
+        if (P) CS_RET(compact_tiles(prev, pr));
         CS_CHECK_LAUNCH();
         pr.P = P;
         ok = true;
@@ -763,20 +781,8 @@ struct cs_scene {
         CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, eviol.p, elist.p, d_iscal.p + I_COUNT + 2, new_, s));
         // surviving base pairs among non-violators
         const long long P0 = basepr.P;
-        CS_RET(keep_flag.ensure(std::max<long long>(P0, 1)));
-        CS_RET(sel.ensure(std::max<long long>(P0, 1)));
-        CS_TRY(cudaMemsetAsync(d_iscal.p + I_COUNT + 3, 0, sizeof(int), s));
-        if (P0) {
-            k_pair_keep<<<grid(P0), 256, 0, s>>>(basepr.keys.p, P0, vlo.p, vhi.p, ttab.box.p, etab.box.p,
-                                                 keep_flag.p, vviol.p, tviol.p, eviol.p);
-            ++launches;
-            bytes = 0;
-            cub::DeviceSelect::Flagged(nullptr, bytes, it, keep_flag.p, sel.p, d_iscal.p + I_COUNT + 3, (int)P0, s);
-            CS_RET(cub_tmp.ensure(bytes));
-            CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, keep_flag.p, sel.p, d_iscal.p + I_COUNT + 3,
-                                              (int)P0, s));
-        }
-        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], d_iscal.p + I_COUNT, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], d_iscal.p + I_COUNT, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_RET(keep_tiles(basepr, vviol.p, tviol.p, eviol.p, I_COUNT + 3));
         CS_TRY(cudaStreamSynchronize(s));
         const int nv = h_iscal[I_COUNT], nt = h_iscal[I_COUNT + 1], ne = h_iscal[I_COUNT + 2];
         const long long Pa = h_iscal[I_COUNT + 3];
@@ -818,12 +824,7 @@ struct cs_scene {
                          P0, Pa, nv, nt, ne, Q, bg[0], bg[1], bg[2], bg[3]);
         }
         CS_RET(pr.reserve(std::max<long long>(Pa + Q, 1)));
-        if (Pa) {
-            k_gather_pairs<<<std::max(1, std::min(grid(Pa), 16 * sm_count)), 256, 0, s>>>(
-                sel.p, d_iscal.p + I_COUNT + 3, basepr.kind.p, basepr.idx.p, basepr.keys.p, pr.kind.p, pr.idx.p,
-                pr.keys.p);
-            ++launches;
-        }
+        if (Pa) CS_RET(compact_tiles(basepr, pr));
         if (Q) {
             k_subset_query<1><<<gq, 128, 0, s>>>(A, W, nullptr, qoff.p,
                                                 PairOut{nullptr, nullptr, pr.kind.p + Pa, pr.idx.p + Pa,
@@ -1307,6 +1308,9 @@ void cs_scene::release() {
     edge_static.release();
     eflip.release();
     keep_flag.release();
+    keep_bits.release();
+    tile_cnt.release();
+    tile_off.release();
     basepr.release();
     blo.release();
     bhi.release();

@@ -1111,6 +1111,98 @@ __global__ void k_pair_keep(const unsigned long long* __restrict__ keys, int64_t
     keep[i] = overlap6(alo, ahi, blo, bhi) ? 1 : 0;
 }
 
+// Fused filter + stable compaction of a pair set (subset / motion-free sites).
+// Pass 1 (k_keep_tiles): per tile of kKeepTile pairs (one block), the keep test as
+// a bitmask (one ballot word per 32 pairs) and the tile's count.  Pass 2
+// (k_compact_tiles), after an exclusive scan of the counts: kept rows copied in
+// order.  Replaces flag array + select + index gather (one pass less over P).
+constexpr int kKeepTile = 256;  // one pair per thread
+
+struct KeepArgs {
+    const unsigned long long* __restrict__ keys;
+    int64_t P;
+    const double* __restrict__ vlo;
+    const double* __restrict__ vhi;
+    const double* __restrict__ tbox;
+    const double* __restrict__ ebox;
+    const uint8_t* __restrict__ vviol;  // nullable: no violators
+    const uint8_t* __restrict__ tviol;
+    const uint8_t* __restrict__ eviol;
+};
+
+__device__ __forceinline__ bool keep_pair(const KeepArgs& A, int64_t i) {
+    const unsigned long long k = A.keys[i];
+    const int p = (int)((k >> 32) & 0x7fffffffu), q = (int)(k & 0xffffffffu);
+    const bool ee = (k >> 63) != 0;
+    if (A.vviol != nullptr && (ee ? (A.eviol[p] | A.eviol[q]) != 0 : (A.vviol[p] | A.tviol[q]) != 0))
+        return false;  // re-found by k_subset_query
+    double alo[3], ahi[3], blo[3], bhi[3];
+    if (ee) {
+        load_box(A.ebox, p, alo, ahi);
+        load_box(A.ebox, q, blo, bhi);
+    } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            alo[c] = A.vlo[3 * (int64_t)p + c];
+            ahi[c] = A.vhi[3 * (int64_t)p + c];
+        }
+        load_box(A.tbox, q, blo, bhi);
+    }
+    return overlap6(alo, ahi, blo, bhi);
+}
+
+__global__ void __launch_bounds__(256) k_keep_tiles(KeepArgs A, unsigned* __restrict__ bits,
+                                                    int* __restrict__ tile_count) {
+    __shared__ int wsum[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * kKeepTile;
+    const int64_t i = base + threadIdx.x;
+    const bool keep = i < A.P && keep_pair(A, i);
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) {
+        bits[(base >> 5) + w] = m;
+        wsum[w] = __popc(m);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int j = 0; j < 8; ++j) t += wsum[j];
+        tile_count[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_compact_tiles(const unsigned* __restrict__ bits,
+                                                       const int* __restrict__ tile_off, int64_t P,
+                                                       const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+                                                       const unsigned long long* __restrict__ keys,
+                                                       int8_t* __restrict__ kind_o, int4* __restrict__ idx_o,
+                                                       unsigned long long* __restrict__ keys_o) {
+    constexpr int W = kKeepTile / 32;  // ballot words per tile
+    __shared__ int wpre[W];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * kKeepTile;
+    const unsigned* __restrict__ tb = bits + (base >> 5);
+    if (w == 0) {  // exclusive prefix of the word popcounts
+        const int c = lane < W ? __popc(tb[lane]) : 0;
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane < W) wpre[lane] = inc - c;
+    }
+    __syncthreads();
+    const unsigned m = tb[w];
+    const int64_t i = base + threadIdx.x;
+    if (i < P && ((m >> lane) & 1u)) {
+        const int pos = tile_off[blockIdx.x] + wpre[w] + __popc(m & ((1u << lane) - 1u));
+        kind_o[pos] = kind[i];
+        idx_o[pos] = idx[i];
+        keys_o[pos] = keys[i];
+    }
+}
+
 __global__ void k_gather_pairs(const int* __restrict__ sel, const int* __restrict__ count,
                                const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                                const unsigned long long* __restrict__ keys, int8_t* __restrict__ kind_o,
