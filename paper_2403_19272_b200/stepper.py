@@ -159,6 +159,17 @@ class Simulation:
         self._obs_dirty = False
         self._pin_pool = {}
         self._step_index = 0
+        # page-locked download buffers are allocated once, here (a cudaHostAlloc of a
+        # large array costs milliseconds): two, so a result still referenced by the
+        # caller does not force an allocation in the step loop
+        self._prealloc_pinned(self.mesh.vertex_count, 2)
+
+    def _prealloc_pinned(self, rows: int, count: int) -> None:
+        import torch
+
+        pool = self._pin_pool.setdefault(rows, [])
+        for _ in range(count - len(pool)):
+            pool.append(torch.empty((rows, 3), dtype=torch.float64, pin_memory=True))
 
     def __del__(self):
         scene = getattr(self, "_scene", None)
