@@ -224,6 +224,7 @@ struct cs_scene {
     DBuf<double> blo, bhi;
     DBuf<uint8_t> vviol, tviol, eviol;
     DBuf<int> vlist, tlist, elist, qcount, qoff;
+    DBuf<unsigned long long> query_dbg;  // CS_TRACE_SITES counters
     bool base_valid = false;
     double base_margin = -1.0;
     DBuf<char> cub_tmp;
@@ -797,12 +798,11 @@ struct cs_scene {
                           ttab.box.p, etab.box.p, vtab.view(), ttab.view(), etab.view(), ttab.inv.p, etab.inv.p,
                           (unsigned)(vtab.T - 1), (unsigned)(etab.T - 1), ntw, new_, nullptr};
         static const bool trace_sites = std::getenv("CS_TRACE_SITES") != nullptr;
-        static DBuf<unsigned long long> dbg;
         QueryArgs Aq = A;
         if (trace_sites) {
-            CS_RET(dbg.ensure(4));
-            CS_TRY(cudaMemsetAsync(dbg.p, 0, 4 * sizeof(unsigned long long), s));
-            Aq.big = dbg.p;
+            CS_RET(query_dbg.ensure(4));
+            CS_TRY(cudaMemsetAsync(query_dbg.p, 0, 4 * sizeof(unsigned long long), s));
+            Aq.big = query_dbg.p;
         }
         const WorldTopo W = world();
         const int gq = (int)std::max<long long>(1, (32 * nq + 127) / 128);
@@ -817,7 +817,7 @@ struct cs_scene {
         const long long Q = h_iscal[I_COUNT], Qvt = h_iscal[I_COUNT + 1];
         if (trace_sites) {
             unsigned long long bg[4];
-            CS_TRY(cudaMemcpy(bg, dbg.p, sizeof(bg), cudaMemcpyDeviceToHost));
+            CS_TRY(cudaMemcpy(bg, query_dbg.p, sizeof(bg), cudaMemcpyDeviceToHost));
             std::fprintf(stderr,
                          "[cs subset] base pairs %lld kept %lld violators v %d t %d e %d query pairs %lld "
                          "big v %llu t %llu e %llu max cells %llu\n",
@@ -1318,6 +1318,7 @@ void cs_scene::release() {
     tviol.release();
     eviol.release();
     for (DBuf<int>* b : {&vlist, &tlist, &elist, &qcount, &qoff}) b->release();
+    query_dbg.release();
     isect_out.release();
     fvbox.release();
     ftbox.release();

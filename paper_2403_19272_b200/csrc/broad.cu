@@ -1082,34 +1082,6 @@ __global__ void __launch_bounds__(128) k_subset_query(QueryArgs A, WorldTopo W, 
     if (PASS == 0 && lane == 0) counts[t] = cnt;
 }
 
-__global__ void k_pair_keep(const unsigned long long* __restrict__ keys, int64_t P, const double* __restrict__ vlo,
-                            const double* __restrict__ vhi, const double* __restrict__ tbox,
-                            const double* __restrict__ ebox, uint8_t* __restrict__ keep,
-                            const uint8_t* __restrict__ vviol = nullptr, const uint8_t* __restrict__ tviol = nullptr,
-                            const uint8_t* __restrict__ eviol = nullptr) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= P) return;
-    const unsigned long long k = keys[i];
-    const int p = (int)((k >> 32) & 0x7fffffffu), q = (int)(k & 0xffffffffu);
-    if (vviol != nullptr &&
-        ((k >> 63) ? (eviol[p] | eviol[q]) != 0 : (vviol[p] | tviol[q]) != 0)) {
-        keep[i] = 0;  // re-found by k_subset_query
-        return;
-    }
-    double alo[3], ahi[3], blo[3], bhi[3];
-    if (k >> 63) {
-        load_box(ebox, p, alo, ahi);
-        load_box(ebox, q, blo, bhi);
-    } else {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            alo[c] = vlo[3 * (int64_t)p + c];
-            ahi[c] = vhi[3 * (int64_t)p + c];
-        }
-        load_box(tbox, q, blo, bhi);
-    }
-    keep[i] = overlap6(alo, ahi, blo, bhi) ? 1 : 0;
-}
 
 // Fused filter + stable compaction of a pair set (subset / motion-free sites).
 // Pass 1 (k_keep_tiles): per tile of kKeepTile pairs (one block), the keep test as
@@ -1203,17 +1175,5 @@ __global__ void __launch_bounds__(256) k_compact_tiles(const unsigned* __restric
     }
 }
 
-__global__ void k_gather_pairs(const int* __restrict__ sel, const int* __restrict__ count,
-                               const int8_t* __restrict__ kind, const int4* __restrict__ idx,
-                               const unsigned long long* __restrict__ keys, int8_t* __restrict__ kind_o,
-                               int4* __restrict__ idx_o, unsigned long long* __restrict__ keys_o) {
-    const int n = count[0];
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-        const int i = sel[k];
-        kind_o[k] = kind[i];
-        idx_o[k] = idx[i];
-        keys_o[k] = keys[i];
-    }
-}
 
 }  // namespace cs
