@@ -722,7 +722,8 @@ struct cs_scene {
     // margin widened by a small slack into basepr and keeps its vertex boxes; the
     // grid tables stay valid until the next full broad phase.
     int build_base(const double* xa, const double* xb, double margin) {
-        static const double slack = std::getenv("CS_SITE_SLACK") ? std::atof(std::getenv("CS_SITE_SLACK")) : 0.01;
+        const char* env = std::getenv("CS_SITE_SLACK");
+        const double slack = env ? std::atof(env) : 0.01;
         CS_RET(broad_phase(xa, xb, margin + slack * margin, basepr));
         CS_RET(blo.ensure(3LL * nw));
         CS_RET(bhi.ensure(3LL * nw));
