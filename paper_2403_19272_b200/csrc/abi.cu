@@ -208,7 +208,7 @@ struct cs_scene {
     PairBuf pa, pb;  // current and next pair sets
     PairBuf* cur = &pa;
     PairBuf* nxt = &pb;
-    DBuf<int> sel, skey, ssrc, skey_s, ssrc_s, seg_beg, seg_end, rowflag, rows_act;
+    DBuf<int> sel, skey, ssrc, skey_s, ssrc_s, seg_beg, seg_end, rowflag, rows_act, skey_c;
     DBuf<double4> stamp;  // collision stamps: target xyz + weight
     DBuf<unsigned long long> hkeys;
     DBuf<int> hvals;
@@ -1058,28 +1058,43 @@ struct cs_scene {
         CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, pr.engaged.p, sel.p, d_iscal.p + I_BAD, (int)pr.P, s));
         k_collision_terms<<<grid(A), 256, 0, s>>>(sel.p, A, pr.kind.p, pr.idx.p, xw, pr.bary.p, pr.normal.p,
                                                   pr.weight.p, cfg.d_hat, n, free_index.p, 0, skey.p, stamp.p);
-        k_iota<<<grid(m), 256, 0, s>>>(ssrc.p, m);
-        launches += 2;
-        // stable sort of the 4A entries by free row keeps np.add.at's per-vertex order
+        ++launches;
+        // entries on a free row (a third of them are not: obstacle / pinned endpoints,
+        // zero weight), compacted in order: indices, then their keys
         bytes = 0;
-        // keys are free rows < nf or the 0x7fffffff sentinel: sort only the bits a row needs,
-        // with the sentinel clamped to 2^bits - 1 (still after every real row)
+        cub::DeviceSelect::If(nullptr, bytes, it, ssrc.p, d_iscal.p + I_COUNT + 7, (int)m, RowKept{skey.p, nf}, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::If(cub_tmp.p, bytes, it, ssrc.p, d_iscal.p + I_COUNT + 7, (int)m,
+                                     RowKept{skey.p, nf}, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 7], d_iscal.p + I_COUNT + 7, sizeof(int), cudaMemcpyDeviceToHost,
+                               s));
+        CS_TRY(cudaStreamSynchronize(s));
+        const long long mc = h_iscal[I_COUNT + 7];
+        static const bool trace_stamps = std::getenv("CS_TRACE_SITES") != nullptr;
+        if (trace_stamps)
+            std::fprintf(stderr, "[cs stamps] engaged %lld stamps %lld on free rows %lld\n", A, m, mc);
+        if (mc == 0) return 0;
+        CS_RET(skey_c.ensure(mc));
+        k_gather_keys<<<std::max(1, std::min(grid(mc), 16 * sm_count)), 256, 0, s>>>(ssrc.p, d_iscal.p + I_COUNT + 7,
+                                                                                    skey.p, skey_c.p);
+        ++launches;
+        // stable sort by free row keeps np.add.at's per-vertex order; only the bits a
+        // row needs
         int bits = 1;
         while ((1LL << bits) <= (long long)nf) ++bits;
-        k_clamp_keys<<<grid(m), 256, 0, s>>>(skey.p, (int)m, (1 << bits) - 1);
-        ++launches;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey.p, skey_s.p, ssrc.p, ssrc_s.p, (int)m, 0, bits, s);
+        bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey_c.p, skey_s.p, ssrc.p, ssrc_s.p, (int)mc, 0, bits, s);
         CS_RET(cub_tmp.ensure(bytes));
-        CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, skey.p, skey_s.p, ssrc.p, ssrc_s.p, (int)m, 0, bits,
-                                               s));
-        CS_TRY(cudaMemsetAsync(rowflag.p, 0, sizeof(int) * m, s));
-        k_mark_segments<<<grid(m), 256, 0, s>>>(skey_s.p, (int)m, nf, seg_beg.p, seg_end.p, rowflag.p);
+        CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, skey_c.p, skey_s.p, ssrc.p, ssrc_s.p, (int)mc, 0,
+                                               bits, s));
+        CS_TRY(cudaMemsetAsync(rowflag.p, 0, sizeof(int) * mc, s));
+        k_mark_segments<<<grid(mc), 256, 0, s>>>(skey_s.p, (int)mc, nf, seg_beg.p, seg_end.p, rowflag.p);
         ++launches;
         bytes = 0;
-        cub::DeviceSelect::Flagged(nullptr, bytes, skey_s.p, rowflag.p, rows_act.p, d_iscal.p + I_ROWS, (int)m, s);
+        cub::DeviceSelect::Flagged(nullptr, bytes, skey_s.p, rowflag.p, rows_act.p, d_iscal.p + I_ROWS, (int)mc, s);
         CS_RET(cub_tmp.ensure(bytes));
         CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, skey_s.p, rowflag.p, rows_act.p, d_iscal.p + I_ROWS,
-                                          (int)m, s));
+                                          (int)mc, s));
         CS_CHECK_LAUNCH();
         stamps_valid = true;
         n_stamp_rows = (int)std::min<long long>(m, nf);  // upper bound; exact count read on device
@@ -1296,7 +1311,7 @@ void cs_scene::release() {
     DBuf<int>* ints[] = {&free_ids, &free_index, &pin_ids, &pin_slot, &e0, &e1, &rinc_ptr, &rinc, &ginc_ptr, &ginc,
                          &st, &binc_ptr, &binc, &sell_ptr, &sell_col, &hfp_ptr, &hfp_col, &wtris, &wedges,
                          &edge_tris, &edge_slot, &patch, &pslot, &sel, &skey, &ssrc, &skey_s,
-                         &ssrc_s, &seg_beg, &seg_end, &rowflag, &rows_act, &hvals, &fallback, &wl_full, &wl_dist, &d_iscal};
+                         &ssrc_s, &seg_beg, &seg_end, &rowflag, &rows_act, &skey_c, &hvals, &fallback, &wl_full, &wl_dist, &d_iscal};
     for (auto* p : ints) p->release();
     DBuf<double>* dbl[] = {&mass, &fext, &mh2, &erest, &ew, &bk, &bw, &sell_val, &diag, &hfp_val, &U, &V, &lam,
                            &x, &v, &xprev, &df, &obs, &z, &xs_w, &xc_w, &anchor_w, &tmp_w, &xf, &xf0, &b, &t,

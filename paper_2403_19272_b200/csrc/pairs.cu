@@ -101,6 +101,19 @@ __global__ void k_mark_segments(const int* __restrict__ skey, int m, int nrows, 
 }
 
 // compaction helpers for the per-stage collision-terms entry point
+// stable compaction of the stamp entries that land on a free row: indices from
+// DeviceSelect::If with this predicate, then their keys
+struct RowKept {
+    const int* __restrict__ key;
+    int nf;
+    __host__ __device__ __forceinline__ bool operator()(int i) const { return key[i] < nf; }
+};
+__global__ void k_gather_keys(const int* __restrict__ idx, const int* __restrict__ count,
+                              const int* __restrict__ key, int* __restrict__ out) {
+    const int n = count[0];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = key[idx[j]];
+}
+
 __global__ void k_key_kept(const int* __restrict__ key, int m, int nf, uint8_t* __restrict__ flag) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) flag[i] = key[i] < nf ? 1 : 0;
