@@ -945,7 +945,7 @@ __global__ void __launch_bounds__(256, 4) k_collision_terms(const int* __restric
         if (cloth_only && ids[k] >= n_cloth) keep = false;
         int64_t o = 4 * a + k;
         key[o] = keep ? free_index[ids[k]] : 0x7fffffff;
-        stamp_out[o] = make_double4(tg.x, tg.y, tg.z, w);
+        if (keep) stamp_out[o] = make_double4(tg.x, tg.y, tg.z, w);  // others are never read
     }
 }
 
