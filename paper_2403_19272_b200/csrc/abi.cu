@@ -393,7 +393,7 @@ struct cs_scene {
         if (refactor && n_rows_act_known > 0) {
             const int gg = std::min(cs_div_up(n_rows_act_known, 8), sm_count);
             CS_RET(part2.ensure((size_t)gg * r * r));
-            k_gram_partial<<<gg, 256, 0, s>>>(rows_act.p, d_iscal.p + I_ROWS, dl, V.p, r, part2.p);
+            k_gram_partial<<<gg, kGramThreads, 0, s>>>(rows_act.p, d_iscal.p + I_ROWS, dl, V.p, r, part2.p);
             k_reduce_partials<<<cs_div_up(r * r, 32), 256, 0, s>>>(part2.p, gg, r * r, gram_red.p);
             launches += 2;
             gram = gram_red.p;

@@ -334,51 +334,76 @@ __global__ void __launch_bounds__(256) k_project_partial(Sell H, const double* _
 }
 
 // G partials over the ascending list of collided rows (count read on device):
-// block b owns a contiguous chunk of the list.
-// Block b owns a contiguous chunk of the collided-row list; rows are staged in
-// shared memory 32 at a time and every thread accumulates its (a, b) entries in
-// row order, s = fma(V_ia, delta_i V_ib, s).
-__global__ void __launch_bounds__(256) k_gram_partial(const int* __restrict__ rows,
-                                                      const int* __restrict__ nrows_ptr,
-                                                      const double* __restrict__ delta,
-                                                      const double* __restrict__ V, int r,
-                                                      double* __restrict__ part) {
-    constexpr int kTile = 32;
-    __shared__ double sv[kTile][33];
-    __shared__ double sd[kTile];
+// block b owns a contiguous chunk of the list.  Rows are staged 64 at a time in
+// shared memory (V_i and delta_i V_i, padded to 32 columns); each of the 64 threads
+// owns a 4x4 register tile of the 32x32 output and accumulates every row of the
+// chunk in order, s = fma(V_ia, delta_i V_ib, s) - four operand loads per 16 FMAs,
+// the same per-entry operation sequence as a thread-per-entry loop.  All 256
+// threads stage (8 independent loads each); the first 64 accumulate.
+constexpr int kGramThreads = 256;
+__global__ void __launch_bounds__(kGramThreads) k_gram_partial(const int* __restrict__ rows,
+                                                               const int* __restrict__ nrows_ptr,
+                                                               const double* __restrict__ delta,
+                                                               const double* __restrict__ V, int r,
+                                                               double* __restrict__ part) {
+    constexpr int kT = 64;
+    __shared__ __align__(16) double sv[kT][32];
+    __shared__ __align__(16) double sw[kT][32];
     const int cnt = *nrows_ptr;
     const int per = (cnt + gridDim.x - 1) / gridDim.x;
     const int beg = min(cnt, (int)blockIdx.x * per);
     const int end = min(cnt, beg + per);
-    const int nout = r * r;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int oa[4], ob[4];
+    const int t = threadIdx.x;
+    const int ta = ((t & 63) >> 3) * 4, tb = (t & 7) * 4;
+    double acc[4][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int o = threadIdx.x + q * blockDim.x;
-        oa[q] = o < nout ? o / r : 0;
-        ob[q] = o < nout ? o % r : 0;
-    }
-    for (int t0 = beg; t0 < end; t0 += kTile) {
-        const int nt = min(kTile, end - t0);
-        for (int e = threadIdx.x; e < nt * r; e += blockDim.x) {
-            const int k = e / r, c = e - k * r;
-            sv[k][c] = V[(int64_t)rows[t0 + k] * r + c];
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int t0 = beg; t0 < end; t0 += kT) {
+        const int nt = min(kT, end - t0);
+        constexpr int kPer = kT * 32 / kGramThreads;
+        double v[kPer], d[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = t + u * kGramThreads, k = e >> 5, c = e & 31;
+            v[u] = 0.0;
+            d[u] = 0.0;
+            if (k < nt && c < r) {
+                const int row = rows[t0 + k];
+                v[u] = V[(int64_t)row * r + c];
+                d[u] = delta[row];
+            }
         }
-        if (threadIdx.x < nt) sd[threadIdx.x] = delta[rows[t0 + threadIdx.x]];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = t + u * kGramThreads, k = e >> 5, c = e & 31;
+            sv[k][c] = v[u];
+            sw[k][c] = d[u] * v[u];
+        }
         __syncthreads();
+        if (t < 64)
         for (int k = 0; k < nt; ++k) {
-            const double dk = sd[k];
+            const double2 a01 = *reinterpret_cast<const double2*>(&sv[k][ta]);
+            const double2 a23 = *reinterpret_cast<const double2*>(&sv[k][ta + 2]);
+            const double2 b01 = *reinterpret_cast<const double2*>(&sw[k][tb]);
+            const double2 b23 = *reinterpret_cast<const double2*>(&sw[k][tb + 2]);
+            const double av[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] = fma(sv[k][oa[q]], dk * sv[k][ob[q]], acc[q]);
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
         }
         __syncthreads();
     }
+    if (t >= 64) return;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int o = threadIdx.x + q * blockDim.x;
-        if (o < nout) part[(int64_t)blockIdx.x * nout + o] = acc[q];
-    }
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int a = ta + i, b = tb + j;
+            if (a < r && b < r) part[(int64_t)blockIdx.x * r * r + a * r + b] = acc[i][j];
+        }
 }
 
 // ---------------------------------------------------------------- reduced solve (one CTA)
