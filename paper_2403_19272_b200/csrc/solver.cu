@@ -299,19 +299,31 @@ __global__ void __launch_bounds__(256) k_project_partial(Sell H, const double* _
             res[r][2] = rr.z;
         }
         __syncthreads();
-        for (int r = warp; r < PROJ_TILE; r += nw) {
-            const int i = tile0 + r;
-            if (i >= H.nrows) break;
-            const double r0 = res[r][0], r1 = res[r][1], r2 = res[r][2];
-            const double* row = B + (int64_t)i * rb;
+        // four rows per step with all basis loads issued first (same row order per lane)
+        for (int r = warp; r < PROJ_TILE; r += 4 * nw) {
+            double bv[4][4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int j = lane + 32 * q;
-                if (j < rb) {
-                    const double bij = __ldg(row + j);
-                    acc[q][0] = fma(bij, r0, acc[q][0]);
-                    acc[q][1] = fma(bij, r1, acc[q][1]);
-                    acc[q][2] = fma(bij, r2, acc[q][2]);
+            for (int u = 0; u < 4; ++u) {
+                const int i = tile0 + r + u * nw;
+                const double* row = B + (int64_t)i * rb;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = lane + 32 * q;
+                    bv[u][q] = (i < H.nrows && r + u * nw < PROJ_TILE && j < rb) ? __ldg(row + j) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int rr = r + u * nw;
+                if (rr >= PROJ_TILE || tile0 + rr >= H.nrows) break;
+                const double r0 = res[rr][0], r1 = res[rr][1], r2 = res[rr][2];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (lane + 32 * q < rb) {
+                        acc[q][0] = fma(bv[u][q], r0, acc[q][0]);
+                        acc[q][1] = fma(bv[u][q], r1, acc[q][1]);
+                        acc[q][2] = fma(bv[u][q], r2, acc[q][2]);
+                    }
                 }
             }
         }
