@@ -263,8 +263,10 @@ struct cs_scene {
         stage_start = e;
     }
     int sync_scalars() {
-        CS_TRY(cudaMemcpyAsync(h_scal, d_scal.p, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaMemcpyAsync(h_iscal, d_iscal.p, I_COUNT * sizeof(int), cudaMemcpyDeviceToHost, s));
+        // doubles [0, S_COUNT) and ints [0, I_COUNT) in one copy (the 4-double scratch
+        // between them rides along; its host copy is only read right after its own sync)
+        CS_TRY(cudaMemcpyAsync(h_scal, d_scal.p, (S_COUNT + 4) * sizeof(double) + I_COUNT * sizeof(int),
+                               cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaStreamSynchronize(s));
         return check_divergence();
     }
@@ -1273,12 +1275,15 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(Xred.ensure(32 * 32));
     CS_RET(beta_red.ensure(1));
     CS_RET(fallback.ensure(1));
-    CS_RET(d_scal.ensure(S_COUNT));
-    CS_RET(d_iscal.ensure(I_COUNT + 8));  // [I_COUNT, +8): subset-site counters
-    CS_TRY(cudaMemset(d_scal.p, 0, sizeof(double) * S_COUNT));
-    CS_TRY(cudaMemset(d_iscal.p, 0, sizeof(int) * I_COUNT));
-    CS_TRY(cudaMallocHost(&h_scal, sizeof(double) * (S_COUNT + 4)));  // [S_COUNT, +4): broad-phase scratch
-    CS_TRY(cudaMallocHost(&h_iscal, sizeof(int) * (I_COUNT + 8)));  // [I_COUNT, +8): broad-phase scratch
+    // scalar block, one allocation on each side so sync_scalars is a single copy:
+    // [S_COUNT doubles | 4 doubles scratch | I_COUNT ints | 8 ints scratch]
+    constexpr int kScalDoubles = S_COUNT + 4 + (I_COUNT + 8 + 1) / 2;
+    CS_RET(d_scal.ensure(kScalDoubles, true));
+    CS_TRY(cudaMemset(d_scal.p, 0, sizeof(double) * kScalDoubles));
+    d_iscal.p = reinterpret_cast<int*>(d_scal.p + S_COUNT + 4);  // view into d_scal
+    d_iscal.n = I_COUNT + 8;
+    CS_TRY(cudaMallocHost(&h_scal, sizeof(double) * kScalDoubles));
+    h_iscal = reinterpret_cast<int*>(h_scal + S_COUNT + 4);
     CS_RET(pa.reserve(1024));
     CS_RET(pb.reserve(1024));
     CS_TRY(cudaDeviceSynchronize());
@@ -1301,8 +1306,7 @@ void cs_scene::release() {
     copy_stream = nullptr;
     for (auto e : ev_pool) cudaEventDestroy(e);
     ev_pool.clear();
-    if (h_scal) cudaFreeHost(h_scal);
-    if (h_iscal) cudaFreeHost(h_iscal);
+    if (h_scal) cudaFreeHost(h_scal);  // h_iscal is a view into it
     if (h_stage) cudaFreeHost(h_stage);
     h_stage = nullptr;
     h_scal = nullptr;
@@ -1311,7 +1315,9 @@ void cs_scene::release() {
     DBuf<int>* ints[] = {&free_ids, &free_index, &pin_ids, &pin_slot, &e0, &e1, &rinc_ptr, &rinc, &ginc_ptr, &ginc,
                          &st, &binc_ptr, &binc, &sell_ptr, &sell_col, &hfp_ptr, &hfp_col, &wtris, &wedges,
                          &edge_tris, &edge_slot, &patch, &pslot, &sel, &skey, &ssrc, &skey_s,
-                         &ssrc_s, &seg_beg, &seg_end, &rowflag, &rows_act, &skey_c, &hvals, &fallback, &wl_full, &wl_dist, &d_iscal};
+                         &ssrc_s, &seg_beg, &seg_end, &rowflag, &rows_act, &skey_c, &hvals, &fallback, &wl_full, &wl_dist};
+    d_iscal.p = nullptr;  // view into d_scal
+    d_iscal.n = 0;
     for (auto* p : ints) p->release();
     DBuf<double>* dbl[] = {&mass, &fext, &mh2, &erest, &ew, &bk, &bw, &sell_val, &diag, &hfp_val, &U, &V, &lam,
                            &x, &v, &xprev, &df, &obs, &z, &xs_w, &xc_w, &anchor_w, &tmp_w, &xf, &xf0, &b, &t,
