@@ -375,7 +375,9 @@ def run_ours(args, ws, rank, local):
     setup_s = time.time() - t_setup
     stream = torch.cuda.current_stream()
     stepper = Stepper(sims, args.streams)
-    stepper.run(args.warmup)
+    # warm-up also exercises the e2e read-back path (first-use costs of the
+    # page-locked download buffers are paid here, not inside either timed region)
+    stepper.run(args.warmup, on_step=None if args.no_e2e else (lambda s: s.state.x))
     barrier(ws)
     torch.cuda.synchronize()
     reps = []
