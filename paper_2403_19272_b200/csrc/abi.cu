@@ -227,6 +227,7 @@ struct cs_scene {
     DBuf<unsigned long long> query_dbg;  // CS_TRACE_SITES counters
     bool base_valid = false;
     double base_margin = -1.0;
+    int subset_fail = 0;  // consecutive outer-loop sites that refused the subset path
     DBuf<char> cub_tmp;
     DBuf<double> d_scal;
     DBuf<int> d_iscal;
@@ -783,16 +784,19 @@ struct cs_scene {
         cub::DeviceSelect::Flagged(nullptr, bytes, it, eviol.p, elist.p, d_iscal.p + I_COUNT + 2, new_, s);
         CS_RET(cub_tmp.ensure(bytes));
         CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, eviol.p, elist.p, d_iscal.p + I_COUNT + 2, new_, s));
-        // surviving base pairs among non-violators
-        const long long P0 = basepr.P;
+        // violator counts decide first (nothing else is queued yet, so a refusal wastes
+        // only the box and violator passes)
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], d_iscal.p + I_COUNT, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_RET(keep_tiles(basepr, vviol.p, tviol.p, eviol.p, I_COUNT + 3));
         CS_TRY(cudaStreamSynchronize(s));
         const int nv = h_iscal[I_COUNT], nt = h_iscal[I_COUNT + 1], ne = h_iscal[I_COUNT + 2];
-        const long long Pa = h_iscal[I_COUNT + 3];
         const long long nq = (long long)nv + nt + ne;
-        // violator x violator work is quadratic: past this the full broad phase is cheaper
-        if ((double)nv * nt + 0.5 * (double)ne * ne > 2e8) return 0;
+        // violator x violator tests: one warp walks a whole violator list, so the
+        // longest list sets the kernel's latency chain, and the total is quadratic;
+        // past these the full broad phase is cheaper
+        if (std::max(nt, ne) > 16384 || (double)nv * nt + 0.5 * (double)ne * ne > 1e8) return 0;
+        // surviving base pairs among non-violators (count lands with the query totals)
+        const long long P0 = basepr.P;
+        CS_RET(keep_tiles(basepr, vviol.p, tviol.p, eviol.p, I_COUNT + 3));
         // violator partners: count, scan, write
         CS_RET(qcount.ensure(nq + 1));
         CS_RET(qoff.ensure(nq + 1));
@@ -818,6 +822,7 @@ struct cs_scene {
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], qoff.p + nv + nt, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaStreamSynchronize(s));
         const long long Q = h_iscal[I_COUNT], Qvt = h_iscal[I_COUNT + 1];
+        const long long Pa = h_iscal[I_COUNT + 3];
         if (trace_sites) {
             unsigned long long bg[4];
             CS_TRY(cudaMemcpy(bg, query_dbg.p, sizeof(bg), cudaMemcpyDeviceToHost));
@@ -918,8 +923,9 @@ struct cs_scene {
         return 0;
     }
 
-    // base: 0 full broad phase; 1 subset of the current base site if possible;
-    // 2 this site becomes the base (first moving site of a step)
+    // base: 0 full broad phase; 1 subset of the current base site if there is one
+    // (else / on refusal the full broad phase); 2 this site becomes the base (first
+    // moving site of a step)
     int ccd_site(const double* xa, const double* xb, PairBuf& pr, cs_step_report* rep, double& clamp,
                  PairBuf* prev_site = nullptr, int base = 0) {
         stage(T_BROAD);
@@ -930,16 +936,18 @@ struct cs_scene {
             CS_RET(broad_phase_static(xa, cfg.d_hat, *prev_site, pr, done));
             if (done && verify) CS_RET(verify_static_site(xa, pr));
             if (done && rep) rep->static_sites += 1;
-        } else if (base != 0 && !no_subset) {
-            if (base == 1) {
-                CS_RET(subset_site(xa, xb, cfg.d_hat, pr, done));
-                if (done && rep) rep->subset_sites += 1;
-                if (done && verify) CS_RET(verify_site(xa, xb, pr));
-            }
-            if (!done) {
+        } else if (base == 2 && !no_subset) {
+            // a base costs a widened broad phase + a compaction; skip it while outer-loop
+            // sites keep refusing the subset path (retry every 8 steps)
+            if (subset_fail < 2 || step_index % 8 == 0) {
                 CS_RET(build_base(xa, xb, cfg.d_hat));
                 CS_RET(subset_site(xa, xb, cfg.d_hat, pr, done));
             }
+        } else if (base == 1 && !no_subset && base_valid) {
+            CS_RET(subset_site(xa, xb, cfg.d_hat, pr, done));
+            subset_fail = done ? 0 : subset_fail + 1;
+            if (done && rep) rep->subset_sites += 1;
+            if (done && verify) CS_RET(verify_site(xa, xb, pr));
         }
         if (!done) CS_RET(broad_phase(xa, xb, cfg.d_hat, pr));
         stage(T_FULL);
