@@ -45,13 +45,20 @@ using namespace cs;
 
 namespace {
 
+// Stream the DBuf (re)allocations of the current call are ordered on.  Buffers come
+// from the device's stream-ordered pool (cudaMallocAsync / cudaFreeAsync, release
+// threshold raised at scene creation): a mid-run regrowth neither synchronises the
+// device nor maps fresh memory once the pool has grown (a plain cudaFree/cudaMalloc
+// pair of a few hundred MB costs tens of ms).
+thread_local cudaStream_t t_alloc_stream = nullptr;
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
     int ensure(size_t m, bool exact = false) {
         if (m <= n && p) return 0;
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, t_alloc_stream);
         p = nullptr;
         // regrowth reserves 2x: per-step sizes (pairs, grid entries) drift and
         // every cudaFree/cudaMalloc of a large buffer stalls the stream
@@ -62,7 +69,7 @@ struct DBuf {
         else if (!exact && want > (1u << 16)) want *= 3;
         static const bool trace = std::getenv("CS_TRACE_ALLOC") != nullptr;
         if (trace) std::fprintf(stderr, "[cs alloc] %zu -> %zu bytes\n", n * sizeof(T), want * sizeof(T));
-        cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), want * sizeof(T), t_alloc_stream);
         if (e != cudaSuccess) {
             n = 0;
             p = nullptr;
@@ -74,7 +81,8 @@ struct DBuf {
     int upload(const T* host, size_t m) {
         CS_RET(ensure(m, true));
         if (m && host) {
-            cudaError_t e = cudaMemcpy(p, host, m * sizeof(T), cudaMemcpyHostToDevice);
+            cudaError_t e = cudaStreamSynchronize(t_alloc_stream);
+            if (e == cudaSuccess) e = cudaMemcpy(p, host, m * sizeof(T), cudaMemcpyHostToDevice);
             if (e != cudaSuccess) return 1000 + (int)e;
         }
         return 0;
@@ -1701,6 +1709,34 @@ long long cs_format_obj_vertices(const double* v, long long n, char* out, long l
 }
 
 cs_scene* cs_scene_create(const cs_scene_desc* desc, const cs_step_config* cfg, int* status) {
+    {
+        // keep freed blocks in the stream-ordered pool (DBuf regrowth reuses them)
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            // map a slab into the pool once per process, so pair-buffer regrowth under
+            // contact is served without mapping fresh memory (CS_POOL_RESERVE_GB, default
+            // min(24 GB, a quarter of the free memory); 0 disables)
+            static bool reserved = false;
+            if (!reserved) {
+                reserved = true;
+                size_t free_b = 0, total_b = 0;
+                cudaMemGetInfo(&free_b, &total_b);
+                const char* env = std::getenv("CS_POOL_RESERVE_GB");
+                size_t want = env ? (size_t)(std::atof(env) * (1ull << 30))
+                                  : std::min<size_t>(24ull << 30, free_b / 4);
+                void* slab = nullptr;
+                if (want && cudaMallocAsync(&slab, want, nullptr) == cudaSuccess) {
+                    cudaFreeAsync(slab, nullptr);
+                    cudaStreamSynchronize(nullptr);
+                }
+                cudaGetLastError();
+            }
+        }
+    }
+    t_alloc_stream = nullptr;
     cs_scene* sc = new cs_scene();
     int rc = sc->create(desc, cfg);
     if (status) *status = rc;
@@ -1733,6 +1769,7 @@ int cs_step(cs_scene* scene, const double* pin_next, const double* obstacle_next
     const auto t0 = std::chrono::steady_clock::now();
     if (report) std::memset(report, 0, sizeof(*report));
     scene->s = (cudaStream_t)stream;
+    t_alloc_stream = scene->s;
     int rc = scene->step(pin_next, obstacle_next, report);
     scene->stage(-1);
     if (trace_host) {
@@ -1750,6 +1787,7 @@ int cs_get_state(cs_scene* sc, double* x, double* x_dot, double* x_prev, double*
                  int* step_index, void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
+    t_alloc_stream = s;
     const size_t nb = sizeof(double) * 3 * sc->n;
     if (x) CS_TRY(cudaMemcpyAsync(x, sc->x.p, nb, cudaMemcpyDeviceToHost, s));
     if (x_dot) CS_TRY(cudaMemcpyAsync(x_dot, sc->v.p, nb, cudaMemcpyDeviceToHost, s));
@@ -1766,6 +1804,7 @@ int cs_set_state(cs_scene* sc, const double* x, const double* x_dot, const doubl
                  const double* obstacle_x, int step_index, void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
+    t_alloc_stream = s;
     const size_t nb = sizeof(double) * 3 * sc->n;
     if (x) CS_TRY(cudaMemcpyAsync(sc->x.p, x, nb, cudaMemcpyHostToDevice, s));
     if (x_dot) CS_TRY(cudaMemcpyAsync(sc->v.p, x_dot, nb, cudaMemcpyHostToDevice, s));
@@ -1795,6 +1834,7 @@ int cs_state_device(cs_scene* sc, double** x, double** x_dot, double** delta_f, 
 int cs_frame_async(cs_scene* sc, double* host_x, int* ticket, void* stream) {
     if (!sc || !host_x || !ticket) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
+    t_alloc_stream = s;
     if (!sc->copy_stream) CS_TRY(cudaStreamCreateWithFlags(&sc->copy_stream, cudaStreamNonBlocking));
     const int k = sc->frame_next;
     cs_scene::FrameSlot& f = sc->frame_slots[k];
@@ -1860,6 +1900,7 @@ int cs_partial_ccd(const int8_t* kind, const int* idx4, const double* x_start, c
     CS_RET(life.ensure(P));
     CS_RET(eng.ensure(P));
     cudaStream_t s = (cudaStream_t)stream;
+    t_alloc_stream = s;
     CS_TRY(cudaMemsetAsync(bary.p, 0, sizeof(double) * 2 * P, s));
     CS_TRY(cudaMemsetAsync(normal.p, 0, sizeof(double) * 3 * P, s));
     CS_TRY(cudaMemsetAsync(life.p, 0, sizeof(int) * P, s));
@@ -1890,6 +1931,7 @@ int cs_broad_phase(cs_scene* sc, const double* x_start_w, const double* x_end_w,
                    void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     CS_RET(sc->broad_phase(x_start_w, x_end_w, margin, *sc->cur));
     if (count) *count = sc->cur->P;
     CS_TRY(cudaStreamSynchronize(sc->s));
@@ -1900,6 +1942,7 @@ int cs_ccd_site(cs_scene* sc, const double* x_start_w, const double* x_end_w, lo
                 void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     double c = 1.0;
     const int rc = sc->ccd_site(x_start_w, x_end_w, *sc->cur, nullptr, c);
     if (count) *count = sc->cur->P;
@@ -1911,6 +1954,7 @@ int cs_ccd_site(cs_scene* sc, const double* x_start_w, const double* x_end_w, lo
 int cs_scene_pair_results(cs_scene* sc, double* toi, double* toi_filter, void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
+    t_alloc_stream = s;
     const long long P = sc->cur->P;
     if (P == 0) return 0;
     if (toi) CS_TRY(cudaMemcpyAsync(toi, sc->cur->toi.p, sizeof(double) * P, cudaMemcpyDeviceToDevice, s));
@@ -1927,6 +1971,7 @@ int cs_scene_set_verify(cs_scene* sc, int on) {
 int cs_intersections(cs_scene* sc, const double* x_world, long long* count, int* pairs, int cap, void* stream) {
     if (!sc || cap < 0) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     const double* xw = x_world;
     if (!xw) {  // current world state
         CS_TRY(cudaMemcpyAsync(sc->tmp_w.p, sc->x.p, sizeof(double) * 3 * sc->n, cudaMemcpyDeviceToDevice, sc->s));
@@ -1958,6 +2003,7 @@ int cs_last_intersections(cs_scene* sc, long long* count, int* pairs, int cap, d
 int cs_scene_pairs(cs_scene* sc, int8_t* kind, int* idx4, void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
+    t_alloc_stream = s;
     const long long P = sc->cur->P;
     if (P == 0) return 0;
     if (kind) CS_TRY(cudaMemcpyAsync(kind, sc->cur->kind.p, P, cudaMemcpyDeviceToDevice, s));
@@ -1969,6 +2015,7 @@ int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const int* c
                     const double* coll_t, int n_coll, double* b, double* delta, void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     cudaStream_t s = sc->s;
     bool with = false;
     CS_TRY(cudaMemsetAsync(sc->seg_beg.p, 0, sizeof(int) * sc->nf, s));
@@ -2008,6 +2055,7 @@ int cs_collision_terms(cs_scene* sc, const int8_t* kind, const int* idx4, const 
                        double* w, double* targets, long long* count, void* stream) {
     if (!sc || P < 0) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     cudaStream_t s = sc->s;
     if (count) *count = 0;
     if (P == 0) return 0;
@@ -2053,6 +2101,7 @@ int cs_collision_terms(cs_scene* sc, const int8_t* kind, const int* idx4, const 
 int cs_residual(cs_scene* sc, const double* b, const double* x, const double* delta, double* r, void* stream) {
     if (!sc || !delta) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     k_residual<<<sc->grid(sc->nf), 256, 0, sc->s>>>(sc->sell(), b, x, delta, r);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(sc->s));
@@ -2063,6 +2112,7 @@ int cs_ajacobi_smooth(cs_scene* sc, const double* b, double* x, int iterations, 
                       void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     const double* dl = delta;
     if (dl == nullptr) {
         CS_TRY(cudaMemsetAsync(sc->delta.p, 0, sizeof(double) * sc->nf, sc->s));
@@ -2075,6 +2125,7 @@ int cs_ajacobi_smooth(cs_scene* sc, const double* b, double* x, int iterations, 
 int cs_reduced_correction(cs_scene* sc, const double* b, double* x, const double* delta, int reuse, void* stream) {
     if (!sc || !delta) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     int rows = 0;
     if (!reuse) {
         // active rows = flatnonzero(delta) (subspace.py:182)
@@ -2098,6 +2149,7 @@ int cs_reduced_correction(cs_scene* sc, const double* b, double* x, const double
 int cs_warmstart_correction(cs_scene* sc, const double* b, double* x, void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     CS_RET(sc->warm_correction(b, x));
     CS_TRY(cudaStreamSynchronize(sc->s));
     return 0;
@@ -2107,6 +2159,7 @@ int cs_energy_gradient(cs_scene* sc, const double* x, const double* z, const int
                        const double* q_t, int n_q, double* grad, void* stream) {
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
     cudaStream_t s = sc->s;
     bool with = false;
     CS_TRY(cudaMemsetAsync(sc->seg_beg.p, 0, sizeof(int) * sc->nf, s));
