@@ -110,3 +110,19 @@ def test_broad_phase_oversize_primitives(cuda, rng):
     ref = _brute_set(x0, x1, sim.world_triangles, sim.tri_static, 1e-3)
     assert len(got) == len(ref)
     assert _canon(got.kind, got.idx) == ref
+
+
+def test_broad_phase_dense_pile(cuda, rng):
+    """A cloth crumpled into a 2 cm ball: every grid cell holds hundreds of entries
+    (bucket runs beyond the shared-memory staging cap take the long-run path)."""
+    import paper_2403_19272_b200 as P
+
+    sim = P.build_scene("hanging", resolution=16, config=P.StepConfig())
+    xw = sim.world(sim.state.x)
+    x0 = 0.02 * rng.random(size=xw.shape)
+    x1 = x0 + 0.005 * rng.normal(size=xw.shape)
+    got = sim.broad_phase(x0, x1, 1e-3)
+    topo = WorldTopology.build(sim.world_triangles, sim.tri_static)
+    k_ref, i_ref = oracle_broad(x0, x1, topo, 1e-3)
+    assert len(got) == len(k_ref) > 100_000
+    assert _rows(got.kind, got.idx) == _rows(k_ref, i_ref)
