@@ -242,6 +242,8 @@ struct cs_scene {
     double* h_scal = nullptr;
     int* h_iscal = nullptr;
     double* h_stage = nullptr;  // pinned: [pins (3 npin) | obstacles (3 nobs)]
+    static constexpr int kMaxNormChecks = 64;
+    double* h_norms = nullptr;  // pinned: smoother residual norms (divergence check)
     cudaStream_t s = 0;
     long long launches = 0;
     // timing
@@ -273,11 +275,14 @@ struct cs_scene {
     }
     int sync_scalars() {
         // doubles [0, S_COUNT) and ints [0, I_COUNT) in one copy (the 4-double scratch
-        // between them rides along; its host copy is only read right after its own sync)
+        // between them rides along; its host copy is only read right after its own
+        // sync), plus the smoother's pending residual norms
         CS_TRY(cudaMemcpyAsync(h_scal, d_scal.p, (S_COUNT + 4) * sizeof(double) + I_COUNT * sizeof(int),
                                cudaMemcpyDeviceToHost, s));
+        const int nchk = pending_checks >= 2 ? std::min(pending_checks, kMaxNormChecks) : 0;
+        if (nchk) CS_TRY(cudaMemcpyAsync(h_norms, norms.p, sizeof(double) * nchk, cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaStreamSynchronize(s));
-        return check_divergence();
+        return check_divergence(nchk);
     }
     int grid(long long m, int bs = 256) { return (int)std::max<long long>(1, (m + bs - 1) / bs); }
 
@@ -378,18 +383,12 @@ struct cs_scene {
         return 0;
     }
 
-    int check_divergence() {
-        if (pending_checks < 2) {
-            pending_checks = 0;
-            return 0;
-        }
-        std::vector<double> hn(pending_checks);
-        CS_TRY(cudaMemcpyAsync(hn.data(), norms.p, sizeof(double) * pending_checks, cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
-        const int m = pending_checks;
+    // smoothing.py:57-64: raise if a checked residual norm grew 10x (norms copied to
+    // h_norms by the caller's sync)
+    int check_divergence(int m) {
         pending_checks = 0;
         for (int i = 1; i < m; ++i)
-            if (hn[i] > 10.0 * hn[i - 1]) return CS_DIVERGENCE;
+            if (h_norms[i] > 10.0 * h_norms[i - 1]) return CS_DIVERGENCE;
         return 0;
     }
 
@@ -1300,6 +1299,7 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     d_iscal.n = I_COUNT + 8;
     CS_TRY(cudaMallocHost(&h_scal, sizeof(double) * kScalDoubles));
     h_iscal = reinterpret_cast<int*>(h_scal + S_COUNT + 4);
+    CS_TRY(cudaMallocHost(&h_norms, sizeof(double) * kMaxNormChecks));
     CS_RET(pa.reserve(1024));
     CS_RET(pb.reserve(1024));
     CS_TRY(cudaDeviceSynchronize());
@@ -1323,6 +1323,8 @@ void cs_scene::release() {
     for (auto e : ev_pool) cudaEventDestroy(e);
     ev_pool.clear();
     if (h_scal) cudaFreeHost(h_scal);  // h_iscal is a view into it
+    if (h_norms) cudaFreeHost(h_norms);
+    h_norms = nullptr;
     if (h_stage) cudaFreeHost(h_stage);
     h_stage = nullptr;
     h_scal = nullptr;
@@ -2119,7 +2121,7 @@ int cs_ajacobi_smooth(cs_scene* sc, const double* b, double* x, int iterations, 
         dl = sc->delta.p;
     }
     CS_RET(sc->smooth(b, x, iterations, omega, dl));
-    return sc->check_divergence();
+    return sc->sync_scalars();  // includes the residual-norm divergence check
 }
 
 int cs_reduced_correction(cs_scene* sc, const double* b, double* x, const double* delta, int reuse, void* stream) {
