@@ -11,6 +11,9 @@ sys.path.insert(0, ".")
 import paper_2403_19272_b200 as P  # noqa: E402
 from paper_2403_19272_b200 import _lib, scenes as S  # noqa: E402
 
+if len(sys.argv) > 1:  # optional: a specific build of the library (A/B)
+    _lib.load(sys.argv[1])
+
 cfg = P.StepConfig(h=1.0 / 200.0)
 sim = S.skirt_scene(cfg, around=584, down=584, eigensolver="device")
 nf = sim.mesh.free.size
