@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(256) k_site_filter(const unsigned long long* _
     wl_append(need_dist, i, wl_dist, counts + 1);
 }
 
-__global__ void __launch_bounds__(128, 6) k_full_ccd_wl(const int* __restrict__ wl, const int* __restrict__ count,
+__global__ void __launch_bounds__(128, 4) k_full_ccd_wl(const int* __restrict__ wl, const int* __restrict__ count,
                                                      const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                                                      const double* __restrict__ x0, const double* __restrict__ x1,
                                                      int single, double tol, double* __restrict__ toi_out) {
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(128, 6) k_full_ccd_wl(const int* __restrict__ 
 // distance march over its worklist + the minimum folded with one atomicMin on the
 // (non-negative) fp64 bit pattern per block - exact and order independent.
 // min_slot must hold +inf before the launch.
-__global__ void __launch_bounds__(128, 6) k_distance_toi_wl(const int* __restrict__ wl, const int* __restrict__ count,
+__global__ void __launch_bounds__(128, 4) k_distance_toi_wl(const int* __restrict__ wl, const int* __restrict__ count,
                                                          const int8_t* __restrict__ kind,
                                                          const int4* __restrict__ idx, const double* __restrict__ x0,
                                                          const double* __restrict__ x1, double floor_frac,
