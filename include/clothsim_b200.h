@@ -106,6 +106,8 @@ typedef struct {
     long long gpu_launches;
     int static_sites;           /* motion-free CCD sites served from the previous site's pairs */
     int subset_sites;           /* moving CCD sites served from the step's base site (+ violator queries) */
+    int verified_sites;         /* subset / motion-free sites re-checked against a full broad phase (CS_VERIFY_STATIC_SITE) */
+    int host_syncs;             /* host<->device synchronisations inside this cs_step */
 } cs_step_report;
 
 /* ---- scene lifetime ---------------------------------------------------- */

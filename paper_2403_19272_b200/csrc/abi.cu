@@ -206,6 +206,7 @@ struct cs_scene {
     DBuf<int> ocount, ooffset;
     // state
     DBuf<double> x, v, xprev, df, obs;
+    DBuf<double> dfn;  // residual-forwarding result, committed with the new state
     int step_index = 0;
     // work arrays
     DBuf<double> z, xs_w, xc_w, anchor_w, tmp_w, xf, xf0, b, t, delta, prev_outer, grad, fr;
@@ -273,6 +274,11 @@ struct cs_scene {
         active_stage = k;
         stage_start = e;
     }
+    int n_syncs = 0;  // host<->device synchronisations in the current cs_step
+    cudaError_t hsync() {
+        ++n_syncs;
+        return cudaStreamSynchronize(s);
+    }
     int sync_scalars() {
         // doubles [0, S_COUNT) and ints [0, I_COUNT) in one copy (the 4-double scratch
         // between them rides along; its host copy is only read right after its own
@@ -281,7 +287,7 @@ struct cs_scene {
                                cudaMemcpyDeviceToHost, s));
         const int nchk = pending_checks >= 2 ? std::min(pending_checks, kMaxNormChecks) : 0;
         if (nchk) CS_TRY(cudaMemcpyAsync(h_norms, norms.p, sizeof(double) * nchk, cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         return check_divergence(nchk);
     }
     int grid(long long m, int bs = 256) { return (int)std::max<long long>(1, (m + bs - 1) / bs); }
@@ -551,7 +557,7 @@ struct cs_scene {
             CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + k], tabs[k]->offset.p + tabs[k]->np, sizeof(int), cudaMemcpyDeviceToHost, s));
             CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 4 + k], tabs[k]->n_over.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         }
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         for (int k = 0; k < 3; ++k) {
             tabs[k]->m = h_iscal[I_COUNT + k];
             tabs[k]->n_over_h = h_iscal[I_COUNT + 4 + k];
@@ -580,7 +586,7 @@ struct cs_scene {
         long long* hits_h = reinterpret_cast<long long*>(h_scal + S_COUNT);
         CS_TRY(cudaMemcpyAsync(&hits_h[0], vtab.iter_off.p + vtab.m, sizeof(long long), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&hits_h[1], etab.iter_off.p + etab.m, sizeof(long long), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         CS_RET(vtab.masks.ensure(std::max<long long>(hits_h[0], 1)));
         CS_RET(etab.masks.ensure(std::max<long long>(hits_h[1], 1)));
         // pair counts: [VT runs][VT oversize][EE runs][EE oversize]
@@ -631,7 +637,7 @@ struct cs_scene {
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], oo_vt + n_ovt, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 2], etab.poffset.p + etab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 3], oo_ee + n_oee, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         const long long c0 = h_iscal[I_COUNT + 0], c1 = h_iscal[I_COUNT + 1], c2 = h_iscal[I_COUNT + 2], c3 = h_iscal[I_COUNT + 3];
         const long long P = c0 + c1 + c2 + c3;
         CS_RET(pr.reserve(std::max<long long>(P, 1)));
@@ -704,7 +710,7 @@ struct cs_scene {
         k_box_contained<<<grid(3LL * nw), 256, 0, s>>>(x, 3 * nw, margin, vlo.p, vhi.p, d_iscal.p + I_FLAG);
         ++launches;
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_FLAG], d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         if (h_iscal[I_FLAG]) return 0;
         // boxes of this site (static), then the surviving subset of prev
         k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(x, x, nw, margin, vlo.p, vhi.p, fvbox.p);
@@ -718,7 +724,7 @@ struct cs_scene {
         k_prim_motion<2><<<ge, 256, 0, s>>>(wedges.p, new_, x, x, febox.p);
         launches += 4;
         CS_RET(keep_tiles(prev, nullptr, nullptr, nullptr, I_FLAG));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         const long long P = h_iscal[I_FLAG];
         CS_RET(pr.reserve(std::max<long long>(P, 1)));
         if (P) CS_RET(compact_tiles(prev, pr));
@@ -794,7 +800,7 @@ struct cs_scene {
         // violator counts decide first (nothing else is queued yet, so a refusal wastes
         // only the box and violator passes)
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], d_iscal.p + I_COUNT, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         const int nv = h_iscal[I_COUNT], nt = h_iscal[I_COUNT + 1], ne = h_iscal[I_COUNT + 2];
         const long long nq = (long long)nv + nt + ne;
         // violator x violator tests: one warp walks a whole violator list, so the
@@ -827,7 +833,7 @@ struct cs_scene {
         CS_RET(scan(qcount.p, qoff.p, (int)nq + 1));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], qoff.p + nq, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], qoff.p + nv + nt, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         const long long Q = h_iscal[I_COUNT], Qvt = h_iscal[I_COUNT + 1];
         const long long Pa = h_iscal[I_COUNT + 3];
         if (trace_sites) {
@@ -859,9 +865,29 @@ struct cs_scene {
     // test hook (CS_VERIFY_STATIC_SITE): the subset path must give exactly the full
     // broad phase's key set; returns CS_INTERNAL on any difference
     int verify_static_site(const double* x, PairBuf& got) { return verify_site(x, x, got); }
+    // The reference broad phase runs on a private set of grid tables, so the step's
+    // base site (its tables, cell sizes and base_valid) survives the check and later
+    // outer-loop sites of the same step still take -- and get checked on -- the
+    // subset path.  The site boxes it recomputes are the same values (same xa, xb,
+    // margin) the subset path just wrote.
+    EntryBuf vtab_v, ttab_v, etab_v;
     int verify_site(const double* xa, const double* xb, PairBuf& got) {
         PairBuf full;
-        CS_RET(broad_phase(xa, xb, cfg.d_hat, full));
+        if (vtab_v.np == 0) {
+            CS_RET(vtab_v.create(nw, false));
+            CS_RET(ttab_v.create(ntw, true));
+            CS_RET(etab_v.create(new_, true));
+        }
+        const bool keep_valid = base_valid;
+        std::swap(vtab, vtab_v);
+        std::swap(ttab, ttab_v);
+        std::swap(etab, etab_v);
+        int brc = broad_phase(xa, xb, cfg.d_hat, full);
+        std::swap(vtab, vtab_v);
+        std::swap(ttab, ttab_v);
+        std::swap(etab, etab_v);
+        base_valid = keep_valid;
+        CS_RET(brc);
         int rc = 0;
         if (full.P != got.P) {
             rc = CS_INTERNAL;
@@ -877,7 +903,7 @@ struct cs_scene {
             std::vector<unsigned long long> ha(full.P), hb(full.P);
             CS_TRY(cudaMemcpyAsync(ha.data(), a.p, sizeof(unsigned long long) * full.P, cudaMemcpyDeviceToHost, s));
             CS_TRY(cudaMemcpyAsync(hb.data(), b.p, sizeof(unsigned long long) * full.P, cudaMemcpyDeviceToHost, s));
-            CS_TRY(cudaStreamSynchronize(s));
+            CS_TRY(hsync());
             if (ha != hb) rc = CS_INTERNAL;
             a.release();
             b.release();
@@ -908,7 +934,7 @@ struct cs_scene {
         CS_RET(table_count(ttab, ts, ttab.inv.p));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], ttab.offset.p + ttab.np, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], ttab.n_over.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         ttab.m = h_iscal[I_COUNT];
         ttab.n_over_h = h_iscal[I_COUNT + 1];
         ttab.set_buckets(ttab.m);
@@ -925,7 +951,7 @@ struct cs_scene {
         launches += 2;
         CS_CHECK_LAUNCH();
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_FLAG], d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         count = h_iscal[I_FLAG];
         return 0;
     }
@@ -943,18 +969,22 @@ struct cs_scene {
             CS_RET(broad_phase_static(xa, cfg.d_hat, *prev_site, pr, done));
             if (done && verify) CS_RET(verify_static_site(xa, pr));
             if (done && rep) rep->static_sites += 1;
+            if (done && verify && rep) rep->verified_sites += 1;
         } else if (base == 2 && !no_subset) {
             // a base costs a widened broad phase + a compaction; skip it while outer-loop
             // sites keep refusing the subset path (retry every 8 steps)
             if (subset_fail < 2 || step_index % 8 == 0) {
                 CS_RET(build_base(xa, xb, cfg.d_hat));
                 CS_RET(subset_site(xa, xb, cfg.d_hat, pr, done));
+                if (done && verify) CS_RET(verify_site(xa, xb, pr));
+                if (done && verify && rep) rep->verified_sites += 1;
             }
         } else if (base == 1 && !no_subset && base_valid) {
             CS_RET(subset_site(xa, xb, cfg.d_hat, pr, done));
             subset_fail = done ? 0 : subset_fail + 1;
             if (done && rep) rep->subset_sites += 1;
             if (done && verify) CS_RET(verify_site(xa, xb, pr));
+            if (done && verify && rep) rep->verified_sites += 1;
         }
         if (!done) CS_RET(broad_phase(xa, xb, cfg.d_hat, pr));
         stage(T_FULL);
@@ -1034,7 +1064,7 @@ struct cs_scene {
         k_count_nonzero<<<grid(old.P), 256, 0, s>>>(old.life.p, old.P, d_iscal.p + I_LIVE);
         ++launches;
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_LIVE], d_iscal.p + I_LIVE, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         const long long live = h_iscal[I_LIVE];
         if (live == 0) return 0;
         unsigned long long cap = 1024;
@@ -1085,7 +1115,7 @@ struct cs_scene {
                                      RowKept{skey.p, nf}, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 7], d_iscal.p + I_COUNT + 7, sizeof(int), cudaMemcpyDeviceToHost,
                                s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         const long long mc = h_iscal[I_COUNT + 7];
         static const bool trace_stamps = std::getenv("CS_TRACE_SITES") != nullptr;
         if (trace_stamps)
@@ -1266,7 +1296,7 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     CS_RET(obs.ensure(std::max(3LL * nobs, 1LL)));
     // work
     for (DBuf<double>* w : {&xs_w, &xc_w, &anchor_w, &tmp_w}) CS_RET(w->ensure(3LL * nw));
-    for (DBuf<double>* w : {&z, &prev_outer, &grad}) CS_RET(w->ensure(3LL * n));
+    for (DBuf<double>* w : {&z, &prev_outer, &grad, &dfn}) CS_RET(w->ensure(3LL * n));
     for (DBuf<double>* w : {&xf, &xf0, &b, &t, &fr}) CS_RET(w->ensure(3LL * nf));
     CS_RET(delta.ensure(nf));
     CS_RET(pins_next_d.ensure(std::max(3 * npin, 1)));
@@ -1339,7 +1369,7 @@ void cs_scene::release() {
     for (auto* p : ints) p->release();
     DBuf<double>* dbl[] = {&mass, &fext, &mh2, &erest, &ew, &bk, &bw, &sell_val, &diag, &hfp_val, &U, &V, &lam,
                            &x, &v, &xprev, &df, &obs, &z, &xs_w, &xc_w, &anchor_w, &tmp_w, &xf, &xf0, &b, &t,
-                           &delta, &prev_outer, &grad, &fr, &pins_next_d, &obs_next_d, &vlo, &vhi, &vdisp, &tdisp, &edisp,
+                           &delta, &prev_outer, &grad, &dfn, &fr, &pins_next_d, &obs_next_d, &vlo, &vhi, &vdisp, &tdisp, &edisp,
                            &part, &part2, &spart, &rhs_red, &gram_red, &q, &Xred, &beta_red, &d_scal, &norms};
     for (auto* p : dbl) p->release();
     tri_static.release();
@@ -1371,12 +1401,16 @@ void cs_scene::release() {
     vtab.release();
     ttab.release();
     etab.release();
+    vtab_v.release();
+    ttab_v.release();
+    etab_v.release();
     ocount.release();
     ooffset.release();
 }
 
 int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_report* rep) {
     launches = 0;
+    n_syncs = 0;
     ev_used = 0;
     spans.clear();
     active_stage = -1;
@@ -1571,21 +1605,26 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             return CS_PENETRATION;
         }
     }
-    // ---- new state (stepper.py:594-602)
-    CS_TRY(cudaMemcpyAsync(xprev.p, x.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
-    k_velocity_update<<<grid(3LL * n), 256, 0, s>>>(tmp_w.p, x.p, v.p, 3LL * n, h);
-    ++launches;
-    CS_TRY(cudaMemcpyAsync(x.p, tmp_w.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
-    CS_TRY(cudaMemsetAsync(df.p, 0, sizeof(double) * 3 * n, s));
-    if (nobs) CS_TRY(cudaMemcpyAsync(obs.p, tmp_w.p + 3LL * n, sizeof(double) * 3 * nobs, cudaMemcpyDeviceToDevice, s));
-    CS_CHECK_LAUNCH();
-    // ---- residual forwarding (stepper.py:604-610)
+    // ---- residual forwarding (stepper.py:604-610) into the scratch dfn: it can
+    // still fail (smoother divergence, allocation), and the reference raises
+    // before `self.state = new_state`, leaving the state untouched
     const bool needs_rf = toi_exit < cfg.eps_toi || (cap_hit && dx_last > cfg.eps_outer);
     if (needs_rf) {
         stage(T_RF);
         CS_RET(residual_forward(tmp_w.p, rep));
         stage(-1);
     }
+    // ---- new state (stepper.py:594-602), committed only after every check passed
+    CS_TRY(cudaMemcpyAsync(xprev.p, x.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    k_velocity_update<<<grid(3LL * n), 256, 0, s>>>(tmp_w.p, x.p, v.p, 3LL * n, h);
+    ++launches;
+    CS_TRY(cudaMemcpyAsync(x.p, tmp_w.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    if (needs_rf)
+        CS_TRY(cudaMemcpyAsync(df.p, dfn.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    else
+        CS_TRY(cudaMemsetAsync(df.p, 0, sizeof(double) * 3 * n, s));
+    if (nobs) CS_TRY(cudaMemcpyAsync(obs.p, tmp_w.p + 3LL * n, sizeof(double) * 3 * nobs, cudaMemcpyDeviceToDevice, s));
+    CS_CHECK_LAUNCH();
     ++step_index;
     if (rep) {
         rep->lg_iterations = lg;
@@ -1597,7 +1636,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         rep->active_pairs = (int)active_pairs;
         rep->n_outer_deltas = n_deltas;
         rep->gpu_launches = launches;
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         double acc[kStages] = {0};
         for (auto& sp : spans) {
             float ms = 0.f;
@@ -1631,7 +1670,8 @@ int cs_scene::residual_forward(const double* xfw, cs_step_report* rep) {
     }
     CS_RET(stamps(ex, A, xfw));
     // f_r = -grad E at x_final (quad collision form), delta from stamps
-    k_energy_grad<<<grid(n), 256, 0, s>>>(n, x.p, z.p, mass.p, cfg.h, edges(), ginc_ptr.p, ginc.p,
+    // cloth rows of x_final_w (the state is not committed yet)
+    k_energy_grad<<<grid(n), 256, 0, s>>>(n, xfw, z.p, mass.p, cfg.h, edges(), ginc_ptr.p, ginc.p,
                                           BendSet{st.p, bk.p, bw.p}, binc_ptr.p, binc.p, free_index.p,
                                           stamps_valid ? seg_beg.p : nullptr, seg_end.p, ssrc_s.p, stamp.p,
                                           grad.p);
@@ -1652,22 +1692,22 @@ int cs_scene::residual_forward(const double* xfw, cs_step_report* rep) {
         CS_RET(sync_scalars());
         if (h_scal[S_RES] <= cfg.rf_tolerance * std::max(h_scal[S_NORM_F], 1e-30)) break;
     }
-    CS_TRY(cudaMemsetAsync(df.p, 0, sizeof(double) * 3 * n, s));
-    k_forward_force<<<grid(nf), 256, 0, s>>>(xf.p, free_ids.p, nf, mass.p, cfg.h, df.p);
+    CS_TRY(cudaMemsetAsync(dfn.p, 0, sizeof(double) * 3 * n, s));
+    k_forward_force<<<grid(nf), 256, 0, s>>>(xf.p, free_ids.p, nf, mass.p, cfg.h, dfn.p);
     ++launches;
-    CS_RET(sqnorm(df.p, nullptr, n, nullptr, S_DFNORM));
+    CS_RET(sqnorm(dfn.p, nullptr, n, nullptr, S_DFNORM));
     CS_RET(sync_scalars());
     const double nrm = h_scal[S_DFNORM];
     if (nrm > cfg.delta_f_cap) {
         h_scal[S_DFSCALE] = cfg.delta_f_cap / nrm;
         CS_TRY(cudaMemcpyAsync(d_scal.p + S_DFSCALE, &h_scal[S_DFSCALE], sizeof(double), cudaMemcpyHostToDevice, s));
-        k_scale<<<grid(3LL * n), 256, 0, s>>>(df.p, 3LL * n, d_scal.p + S_DFSCALE);
+        k_scale<<<grid(3LL * n), 256, 0, s>>>(dfn.p, 3LL * n, d_scal.p + S_DFSCALE);
         ++launches;
     }
     CS_CHECK_LAUNCH();
     if (rep) {
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_FALLBACK], fallback.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(cudaStreamSynchronize(s));
+        CS_TRY(hsync());
         rep->reduced_fallbacks += h_iscal[I_FALLBACK];
     }
     return 0;

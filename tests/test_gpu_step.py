@@ -231,11 +231,38 @@ def test_subset_sites_are_exact(cuda, monkeypatch, kind, kw, steps):
 
     monkeypatch.setenv("CS_VERIFY_STATIC_SITE", "1")
     sim = P.build_scene(kind, config=P.StepConfig(h=1.0 / 200.0), **kw)
-    served = 0
+    served = verified = 0
     for _ in range(steps):
         sim.step()
-        served += sim.last_report_c.subset_sites
+        c = sim.last_report_c
+        served += c.subset_sites
+        verified += c.verified_sites
+        # every subset / motion-free site of the step was re-checked (the check's own
+        # broad phase runs on private grid tables, so the base survives it)
+        assert c.verified_sites >= c.subset_sites + c.static_sites, (c.verified_sites, c.subset_sites)
     assert served >= steps // 2, served
+
+
+def test_subset_sites_verified_across_outer_loops(cuda, monkeypatch):
+    """Contact steps with several outer loops: the 2nd and later outer-loop sites of a
+    step still take the subset path after the first one was verified, and are verified
+    too (a verification broad phase must not invalidate the step's base site)."""
+    import paper_2403_19272_b200 as P
+    from conftest import golden
+
+    monkeypatch.setenv("CS_VERIFY_STATIC_SITE", "1")
+    g = golden("contact_sphere14.npz")
+    sim = P.build_scene("sphere_drape", resolution=14, size=0.2, config=P.StepConfig())
+    best = 0
+    for s in range(12, 24):
+        sim.state = P.SimState(x=g["x"][s], x_dot=g["x_dot"][s], x_prev=g["x_prev"][s], delta_f=g["delta_f"][s],
+                               step_index=s)
+        sim.obstacle_x = g["obstacle_x"][s]
+        sim.step()
+        c = sim.last_report_c
+        assert c.verified_sites >= c.subset_sites + c.static_sites
+        best = max(best, c.subset_sites)
+    assert best >= 2, "no step served more than one outer-loop site from its base"
 
 
 def test_subset_sites_exact_without_slack(cuda, monkeypatch):
