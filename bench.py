@@ -1,18 +1,23 @@
 """Benchmark: sim FPS & ms/frame at dt = 1/200 on the ~340K-vertex garment (BASELINE config 4).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload skirt|batch]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload skirt|batch|small]
 
-One process per GPU (torchrun for N > 1).  A single garment does not shard
-(SURVEY.md section 8e): at N > 1 every rank steps its own independent replica
-(weak scaling, no collective on the hot path; the only collective is the
-max-over-ranks timing reduction).  ``--workload batch`` runs config 5 (64
-independent 100K-vertex drapes split 64/N per GPU).
+One process per GPU.  ``--gpus N`` with N > 1 and no torchrun environment
+re-launches itself under ``torch.distributed.run`` (N ranks, 127.0.0.1); under
+torchrun the ranks are read from the environment.  A single garment does not
+shard: at N = 1 the workload is config 4 (the skirt);
+at N > 1 it is config 5 (64 independent 100K-vertex drapes split 64/N per GPU,
+``batch.scene_shard``) -- scene-parallel, no collective on the hot path (the
+process group carries only the barriers, the max-over-ranks timing reduction
+and the rank census).  ``--workload`` overrides.
 
 Rank 0 prints ONE JSON line.  ``value`` = whole-job steps/s (device time,
 CUDA events on the launching stream, max over ranks); ``e2e`` = the same
 metric through the public API with host buffers every step (pin/obstacle
 targets H2D inside cs_step, state x D2H after it), on the SAME K steps: the state
-is snapshotted before the timed region and restored for the e2e replay.
+is snapshotted before the timed region and restored for the e2e replay.  The
+same K steps are replayed a third time (untimed) with the device intersection
+check on every step (``penetration_free.verified_steps == steps``).
 """
 
 from __future__ import annotations
@@ -40,14 +45,18 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="skirt", choices=["skirt", "batch", "small"])
+    ap.add_argument("--workload", default=None, choices=["skirt", "batch", "small"],
+                    help="default: skirt (config 4) at N = 1, batch (config 5) at N > 1")
     ap.add_argument("--resolution", type=int, default=584)
     ap.add_argument("--batch-scenes", type=int, default=64)
     ap.add_argument("--streams", type=int, default=8, help="worker streams for multi-scene workloads")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--verify-steps", type=int, default=5,
-                    help="untimed steps with the device intersection check after the timed region")
+    ap.add_argument("--no-verify", action="store_true",
+                    help="skip the untimed verified replay of the timed steps")
+    ap.add_argument("--no-paper-regime", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-process plumbing only (spawn, rank census, barriers, max-over-ranks); no GPU work")
     return ap.parse_args()
 
 
@@ -107,6 +116,20 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def maybe_spawn(args):
+    """--gpus N > 1 outside torchrun: re-launch this script as N ranks (one per GPU)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -115,14 +138,59 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
-        # one process per GPU; BENCH_DIST_BACKEND=gloo lets the N>1 plumbing be
-        # exercised with several ranks sharing one device (collectives are only the
-        # barrier and the max-over-ranks timing reduction - nothing on the hot path)
-        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
-        local = local % max(torch.cuda.device_count(), 1)
-        torch.cuda.set_device(local)
+        # one process per GPU; the process group carries no data-plane traffic (barriers,
+        # the max-over-ranks timing reduction and the rank census only).
+        # BENCH_DIST_BACKEND=gloo runs the plumbing with ranks sharing one device / no device.
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
+        if torch.cuda.is_available():
+            local = local % max(torch.cuda.device_count(), 1)
+            torch.cuda.set_device(local)
         dist.init_process_group(backend)
     return ws, rank, local
+
+
+def rank_census(ws: int, rank: int, local: int) -> list:
+    """Every rank's identity (pid, host, device), gathered on all ranks."""
+    import socket
+
+    me = {"rank": rank, "local_rank": local, "pid": os.getpid(), "host": socket.gethostname(), "device": None}
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            me["device"] = f"cuda:{torch.cuda.current_device()} {torch.cuda.get_device_name()}"
+    except Exception:  # noqa: BLE001
+        pass
+    if ws == 1:
+        return [me]
+    import torch.distributed as dist
+
+    out = [None] * ws
+    dist.all_gather_object(out, me)
+    return out
+
+
+def process_group_info(ws: int) -> dict:
+    if ws == 1:
+        return {"world_size": 1, "backend": None, "data_plane": "none (single process)"}
+    import torch.distributed as dist
+
+    return {"world_size": ws, "backend": dist.get_backend(),
+            "data_plane": "no communicator on the hot path: ranks step disjoint scene sets; the process group "
+                          "carries barriers, the max-over-ranks timing reduction and this census"}
+
+
+def run_dry(args, ws, rank, local):
+    """Plumbing check (CPU ok): spawn, census, barrier, max-over-ranks; no numbers are claimed."""
+    census = rank_census(ws, rank, local)
+    barrier(ws)
+    t0 = time.perf_counter()
+    barrier(ws)
+    t = max_over_ranks(time.perf_counter() - t0, ws)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "value": None, "n_gpus": ws, "ranks": census,
+                          "process_group": process_group_info(ws), "barrier_s_max": t,
+                          "workload": args.workload}), flush=True)
 
 
 def max_over_ranks(v: float, ws: int) -> float:
@@ -131,7 +199,7 @@ def max_over_ranks(v: float, ws: int) -> float:
     import torch
     import torch.distributed as dist
 
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"  # gloo: host tensor
     t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -162,66 +230,124 @@ def make_scenes(args, rank: int, ws: int):
 
 
 # ------------------------------------------------------------------ CPU oracle timing (bounded sample)
+def _one_thread():
+    """Pin BLAS to one host thread (the reference is a single-
+    threaded numpy program); returns the context manager."""
+    from threadpoolctl import threadpool_limits
+
+    return threadpool_limits(limits=1)
+
+
+def broad_calibration():
+    """Reference patch-BVH / oracle grid-join broad-phase time ratio at the bench's
+    spacing (profiles/broad_calibration.json, tools/calibrate_broad.py: both run on
+    the same worlds in the build container)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "broad_calibration.json")) as fh:
+            cal = json.load(fh)
+        skirt = [c["factor"] for c in cal["cases"] if c["world"].startswith("skirt")]
+        return float(skirt[0] if skirt else cal["factor"]), cal
+    except (OSError, KeyError, ValueError):
+        return 1.0, None
+
+
 def cpu_oracle_estimate(o, counts, band: int = 8):
-    """Oracle (numpy port of the reference, single thread) seconds per step on this
-    workload, from a bounded sample (~10-20 s of CPU work):
+    """Reference-algorithm seconds per step on this workload from a bounded sample
+    (~15-25 s of CPU work, one host thread):
       * one warm-start correction and one LG iteration on the full mesh;
       * one broad phase over a contiguous 1/band slice of the world triangles
-        (rows of the garment), scaled per candidate pair;
-      * full CCD + distance march and partial CCD on a 20K-pair sample.
-    Combined with the GPU run's own per-step counts (warm-start iterations, LG
-    iterations, CCD sites, pairs per site)."""
+        (rows of the garment), per candidate pair, scaled by the reference/port
+        broad-phase ratio measured on the same spacing (broad_calibration);
+      * full CCD + distance march and partial CCD on a 20K-pair sample;
+    combined with the per-step counts (warm-start iterations, LG iterations, CCD
+    sites, pairs per site) of the GPU run of this trajectory."""
     from oracle import narrow, solver
     from oracle.broad import WorldTopology, broad_phase
 
-    st = o.state
-    cfg = o.cfg
-    t0 = time.perf_counter()
-    z = st.x + cfg.h * st.x_dot + (cfg.h * cfg.h) * (o.gravity_force + st.delta_f) / o.mesh.vertex_mass[:, None]
-    pins = st.x[o.mesh.pinned]
-    z[o.mesh.pinned] = pins
-    b, _ = solver.assemble_rhs(o.sys, o.mesh, o.el, z, z, pins)
-    solver.warmstart_correction(o.sub, o.sys, b, z[o.mesh.free])
-    t_ws = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    rep = {"timings": {k: 0.0 for k in ("local", "global", "smoothing")}}
-    o.inner_solve(z, st.x.copy(), pins, None, rep)
-    t_lg = time.perf_counter() - t0
-    xw = o.world(st.x)
-    xw1 = xw + 1e-4
-    tris = o.topo.triangles
-    m = max(1, len(tris) // band)
-    sub = WorldTopology.build(tris[:m], o.topo.tri_static[:m])
-    t0 = time.perf_counter()
-    kind, idx = broad_phase(xw, xw1, sub, cfg.d_hat)
-    t_bp_sub = time.perf_counter() - t0
-    per_pair_bp = t_bp_sub / max(len(kind), 1)
-    ns = min(len(kind), 20000)
-    sel = np.random.default_rng(0).choice(len(kind), ns, replace=False) if len(kind) > ns else np.arange(len(kind))
-    t0 = time.perf_counter()
-    narrow.full_ccd(kind[sel], idx[sel], xw, xw1)
-    narrow.distance_toi(kind[sel], idx[sel], xw, xw1, floor_frac=1.0 - cfg.alpha)
-    t_pair = (time.perf_counter() - t0) / max(ns, 1)
-    t0 = time.perf_counter()
-    narrow.partial_ccd(kind[sel], idx[sel], xw, xw1, cfg.samples)
-    t_partial = (time.perf_counter() - t0) / max(ns, 1)
+    with _one_thread():
+        st = o.state
+        cfg = o.cfg
+        t0 = time.perf_counter()
+        z = st.x + cfg.h * st.x_dot + (cfg.h * cfg.h) * (o.gravity_force + st.delta_f) / o.mesh.vertex_mass[:, None]
+        pins = st.x[o.mesh.pinned]
+        z[o.mesh.pinned] = pins
+        b, _ = solver.assemble_rhs(o.sys, o.mesh, o.el, z, z, pins)
+        solver.warmstart_correction(o.sub, o.sys, b, z[o.mesh.free])
+        t_ws = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rep = {"timings": {k: 0.0 for k in ("local", "global", "smoothing")}}
+        o.inner_solve(z, st.x.copy(), pins, None, rep)
+        t_lg = time.perf_counter() - t0
+        xw = o.world(st.x)
+        xw1 = xw + 1e-4
+        tris = o.topo.triangles
+        m = max(1, len(tris) // band)
+        sub = WorldTopology.build(tris[:m], o.topo.tri_static[:m])
+        t0 = time.perf_counter()
+        kind, idx = broad_phase(xw, xw1, sub, cfg.d_hat)
+        t_bp_sub = time.perf_counter() - t0
+        factor, _ = broad_calibration()
+        per_pair_bp = factor * t_bp_sub / max(len(kind), 1)
+        ns = min(len(kind), 20000)
+        sel = np.random.default_rng(0).choice(len(kind), ns, replace=False) if len(kind) > ns else np.arange(len(kind))
+        t0 = time.perf_counter()
+        narrow.full_ccd(kind[sel], idx[sel], xw, xw1)
+        narrow.distance_toi(kind[sel], idx[sel], xw, xw1, floor_frac=1.0 - cfg.alpha)
+        t_pair = (time.perf_counter() - t0) / max(ns, 1)
+        t0 = time.perf_counter()
+        narrow.partial_ccd(kind[sel], idx[sel], xw, xw1, cfg.samples)
+        t_partial = (time.perf_counter() - t0) / max(ns, 1)
     pairs = counts.get("pairs") or float(len(kind)) * len(tris) / m
-    try:  # BLAS stages (warm-start projection, cubic fits) use OpenBLAS's thread pool
-        from threadpoolctl import threadpool_info
-
-        blas = max([i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
-    except Exception:  # noqa: BLE001
-        blas = 1
     per_step = (t_ws * counts["ws_iters"] + counts["lg"] * (t_lg + pairs * t_partial)
                 + counts["sites"] * pairs * (per_pair_bp + t_pair))
-    sample = (f"oracle numpy port (reference algorithm; elementwise numpy single-threaded, BLAS on {blas} "
-              f"threads): warm-start iteration {t_ws:.2f}s and LG "
+    sample = (f"reference algorithm (oracle numpy port), 1 host thread: warm-start iteration {t_ws:.2f}s and LG "
               f"iteration {t_lg:.2f}s on the full mesh; broad phase on 1/{band} of the triangles {t_bp_sub:.2f}s "
-              f"({len(kind)} pairs, {per_pair_bp * 1e6:.2f}us/pair); full CCD + march {t_pair * 1e6:.1f}us/pair "
+              f"({len(kind)} pairs) x {factor:.3f} (reference patch-BVH / port time, profiles/broad_calibration.json)"
+              f" = {per_pair_bp * 1e6:.2f}us/pair; full CCD + march {t_pair * 1e6:.1f}us/pair "
               f"and partial CCD {t_partial * 1e6:.1f}us/pair on {ns} pairs; scaled by the GPU run's per-step "
               f"counts (ws {counts['ws_iters']:.1f}, LG {counts['lg']:.1f}, sites {counts['sites']:.1f}, "
-              f"pairs/site {pairs:.0f})")
-    return per_step, sample, blas
+              f"pairs/site {pairs:.0f}); an estimate, not a timed full step")
+    return per_step, sample, 1
+
+
+def config1_timed(steps: int = 5):
+    """BASELINE config 1 (64^2 two-corner pin, h = 1/200) stepped end to end by the
+    reference algorithm on one host thread: a measured, not extrapolated, CPU
+    number beside the GPU's own config-1 step time."""
+    from paper_2403_19272_b200 import StepConfig
+    from paper_2403_19272_b200.scenes import scene_parts
+    from oracle.stepper import OracleSimulation
+
+    cfg = StepConfig(h=1.0 / 200.0)
+    with _one_thread():
+        o = OracleSimulation.from_parts(scene_parts("two_corner", resolution=64, config=cfg), cfg)
+        o.step()                                    # first step (allocations)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            o.step()
+        per = (time.perf_counter() - t0) / steps
+    return {"workload": "config 1: 64^2 cloth pinned at two corners, h=1/200 (full steps, timed)",
+            "cpu_s_per_step": per, "cpu_steps": steps, "cpu_threads": 1, "kind": "port"}
+
+
+def gpu_config1(steps: int = 20):
+    """Our device step time on config 1 (CUDA events), for the config-1 comparison."""
+    import torch
+
+    import paper_2403_19272_b200 as P
+
+    sim = P.build_scene("two_corner", resolution=64, config=P.StepConfig(h=1.0 / 200.0))
+    for _ in range(3):
+        sim.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s = torch.cuda.current_stream()
+    e0.record(s)
+    for _ in range(steps):
+        sim.step()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
 
 
 # ------------------------------------------------------------------ arms
@@ -274,29 +400,36 @@ def reference_oracle(args):
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the reference's CPU algorithm (oracle port) on the same workload."""
+    """--impl reference: the reference's CPU algorithm (oracle port) on the same workload,
+    one host thread; config-4 per-stage samples scaled by the trajectory's per-step
+    counts (profiles/skirt_counts.json, measured by the GPU arm), plus a timed
+    end-to-end run of config 1 reported beside it."""
     if rank != 0:
         return
     t_start = time.time()
     o, workload = reference_oracle(args)
-    # per-step counts of this workload's first steps: 1 warm-start iteration, 1 LG
-    # iteration, 3 CCD sites (the GPU arm reproduces the reference's trajectory
-    # step for step and reports the same counts); pairs per site are estimated from
-    # the sampled broad phase, scaled to the whole world
-    counts = {"ws_iters": 1.0, "lg": 1.0, "sites": 3.0, "pairs": None} if args.workload == "skirt" else \
-        {"ws_iters": 1.0, "lg": 2.0, "sites": 3.0, "pairs": None}
+    counts = {"ws_iters": 1.0, "lg": 2.0, "sites": 3.0, "pairs": None}
+    if args.workload == "skirt":
+        try:
+            with open(os.path.join(ROOT, "profiles", "skirt_counts.json")) as fh:
+                c = json.load(fh)
+            counts = {k: float(c[k]) for k in ("ws_iters", "lg", "sites", "pairs")}
+        except (OSError, KeyError, ValueError):
+            counts = {"ws_iters": 1.0, "lg": 1.0, "sites": 3.0, "pairs": None}
     per_steps = []
     sample = ""
     for _ in range(max(1, min(args.steps, 2))):
-        per, sample, blas = cpu_oracle_estimate(o, counts)
+        per, sample, cores = cpu_oracle_estimate(o, counts)
         per_steps.append(per)
     per = float(np.median(per_steps))
     fps = 1.0 / per
-    line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "FPS", "n_gpus": args.gpus,
+    c1 = config1_timed()
+    line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "FPS", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": fps / PAPER_FPS, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload},
-            "cpu_baseline": {"value": fps, "unit": "FPS", "cores": blas, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": fps, "unit": "FPS", "cores": cores, "kind": "port", "sample": sample,
+                             "config1_timed": c1},
             "e2e": {"value": fps, "unit": "FPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.time() - t_start}
     print(json.dumps(line), flush=True)
@@ -420,33 +553,72 @@ def run_ours(args, ws, rank, local):
                "d2h_bytes_per_step": int(d2h), "steps": k_e2e,
                "replay": "the timed steps replayed from a state snapshot (same work as `value`)"}
 
-    # penetration-free invariant (untimed): further steps in verify mode, where cs_step
-    # runs the device intersection check on every new state (reference stepper.py:614-621)
+    # penetration-free invariant (untimed): the SAME K timed steps replayed a third time
+    # from the snapshot (the step is bitwise deterministic, tests/test_gpu_step.py::
+    # test_determinism) in verify mode, where cs_step runs the device intersection check
+    # on every new state before committing it (reference stepper.py:614-621)
     pen = None
-    if args.verify_steps > 0:
+    if not args.no_verify and snap is not None:
         import dataclasses
 
         from paper_2403_19272_b200 import PenetrationError
 
-        bad_steps, checked = 0, 0
-        for s in sims[:2]:
+        for s, (st, ob) in zip(sims, snap):
+            s.state = st
+            s.obstacle_x = ob
             s.config = dataclasses.replace(s.config, verify=True)
-            for _ in range(args.verify_steps):
+        bad_steps = checked = 0
+        for _ in range(args.steps):
+            for s in sims:
                 try:
                     s.step()
+                    checked += 1
                 except PenetrationError:
                     bad_steps += 1
-                    break
-                checked += 1
+        for s in sims:
             s.config = dataclasses.replace(s.config, verify=False)
         torch.cuda.synchronize()
         ta = time.perf_counter()
         n_pairs = len(sims[0].intersecting_pairs())
         t_check = time.perf_counter() - ta
-        pen = {"verified_steps": checked, "steps_with_intersections": bad_steps,
+        pen = {"verified_steps": checked // len(sims), "steps": args.steps, "scenes": len(sims),
+               "scene_steps_verified": checked, "steps_with_intersections": bad_steps,
                "intersecting_pairs_final": n_pairs, "device_check_ms": round(1e3 * t_check, 2),
-               "check": "all non-adjacent world-triangle pairs, 17-axis SAT (reference oracles.py:83-131)"}
+               "check": "every timed step replayed (bitwise-deterministic) with the device check of all "
+                        "non-adjacent world-triangle pairs, 17-axis SAT (reference oracles.py:83-131)"}
 
+    # the paper's solver regime (untimed by the headline): same skirt, same snapshot, the
+    # reference's iteration-cap mode with eps_inner 1e-9, cap 67 LG
+    # iterations per step (the paper's fashion show)
+    paper = None
+    if not args.no_paper_regime and snap is not None and args.workload == "skirt" and rank == 0:
+        import dataclasses
+
+        s0 = sims[0]
+        st, ob = snap[0]
+        s0.state = st
+        s0.obstacle_x = ob
+        base_cfg = s0.config
+        s0.config = dataclasses.replace(base_cfg, eps_inner=1e-9, iteration_cap=67)
+        preps = []
+        torch.cuda.synchronize()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(2):
+            preps.append(s0.step())
+        q1.record(stream)
+        torch.cuda.synchronize()
+        s0.config = base_cfg
+        ms = q0.elapsed_time(q1) / len(preps)
+        lgp = float(np.mean([r.lg_iterations for r in preps]))
+        paper = {"config": "StepConfig(eps_inner=1e-9, iteration_cap=67), same snapshot", "steps": len(preps),
+                 "ms_per_step": ms, "fps": 1e3 / ms, "lg_iterations_per_step": lgp,
+                 "ms_per_lg_iteration": ms / max(lgp, 1.0), "paper_fps": PAPER_FPS,
+                 "stages_ms_per_frame": {k: float(np.mean([r.timings[k] for r in preps]))
+                                         for k in ("warm_start", "local", "global", "smoothing", "broad",
+                                                   "narrow_partial", "narrow_full", "rf")}}
+
+    census = rank_census(ws, rank, local)
     if rank != 0:
         return
     # per-stage ms/frame and counters
@@ -482,12 +654,17 @@ def run_ours(args, ws, rank, local):
     if not args.no_cpu_baseline and ws == 1:
         from oracle.stepper import OracleSimulation
 
-        per, sample, blas = cpu_oracle_estimate(OracleSimulation.from_simulation(sim0),
-                                                {"ws_iters": ws_iters, "lg": lg, "sites": sites, "pairs": pairs})
-        cpu = {"value": 1.0 / per, "unit": "FPS", "cores": blas, "kind": "port", "sample": sample}
+        per, sample, cores = cpu_oracle_estimate(OracleSimulation.from_simulation(sim0),
+                                                 {"ws_iters": ws_iters, "lg": lg, "sites": sites, "pairs": pairs})
+        c1 = config1_timed()
+        c1["gpu_ms_per_step"] = gpu_config1()
+        c1["speedup"] = c1["cpu_s_per_step"] * 1e3 / c1["gpu_ms_per_step"]
+        cpu = {"value": 1.0 / per, "unit": "FPS", "cores": cores, "kind": "port", "sample": sample,
+               "config1_timed": c1}
     line = {
         "metric": METRIC, "value": value, "unit": "FPS", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * dev_s / args.steps / len(sims), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * dev_s / args.steps / len(sims), "higher_is_better": True,
+        "scaling": "weak",
         "vs_baseline": value / PAPER_FPS if args.workload == "skirt" else None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload, "n_vertices": int(sim0.mesh.vertex_count), "n_free": int(nf),
@@ -507,14 +684,22 @@ def run_ours(args, ws, rank, local):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "penetration_free": pen,
+        "paper_regime": paper,
+        "ranks": census,
+        "process_group": process_group_info(ws),
     }
     print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
+    maybe_spawn(args)
     ws, rank, local = dist_setup()
-    if args.impl == "reference":
+    if args.workload is None:
+        args.workload = "skirt" if ws == 1 else "batch"
+    if args.dry_run:
+        run_dry(args, ws, rank, local)
+    elif args.impl == "reference":
         run_reference(args, ws, rank)
     else:
         run_ours(args, ws, rank, local)

@@ -167,8 +167,9 @@ def simulate(cfg: SceneConfig, steps=None, verify=False, barrier=None, iteration
                     rep = sim.step()
                 except PenetrationError as exc:
                     dump = out / f"state_dump_{step:06d}.obj"
-                    x = exc.state_dump["x"] if exc.state_dump and "x" in exc.state_dump else sim.state.x
-                    frames.fmt.write(dump, x)
+                    # the last good state, as the reference CLI dumps it (cli.py:81-86); the
+                    # failing candidate stays in exc.state_dump["x"]
+                    frames.fmt.write(dump, sim.state.x)
                     print(f"invariant breach at step {step}: {exc}; state dump: {dump}", file=sys.stderr)
                     return 2
                 writer.writerow(metrics_row(step, rep))

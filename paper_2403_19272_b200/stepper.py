@@ -14,6 +14,7 @@ mirror; in-place edits of that mirror (reference tests do
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import time
 
@@ -37,8 +38,17 @@ def _rms(v: np.ndarray) -> float:
 
 
 class _Tracked(np.ndarray):
-    """ndarray that records writes through item assignment (``a[...] = v``, also on
-    views) so only modified state fields are written back to the device."""
+    """ndarray view of a downloaded state field that records writes, so only modified
+    fields are written back to the device.
+
+    The field is handed out READ-ONLY at the numpy level; the writers numpy routes
+    through the subclass (item assignment, in-place / ``out=`` ufuncs incl.
+    ``np.add.at``, ``np.copyto`` / ``np.put`` / ``np.place`` / ``np.putmask``,
+    ``.fill`` / ``.put`` / ``.sort``) open it for the write and mark the field
+    dirty.  Any other write path (e.g. through ``np.asarray(field)``) raises
+    "assignment destination is read-only" instead of being silently lost."""
+
+    _WRITERS = ("copyto", "put", "place", "putmask", "fill_diagonal")
 
     # views keep a reference to the root array (never to themselves: a self-cycle would
     # leave the array to the cyclic GC and delay recycling its pinned buffer)
@@ -49,22 +59,65 @@ class _Tracked(np.ndarray):
             self._root = None
         self._dirty = False
 
+    @classmethod
+    def wrap(cls, a: np.ndarray) -> "_Tracked":
+        t = a.view(cls)
+        t._dirty = False
+        t.flags.writeable = False
+        return t
+
     def _mark(self):
         (self._root if self._root is not None else self)._dirty = True
 
-    def __setitem__(self, key, value):
+    @contextlib.contextmanager
+    def _open(self):
+        """Root and this view writeable for one write; yields a plain ndarray view."""
+        root = self._root if self._root is not None else self
         self._mark()
-        super().__setitem__(key, value)
+        prev = root.flags.writeable
+        root.flags.writeable = True
+        own = self is not root and not self.flags.writeable
+        if own:
+            self.flags.writeable = True
+        try:
+            yield self.view(np.ndarray)
+        finally:
+            if own:
+                self.flags.writeable = False
+            root.flags.writeable = prev
+
+    def __setitem__(self, key, value):
+        with self._open() as w:
+            w[key] = value
+
+    def fill(self, value):
+        with self._open() as w:
+            w.fill(value)
+
+    def put(self, *args, **kw):
+        with self._open() as w:
+            w.put(*args, **kw)
+
+    def sort(self, *args, **kw):
+        with self._open() as w:
+            w.sort(*args, **kw)
 
     def __array_ufunc__(self, ufunc, method, *inputs, out=None, **kw):
-        # arithmetic yields plain arrays; in-place ufuncs (out=state field) mark dirty
-        plain = tuple(np.asarray(a) if isinstance(a, _Tracked) else a for a in inputs)
-        if out is not None:
-            for o in out:
-                if isinstance(o, _Tracked):
-                    o._mark()
-            kw["out"] = tuple(np.asarray(o) if isinstance(o, _Tracked) else o for o in out)
-        return getattr(ufunc, method)(*plain, **kw)
+        # arithmetic yields plain arrays; in-place ufuncs (out= / ufunc.at on a state
+        # field) write through an opened view and mark the field dirty
+        plain = tuple(a.view(np.ndarray) if isinstance(a, _Tracked) else a for a in inputs)
+        with contextlib.ExitStack() as stack:
+            if method == "at" and isinstance(inputs[0], _Tracked):
+                plain = (stack.enter_context(inputs[0]._open()),) + plain[1:]
+            if out is not None:
+                kw["out"] = tuple(stack.enter_context(o._open()) if isinstance(o, _Tracked) else o for o in out)
+            return getattr(ufunc, method)(*plain, **kw)
+
+    def __array_function__(self, func, types, args, kwargs):
+        if func.__name__ in self._WRITERS and args and isinstance(args[0], _Tracked):
+            with args[0]._open() as w:
+                return func(w, *args[1:], **kwargs)
+        return super().__array_function__(func, types, args, kwargs)
 
 
 class DeviceSimState:
@@ -83,8 +136,7 @@ class DeviceSimState:
         def get(self):
             a = self._cache.get(name)
             if a is None:
-                a = self._cache[name] = self._sim._download(name).view(_Tracked)
-                a._dirty = False
+                a = self._cache[name] = _Tracked.wrap(self._sim._download(name))
             return a
 
         def put(self, value):
@@ -177,6 +229,20 @@ class Simulation:
             self._lib.cs_scene_destroy(scene)
             self._scene = None
 
+    @property
+    def config(self) -> StepConfig:
+        return self._config
+
+    @config.setter
+    def config(self, cfg: StepConfig) -> None:
+        """Replacing the config takes effect at the next step, as in the reference (which
+        reads self.config inside step()); k / kappa stay as resolved at construction
+        (stepper.py:164-169)."""
+        self._config = cfg
+        if getattr(self, "_scene", None):
+            self._cfg_c = step_config_c(cfg, self.k, self.kappa)
+            _lib.check(self._lib.cs_scene_set_config(self._scene, ctypes.byref(self._cfg_c)), "cs_scene_set_config")
+
     # ------------------------------------------------------------ state mirror
     def _stream(self):
         return _lib.stream_handle()
@@ -197,11 +263,14 @@ class Simulation:
             a = np.ascontiguousarray(np.asarray(st._cache[name]), dtype=np.float64)
             keep.append(a)
             ptrs.append(a.ctypes.data)
-        o = np.ascontiguousarray(obs, dtype=np.float64) if (obs is not None and self._n_obs and self._obs_dirty) else None
+        obs_dirty = self._obs_dirty or (isinstance(obs, _Tracked) and obs._dirty)
+        o = np.ascontiguousarray(obs, dtype=np.float64) if (obs is not None and self._n_obs and obs_dirty) else None
         step = int(st.step_index) if st is not None else -1
         _lib.check(self._lib.cs_set_state(self._scene, *ptrs, o.ctypes.data if o is not None else None, step,
                                           self._stream()), "cs_set_state")
         self._obs_dirty = False
+        if isinstance(obs, _Tracked):
+            obs._dirty = False
         if st is not None:
             self._step_index = step
             for name in DeviceSimState.FIELDS:
@@ -254,7 +323,7 @@ class Simulation:
     @property
     def obstacle_x(self) -> np.ndarray:
         if self._host_obstacles is None:
-            self._host_obstacles = self._download("obstacle_x")
+            self._host_obstacles = _Tracked.wrap(self._download("obstacle_x"))
         return self._host_obstacles
 
     @obstacle_x.setter
@@ -288,6 +357,11 @@ class Simulation:
         pins = self._pin_targets(t_now + cfg.h)
         obs = self._obstacle_targets(t_now + cfg.h)
         rep = _lib.StepReportC()
+        # host-oracle verify mode checks after the device step: keep the state to roll
+        # back to (the reference raises before `self.state = new_state`)
+        host_verify = bool(cfg.verify and self._verify_oracle is not None)
+        if host_verify:
+            saved = (self.host_state(), np.array(self.obstacle_x, copy=True), self._step_index)
         # verify mode without an injected host oracle: the device intersection check
         # (csrc/intersect.cu, reference oracles.py:83-131) runs inside cs_step on x_final
         device_verify = bool(cfg.verify and self._verify_oracle is None)
@@ -324,14 +398,19 @@ class Simulation:
                      "narrow_full": rep.t_narrow_full, "rf": rep.t_rf})
         if device_verify:
             report.penetration_free = True
-        elif cfg.verify and self._verify_oracle is not None:
-            st = self.state
-            xw = self.world(st.x)
+        elif host_verify:
+            x_final = np.array(self.state.x, copy=True)
+            xw = self.world(x_final)
             bad = self._verify_oracle(xw, self.bvh.triangles)
             report.penetration_free = len(bad) == 0
             if not report.penetration_free:
-                raise PenetrationError(f"step {self._step_index - 1}: {len(bad)} intersecting triangle pairs",
-                                       state_dump={"x": st.x, "pairs": bad})
+                st, obs, idx = saved
+                self.state = st
+                self.obstacle_x = obs
+                self._flush()
+                self._step_index = idx
+                raise PenetrationError(f"step {idx}: {len(bad)} intersecting triangle pairs",
+                                       state_dump={"x": x_final, "pairs": bad})
         return report
 
     def run(self, steps: int, on_step=None) -> list:

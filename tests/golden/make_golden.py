@@ -177,17 +177,54 @@ def dbb_fixture(steps=18):
     traj_fixture("sphere14_dbb", "sphere_drape", steps, {"barrier_mode": "dbb"}, resolution=14, size=0.2)
 
 
-def two_corner_fixture(steps=3):
+def two_corner_fixture(steps=20):
     """BASELINE config 1: 64x64 grid pinned at two corners, h = 1/200."""
     v, t = grid_cloth(64, 1.0)
     mesh = clothsim.build_mesh(v, t, 0.3, pins=[0, 63])
     sim = clothsim.Simulation(mesh, clothsim.StepConfig(h=1.0 / 200.0))
-    xs, lg = [], []
+    xs, lg, outer, sites = [], [], [], []
     for _ in range(steps):
         r = sim.step()
         xs.append(sim.state.x.copy())
         lg.append(r.lg_iterations)
-    save("traj_two_corner64.npz", x=np.stack(xs), lg=np.array(lg))
+        outer.append(r.outer_loops)
+        sites.append(r.full_ccd_calls)
+    save("traj_two_corner64.npz", x=np.stack(xs), lg=np.array(lg), outer=np.array(outer), sites=np.array(sites),
+         x_dot=sim.state.x_dot)
+
+
+def sphere_ground_fixture(steps=14, keep=6):
+    """BASELINE config 2: 128x128 cloth dropped onto a sphere (r 0.25) above a ground slab,
+    h = 1/200, run by the reference.  Positions of the last `keep` steps (the first
+    contact steps) + counters of every step: a test rebuilds the full state before step s
+    from them (x_prev = x[s-1], x_dot = (x[s] - x[s-1]) / h, delta_f stored when nonzero)
+    and teacher-forces the GPU step against x[s+1]."""
+    from clothsim.scenes import box_mesh
+
+    cfg = clothsim.StepConfig(h=1.0 / 200.0)
+    v, t = grid_cloth(128, 1.0, height=0.25 + 2.0 * cfg.d_hat + 0.01)
+    v[:, :2] -= 0.5
+    mesh = clothsim.build_mesh(v, t, 0.3, pins=[])
+    obstacles = [icosphere(3, 0.25), box_mesh(center=(0.0, 0.0, -(0.25 + 0.005 + 0.01)), extents=(2.0, 2.0, 0.02),
+                                              divisions=4)]
+    sim = clothsim.Simulation(mesh, cfg, obstacles=obstacles)
+    xs, dfs, lg, outer, rf, toi, act = [], [], [], [], [], [], []
+    for _ in range(steps):
+        r = sim.step()
+        xs.append(sim.state.x.copy())
+        dfs.append(sim.state.delta_f.copy())
+        lg.append(r.lg_iterations)
+        outer.append(r.outer_loops)
+        rf.append(r.rf_triggered)
+        toi.append(r.toi_exit)
+        act.append(r.active_pairs)
+        print("step", len(xs), r.lg_iterations, r.outer_loops, r.rf_triggered, r.toi_exit, r.active_pairs, flush=True)
+    first = steps - keep
+    df = np.stack(dfs[first:])
+    save("traj_sphere_ground128.npz", x=np.stack(xs[first:]), first=np.array(first), h=np.array(cfg.h),
+         df_nonzero=np.array([bool(np.any(d)) for d in df]), delta_f=df[[bool(np.any(d)) for d in df]],
+         lg=np.array(lg), outer=np.array(outer), rf=np.array(rf), toi=np.array(toi), active=np.array(act),
+         obstacle_x=sim.obstacle_x)
 
 
 def io_fixture():
@@ -237,6 +274,7 @@ if __name__ == "__main__":
     traj_fixture("sphere14", "sphere_drape", 12, {}, resolution=14, size=0.2)
     traj_fixture("twist10", "twist", 6, {}, resolution=10, size=0.3)
     two_corner_fixture()
+    sphere_ground_fixture()
     contact_state_fixture()
     dbb_fixture()
     io_fixture()

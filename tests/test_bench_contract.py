@@ -20,3 +20,19 @@ def test_reference_arm_json_line():
     assert line["value"] > 0 and line["unit"] == "FPS" and line["higher_is_better"] is True
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_multi_rank_plumbing_dry_run():
+    """`bench.py --gpus 2` outside torchrun spawns two ranks itself (gloo on CPU here):
+    the line reports n_gpus == 2 and two distinct processes; no device work."""
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run", "--steps", "1", "--warmup", "0"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["dry_run"] is True and line["n_gpus"] == 2
+    assert sorted(r["rank"] for r in line["ranks"]) == [0, 1]
+    assert len({r["pid"] for r in line["ranks"]}) == 2
+    assert line["process_group"]["world_size"] == 2 and line["process_group"]["backend"] == "gloo"
+    assert line["workload"] == "batch"          # N > 1 defaults to the config-5 scene batch

@@ -401,3 +401,54 @@ def test_dbb_free_running_close(cuda):
         r = sim.step()
         assert r.lg_iterations == g["lg"][s], s
         assert np.abs(sim.state.x - g["x"][s]).max() <= 1e-8, s
+
+
+def test_two_corner64_vs_reference(cuda):
+    """BASELINE config 1 at its stated size (64^2, pinned at two corners, h = 1/200)
+    against the reference's own 20-step run (tests/golden/traj_two_corner64.npz):
+    free running, every step's positions and counters."""
+    import paper_2403_19272_b200 as P
+    from conftest import golden
+
+    g = golden("traj_two_corner64.npz")
+    sim = P.build_scene("two_corner", resolution=64, config=P.StepConfig(h=1.0 / 200.0))
+    for s in range(len(g["x"])):
+        r = sim.step()
+        assert r.lg_iterations == g["lg"][s], s
+        assert r.outer_loops == g["outer"][s], s
+        assert r.full_ccd_calls == g["sites"][s], s
+        assert np.abs(sim.state.x - g["x"][s]).max() <= 1e-9, s
+    assert np.abs(sim.state.x_dot - g["x_dot"]).max() <= 1e-6
+
+
+def test_sphere_ground128_contact_vs_reference(cuda):
+    """BASELINE config 2 at its stated size (128^2 cloth onto a sphere above a ground
+    slab) against the reference's own run (tests/golden/traj_sphere_ground128.npz):
+    the first contact steps, teacher forced from the reference's state, must land on
+    the reference's next state with identical counters and line-search TOI."""
+    import paper_2403_19272_b200 as P
+    from conftest import golden
+
+    g = golden("traj_sphere_ground128.npz")
+    h = float(g["h"])
+    first = int(g["first"])
+    xs = g["x"]
+    df = np.zeros_like(xs)
+    df[g["df_nonzero"]] = g["delta_f"]
+    sim = P.build_scene("sphere_ground", resolution=128, size=1.0, config=P.StepConfig(h=h))
+    obstacles = sim.obstacle_x.copy()
+    contact = 0
+    for j in range(1, len(xs) - 1):
+        k = first + j + 1                      # steps taken before this one
+        sim.state = P.SimState(x=xs[j], x_dot=(xs[j] - xs[j - 1]) / h, x_prev=xs[j - 1], delta_f=df[j],
+                               step_index=k)
+        sim.obstacle_x = obstacles
+        r = sim.step()
+        contact = max(contact, r.active_pairs)
+        assert r.active_pairs == g["active"][k], k
+        assert r.lg_iterations == g["lg"][k], k
+        assert r.outer_loops == g["outer"][k], k
+        assert r.rf_triggered == bool(g["rf"][k]), k
+        assert abs(r.toi_exit - g["toi"][k]) <= 1e-9 * g["toi"][k] + 1e-15, k
+        assert np.abs(sim.state.x - xs[j + 1]).max() <= 1e-9, k
+    assert contact > 0

@@ -51,3 +51,29 @@ def test_inplace_ufunc_marks_dirty():
     assert st.dirty("x_dot")
     np.add(st.x_prev, 1.0, out=st.x_prev)
     assert st.dirty("x_prev")
+
+
+def test_every_write_path_is_tracked_or_loud():
+    """np.copyto / .fill / np.add.at / np.put reach the device; a write
+    through an untracked plain view raises instead of being silently lost."""
+    import pytest
+
+    sim = _FakeSim()
+    st = DeviceSimState(sim)
+    np.copyto(st.x, np.zeros((5, 3)))
+    assert st.dirty("x") and not st.x.any()
+    st.x_dot.fill(2.0)
+    assert st.dirty("x_dot") and (st.x_dot == 2.0).all()
+    np.add.at(st.delta_f, [0, 0], 1.0)
+    assert st.dirty("delta_f")
+    np.put(st.x_prev, [0], 9.0)
+    assert st.dirty("x_prev") and st.x_prev[0, 0] == 9.0
+    fresh = DeviceSimState(sim)
+    with pytest.raises(ValueError, match="read-only"):
+        np.asarray(fresh.x)[0] = 1.0
+    assert not fresh.dirty("x")
+    row = fresh.x[2]                                      # a view taken before the write
+    row[1] = 4.0
+    assert fresh.dirty("x") and fresh.x[2, 1] == 4.0
+    y = fresh.x_dot.copy()                                # copies are writeable
+    y[0] = 1.0
