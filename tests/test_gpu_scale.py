@@ -113,11 +113,13 @@ def test_skirt584_ccd_site_bitwise(skirt584, site584):
     kind, idx = pairs.kind, pairs.idx
     _, _, _, dist0 = P.pair_witness(kind, idx, xw0)
     near = np.flatnonzero(_reachable(kind, idx, xw0, xw1, dist0, sim.config.d_hat))
-    rng = np.random.default_rng(584)
-    sample = rng.choice(len(kind), SAMPLE, replace=False)
-    sel = np.union1d(near, sample)
     hits = np.flatnonzero(~np.isnan(toi) | ~np.isnan(filt))
-    assert np.isin(hits, sel).all(), "a device hit outside the reachable set"
+    assert np.isin(hits, near).all(), "a device hit outside the reachable set"
+    # every device hit, 1.5 M of the reachable pairs (where a wrongly filtered pair would
+    # hide) and 0.5 M of all pairs
+    rng = np.random.default_rng(584)
+    sel = np.union1d(np.union1d(hits, rng.choice(near, min(len(near), 1_500_000), replace=False)),
+                     rng.choice(len(kind), SAMPLE // 2, replace=False))
     for sl in _chunks(len(sel)):
         s = sel[sl]
         e_toi = ON.full_ccd(kind[s], idx[s], xw0, xw1)
@@ -128,17 +130,27 @@ def test_skirt584_ccd_site_bitwise(skirt584, site584):
 
 
 def test_skirt584_partial_ccd_and_witness_bitwise(skirt584, site584):
+    """partial_ccd over the site's pairs for the real step motion and for a 1 mm
+    random perturbation of it (which flips many pair offsets, so the active set is
+    large); every device-active pair (up to 500 K) + a 1 M random sample vs the oracle."""
     import paper_2403_19272_b200 as P
 
     sim, ref, xw0, xw1 = skirt584
     pairs, _, _ = site584
     rng = np.random.default_rng(5840)
+    samples = P.default_samples(sim.config.samples)
+    xw1p = xw1 + rng.uniform(-1e-3, 1e-3, xw1.shape)
+    n_active = 0
+    for xe in (xw1, xw1p):
+        got_all = P.partial_ccd(pairs.kind, pairs.idx, xw0, xe, samples)
+        act = np.flatnonzero(got_all)
+        n_active = max(n_active, len(act))
+        s = np.union1d(act[rng.permutation(len(act))[:500_000]], rng.choice(len(pairs), SAMPLE, replace=False))
+        exp = ON.partial_ccd(pairs.kind[s], pairs.idx[s], xw0, xe, sim.config.samples)
+        np.testing.assert_array_equal(got_all[s], exp)
+    assert n_active > 10_000, n_active
     s = np.sort(rng.choice(len(pairs), SAMPLE, replace=False))
     kind, idx = pairs.kind[s], pairs.idx[s]
-    got = P.partial_ccd(kind, idx, xw0, xw1, P.default_samples(sim.config.samples))
-    exp = ON.partial_ccd(kind, idx, xw0, xw1, sim.config.samples)
-    np.testing.assert_array_equal(got, exp)
-    assert got.any() and not got.all()
     for got_w, exp_w in zip(P.pair_witness(kind, idx, xw1), ON.witness(kind, idx, xw1)):
         np.testing.assert_array_equal(got_w, exp_w)
 
@@ -154,7 +166,7 @@ def test_skirt_band_step_teacher_forced(cuda):
     sim = S.skirt_scene(P.StepConfig(h=1.0 / 200.0), around=584, down=down, length=0.6 * (down - 1) / 583)
     for _ in range(3):
         sim.step()
-    for _ in range(2):
+    for _ in range(1):
         ref = OracleSimulation.from_simulation(sim)
         r = sim.step()
         rr = ref.step()

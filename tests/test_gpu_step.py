@@ -244,24 +244,32 @@ def test_subset_sites_are_exact(cuda, monkeypatch, kind, kw, steps):
 
 
 def test_subset_sites_verified_across_outer_loops(cuda, monkeypatch):
-    """Contact steps with several outer loops: the 2nd and later outer-loop sites of a
-    step still take the subset path after the first one was verified, and are verified
-    too (a verification broad phase must not invalidate the step's base site)."""
+    """Contact steps with two outer loops (BASELINE config 2, the reference's own steps 11
+    and 12 of tests/golden/traj_sphere_ground128.npz): the 2nd outer-loop site of a step
+    still takes the subset path after the first one was verified, and is verified too
+    (a verification broad phase must not invalidate the step's base site)."""
     import paper_2403_19272_b200 as P
     from conftest import golden
 
     monkeypatch.setenv("CS_VERIFY_STATIC_SITE", "1")
-    g = golden("contact_sphere14.npz")
-    sim = P.build_scene("sphere_drape", resolution=14, size=0.2, config=P.StepConfig())
+    g = golden("traj_sphere_ground128.npz")
+    h, first, xs = float(g["h"]), int(g["first"]), g["x"]
+    df = np.zeros_like(xs)
+    df[g["df_nonzero"]] = g["delta_f"]
+    sim = P.build_scene("sphere_ground", resolution=128, size=1.0, config=P.StepConfig(h=h))
+    obstacles = sim.obstacle_x.copy()
     best = 0
-    for s in range(12, 24):
-        sim.state = P.SimState(x=g["x"][s], x_dot=g["x_dot"][s], x_prev=g["x_prev"][s], delta_f=g["delta_f"][s],
-                               step_index=s)
-        sim.obstacle_x = g["obstacle_x"][s]
-        sim.step()
+    for j in range(1, len(xs) - 1):
+        k = first + j + 1
+        sim.state = P.SimState(x=xs[j], x_dot=(xs[j] - xs[j - 1]) / h, x_prev=xs[j - 1], delta_f=df[j],
+                               step_index=k)
+        sim.obstacle_x = obstacles
+        r = sim.step()
         c = sim.last_report_c
+        assert r.outer_loops == g["outer"][k]
         assert c.verified_sites >= c.subset_sites + c.static_sites
         best = max(best, c.subset_sites)
+    assert max(g["outer"][first + 2:first + len(xs)]) >= 2
     assert best >= 2, "no step served more than one outer-loop site from its base"
 
 
