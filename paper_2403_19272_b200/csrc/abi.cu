@@ -1637,6 +1637,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         rep->n_outer_deltas = n_deltas;
         rep->gpu_launches = launches;
         CS_TRY(hsync());
+        rep->host_syncs = n_syncs;
         double acc[kStages] = {0};
         for (auto& sp : spans) {
             float ms = 0.f;

@@ -6,7 +6,7 @@
 set -u
 OUT=${OUT:-gpurun_out}
 mkdir -p "$OUT"
-ARGS=${ARGS:-"--steps 2 --warmup 1 --no-cpu-baseline --no-e2e --verify-steps 0"}
+ARGS=${ARGS:-"--steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-verify --no-paper-regime"}
 ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:k_|Device|cub' --csv \
     --log-file "$OUT/launches.csv" python bench.py $ARGS > "$OUT/ncu_launches.log" 2>&1
 echo "launch list rc=$?"

@@ -460,3 +460,4 @@ def test_sphere_ground128_contact_vs_reference(cuda):
         assert abs(r.toi_exit - g["toi"][k]) <= 1e-9 * g["toi"][k] + 1e-15, k
         assert np.abs(sim.state.x - xs[j + 1]).max() <= 1e-9, k
     assert contact > 0
+
