@@ -52,6 +52,34 @@ namespace {
 // pair of a few hundred MB costs tens of ms).
 thread_local cudaStream_t t_alloc_stream = nullptr;
 
+// The library's own stream-ordered pool per device (cudaMemPoolCreate): freed blocks
+// stay mapped for the next regrowth, without touching the device's default pool that
+// PyTorch / CuPy / other cudaMallocAsync users of the process share.
+cudaMemPool_t lib_pool() {
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        unsigned long long keep = ~0ull;
+        cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    return pools[dev];
+}
+
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t st) {
+    cudaMemPool_t pool = lib_pool();
+    return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+}
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
@@ -69,7 +97,7 @@ struct DBuf {
         else if (!exact && want > (1u << 16)) want *= 3;
         static const bool trace = std::getenv("CS_TRACE_ALLOC") != nullptr;
         if (trace) std::fprintf(stderr, "[cs alloc] %zu -> %zu bytes\n", n * sizeof(T), want * sizeof(T));
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), want * sizeof(T), t_alloc_stream);
+        cudaError_t e = pool_alloc(reinterpret_cast<void**>(&p), want * sizeof(T), t_alloc_stream);
         if (e != cudaSuccess) {
             n = 0;
             p = nullptr;
@@ -1752,31 +1780,28 @@ long long cs_format_obj_vertices(const double* v, long long n, char* out, long l
 }
 
 cs_scene* cs_scene_create(const cs_scene_desc* desc, const cs_step_config* cfg, int* status) {
-    {
-        // keep freed blocks in the stream-ordered pool (DBuf regrowth reuses them)
+    if (desc) {
+        // map a slab into the library pool once per process and device, so pair-buffer
+        // regrowth under contact is served without mapping fresh memory: ~4 KB per world
+        // primitive (pair sets, grid tables, stamps at the bench's contact density),
+        // at most a quarter of the free memory; CS_POOL_RESERVE_GB overrides (0 = none)
+        static bool reserved[64] = {};
         int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            unsigned long long keep = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-            // map a slab into the pool once per process, so pair-buffer regrowth under
-            // contact is served without mapping fresh memory (CS_POOL_RESERVE_GB, default
-            // min(24 GB, a quarter of the free memory); 0 disables)
-            static bool reserved = false;
-            if (!reserved) {
-                reserved = true;
-                size_t free_b = 0, total_b = 0;
-                cudaMemGetInfo(&free_b, &total_b);
-                const char* env = std::getenv("CS_POOL_RESERVE_GB");
-                size_t want = env ? (size_t)(std::atof(env) * (1ull << 30))
-                                  : std::min<size_t>(24ull << 30, free_b / 4);
-                void* slab = nullptr;
-                if (want && cudaMallocAsync(&slab, want, nullptr) == cudaSuccess) {
-                    cudaFreeAsync(slab, nullptr);
-                    cudaStreamSynchronize(nullptr);
-                }
-                cudaGetLastError();
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool = lib_pool();
+        if (pool && dev >= 0 && dev < 64 && !reserved[dev]) {
+            reserved[dev] = true;
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            const char* env = std::getenv("CS_POOL_RESERVE_GB");
+            const size_t prims = (size_t)std::max(desc->n_world_tris, 0) + (size_t)std::max(desc->n_world_edges, 0);
+            size_t want = env ? (size_t)(std::atof(env) * (1ull << 30)) : std::min<size_t>(4096 * prims, free_b / 4);
+            void* slab = nullptr;
+            if (want && cudaMallocFromPoolAsync(&slab, want, pool, nullptr) == cudaSuccess) {
+                cudaFreeAsync(slab, nullptr);
+                cudaStreamSynchronize(nullptr);
             }
+            cudaGetLastError();
         }
     }
     t_alloc_stream = nullptr;
