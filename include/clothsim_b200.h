@@ -113,6 +113,19 @@ typedef struct {
 /* ---- scene lifetime ---------------------------------------------------- */
 /* replaces Simulation.__init__'s device-side state (stepper.py:127-173) */
 cs_scene *cs_scene_create(const cs_scene_desc *desc, const cs_step_config *cfg, int *status);
+/* A context holding only some parts of a scene, for the module-level stage functions
+ * that take the reference's setup objects rather than a Simulation
+ * (ajacobi_smooth(system, ...), reduced_correction(sub, system, ...),
+ * assemble_rhs(system, mesh, elastic, ...), broad_phase(x0, x1, bvh, margin);
+ * smoothing.py:23-78, subspace.py:165-192, constraints.py:229-256, bvh.py:207-292).
+ * Only the desc fields of the requested parts are read; stage entry points return
+ * CS_BAD_ARGUMENT on a context missing a part they need; cs_step needs CS_PART_ALL. */
+#define CS_PART_SYSTEM 1  /* H (SELL-32), diag: smoothing, residual */
+#define CS_PART_CLOTH 2   /* mesh + elastic + H_fp: rhs, collision terms, energy gradient (with SYSTEM) */
+#define CS_PART_BASIS 4   /* U, eigenvalues: reduced update / build (alone), corrections (with SYSTEM) */
+#define CS_PART_WORLD 8   /* world topology: broad phase, CCD site, intersections */
+#define CS_PART_ALL 15    /* every part + the state: a full scene */
+cs_scene *cs_scene_create_parts(const cs_scene_desc *desc, const cs_step_config *cfg, int parts, int *status);
 void cs_scene_destroy(cs_scene *scene);
 int cs_scene_set_config(cs_scene *scene, const cs_step_config *cfg);
 
@@ -165,10 +178,11 @@ int cs_scene_pairs(cs_scene *scene, int8_t *kind, int *idx4, void *stream);
 int cs_ccd_site(cs_scene *scene, const double *x_start_w, const double *x_end_w, long long *count, double *clamp,
                 void *stream);
 int cs_scene_pair_results(cs_scene *scene, double *toi, double *toi_filter, void *stream);
-/* assemble_rhs (constraints.py:229-256); coll_* (n_coll) are the flat
+/* assemble_rhs (constraints.py:229-256); pins (n_cloth*3, only the pinned rows are read)
+ * carries pinned_positions (NULL: the pinned rows of x); coll_* (n_coll) are the flat
  * (ids, weights, targets) of Simulation._collision_terms in order; ids are cloth ids. */
-int cs_assemble_rhs(cs_scene *scene, const double *z, const double *x, const int *coll_ids, const double *coll_w,
-                    const double *coll_t, int n_coll, double *b, double *delta, void *stream);
+int cs_assemble_rhs(cs_scene *scene, const double *z, const double *x, const double *pins, const int *coll_ids,
+                    const double *coll_w, const double *coll_t, int n_coll, double *b, double *delta, void *stream);
 /* Simulation._collision_terms (stepper.py:238-285): per engaged pair with weight > 0, its
  * movable cloth vertices' (ids, weights, targets) in pair-then-slot order; DEVICE arrays
  * (ids/w capacity 4P, targets 4P*3); count = entries written */
@@ -184,11 +198,41 @@ int cs_ajacobi_smooth(cs_scene *scene, const double *b, double *x, int iteration
 /* reduced_correction (subspace.py:165-186); reuse != 0 keeps the last reduced system */
 int cs_reduced_correction(cs_scene *scene, const double *b, double *x, const double *delta, int reuse,
                           void *stream);
+/* jacobi_step (smoothing.py:69-78): out = x + (1 - omega) D^-1 (b - (H + delta) x); delta may be NULL */
+int cs_jacobi_step(cs_scene *scene, const double *b, const double *x, double omega, const double *delta,
+                   double *out, void *stream);
+/* reduced_update (subspace.py:97-106): G (r*r) = sum_j weights[j] V_rows[j] V_rows[j]^T */
+int cs_reduced_update(cs_scene *scene, const int *rows, const double *weights, int m, double *G, void *stream);
+/* build_reduced (subspace.py:122-140): A = diag(lambda_r) + G (G may be NULL), beta = rhs_scale
+ * (1 if <= 0), inverse (r*r, DEVICE) with A inverse = I / beta, LU with the pinv fallback;
+ * beta / fallback HOST.  Becomes the context's current reduced system (reuse != 0 in
+ * cs_reduced_correction applies it). */
+int cs_build_reduced(cs_scene *scene, const double *G, double rhs_scale, double *inverse, double *beta,
+                     int *fallback, void *stream);
+/* the context's current reduced system: inverse (r*r, DEVICE), beta / fallback (HOST); any may be NULL */
+int cs_reduced_get(cs_scene *scene, double *inverse, double *beta, int *fallback, void *stream);
 /* warmstart_correction (subspace.py:189-192) */
 int cs_warmstart_correction(cs_scene *scene, const double *b, double *x, void *stream);
 /* Simulation.energy gradient (stepper.py:309-380, "quad" form); grad (n_cloth*3) */
 int cs_energy_gradient(cs_scene *scene, const double *x, const double *z, const int *q_ids, const double *q_w,
                        const double *q_t, int n_q, double *grad, void *stream);
+
+/* ---- scene-free module-level helpers (DEVICE pointers) -------------------- */
+/* tri_tri_intersect (oracles.py:33-48): p, q (m,3,3); out (m) 1 = closed triangles intersect */
+int cs_tri_tri_intersect(const double *p, const double *q, long long m, uint8_t *out, void *stream);
+/* coplanarity_coefficients (collision/ccd.py:36-44): coef (P,4), lowest order first */
+int cs_coplanarity_coefficients(const int8_t *kind, const int *idx4, const double *x_start, const double *x_end,
+                                long long P, double *coef, void *stream);
+/* query_q (collision/partial.py:133-146): lam (P,k,2), or (k,2) when shared != 0; out (P,k) */
+int cs_query_q(const int8_t *kind, const int *idx4, const double *x_start, const double *x_end, long long P,
+               const double *lam, int k, int shared, double *out, void *stream);
+/* swept_boxes (collision/bvh.py:140-143): points (m,k,3) at both ends -> lo, hi (m,3) */
+int cs_swept_boxes(const double *points_start, const double *points_end, long long m, int k, double margin,
+                   double *lo, double *hi, void *stream);
+/* dbb_weight / dbb_weight_gradient (collision/pairs.py:83-108); flag: DEVICE int scratch;
+ * returns CS_NONFINITE when a distance is <= 0 (weight only; FloatingPointError) */
+int cs_dbb_weight(const double *d, long long m, double d_hat, double kappa, int gradient, double *out, int *flag,
+                  void *stream);
 
 /* ---- penetration-free invariant ----------------------------------------- */
 /* oracle_intersect (oracles.py:83-131): intersecting non-adjacent world-triangle pairs at

@@ -65,3 +65,69 @@ def intersecting_pairs(x, triangles, chunk: int = 512):
     out = np.concatenate(found)
     out.sort(axis=1)
     return out
+
+
+def tri_tri_intersect_exact(p, q) -> bool:
+    """Rational-arithmetic separating-axis verdict for one pair (oracles.py:51-80)."""
+    from fractions import Fraction
+
+    P = [[Fraction(float(c)) for c in v] for v in p]
+    Q = [[Fraction(float(c)) for c in v] for v in q]
+
+    def sub(a, b):
+        return [a[i] - b[i] for i in range(3)]
+
+    def cross(a, b):
+        return [a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]]
+
+    def dot(a, b):
+        return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]
+
+    ep = [sub(P[1], P[0]), sub(P[2], P[1]), sub(P[0], P[2])]
+    eq = [sub(Q[1], Q[0]), sub(Q[2], Q[1]), sub(Q[0], Q[2])]
+    n_p, n_q = cross(ep[0], ep[1]), cross(eq[0], eq[1])
+    axes = [n_p, n_q] + [cross(a, b) for a in ep for b in eq] + [cross(n_p, e) for e in ep] + \
+        [cross(n_q, e) for e in eq]
+    for ax in axes:
+        if ax == [0, 0, 0]:
+            continue
+        dp = [dot(ax, v) for v in P]
+        dq = [dot(ax, v) for v in Q]
+        if max(dp) < min(dq) or max(dq) < min(dp):
+            return False
+    return True
+
+
+def exact_separation_margin(p, q) -> float:
+    """Largest normalised separation over the 17 axes in exact arithmetic, 0 when the
+    triangles intersect (reference tests/test_harness.py:127-163)."""
+    from fractions import Fraction
+
+    P = [[Fraction(float(c)) for c in v] for v in p]
+    Q = [[Fraction(float(c)) for c in v] for v in q]
+
+    def sub(a, b):
+        return [a[i] - b[i] for i in range(3)]
+
+    def cross(a, b):
+        return [a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]]
+
+    def dot(a, b):
+        return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]
+
+    ep = [sub(P[1], P[0]), sub(P[2], P[1]), sub(P[0], P[2])]
+    eq = [sub(Q[1], Q[0]), sub(Q[2], Q[1]), sub(Q[0], Q[2])]
+    n_p, n_q = cross(ep[0], ep[1]), cross(eq[0], eq[1])
+    axes = [n_p, n_q] + [cross(a, b) for a in ep for b in eq] + [cross(n_p, e) for e in ep] + \
+        [cross(n_q, e) for e in eq]
+    best = Fraction(0)
+    for ax in axes:
+        norm2 = dot(ax, ax)
+        if norm2 == 0:
+            continue
+        dp = [dot(ax, v) for v in P]
+        dq = [dot(ax, v) for v in Q]
+        gap = max(min(dq) - max(dp), min(dp) - max(dq))
+        if gap > 0:
+            best = max(best, gap * gap / norm2)
+    return float(best) ** 0.5

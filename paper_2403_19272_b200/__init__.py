@@ -7,14 +7,20 @@ CUDA kernels behind the C ABI in include/clothsim_b200.h.
 """
 
 from .mesh import ClothMesh, MeshError, SimState, build_mesh, inertia_target, load_obj, save_obj, triangle_areas
-from .constraints import (ElasticConstraints, GlobalSystem, assemble_global, bend_coefficients, build_elastic,
-                          project_stretch)
-from .subspace import EigensolverError, Subspace, build_subspace
+from .constraints import (ElasticConstraints, GlobalSystem, assemble_global, assemble_rhs, bend_coefficients,
+                          build_elastic, project_stretch)
+from .subspace import (EigensolverError, ReducedSystem, Subspace, build_reduced, build_subspace, reduced_correction,
+                       reduced_update, warmstart_correction)
+from .smoothing import ajacobi_smooth, jacobi_step
 from .stepconfig import StepConfig, StepReport
 from ._lib import PenetrationError, SmootherDivergence
-from .collision import (EE, VT, LIFE_SPAN_CAP, CollisionWorld, PairSet, SampleSet, build_patches, default_samples,
-                        distance_toi, full_ccd, global_toi, ndb_weights, pair_witness, partial_ccd, sample_bound,
+from .collision import (EE, VT, LIFE_SPAN_CAP, CollisionWorld, PairSet, PatchBVH, SampleSet, broad_phase,
+                        build_patches, coplanarity_coefficients, dbb_weight, dbb_weight_gradient, default_samples,
+                        distance_toi, full_ccd, global_toi, lattice_samples, ndb_weights, pair_witness, partial_ccd,
+                        point_triangle_closest, query_q, sample_bound, segment_segment_closest, swept_boxes,
                         update_ndb_weights)
+from .oracles import oracle_intersect, tri_tri_intersect, tri_tri_intersect_exact
+from .sceneconfig import ConfigError, SceneConfig, load_config, parse_config, save_config, serialize_config
 from .scenes import box_mesh, build_scene, grid_cloth, icosphere, strip_cloth
 
 

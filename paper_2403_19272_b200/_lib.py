@@ -64,6 +64,7 @@ class StepReportC(ctypes.Structure):
 
 
 CS_OK, CS_PENETRATION, CS_NONFINITE, CS_DIVERGENCE, CS_BAD_DIAGONAL, CS_BAD_ARGUMENT, CS_INTERNAL = range(7)
+CS_PART_SYSTEM, CS_PART_CLOTH, CS_PART_BASIS, CS_PART_WORLD, CS_PART_ALL = 1, 2, 4, 8, 15
 
 # every symbol include/clothsim_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
@@ -71,7 +72,9 @@ EXPORTED = (
     "cs_state_device", "cs_full_ccd", "cs_distance_toi", "cs_partial_ccd", "cs_pair_witness", "cs_broad_phase",
     "cs_scene_pairs", "cs_ccd_site", "cs_scene_pair_results", "cs_assemble_rhs", "cs_ajacobi_smooth", "cs_reduced_correction", "cs_warmstart_correction",
     "cs_energy_gradient", "cs_collision_terms", "cs_residual", "cs_intersections", "cs_scene_set_verify", "cs_last_intersections", "cs_version",
-    "cs_frame_async", "cs_frame_wait", "cs_format_obj_vertices",
+    "cs_frame_async", "cs_frame_wait", "cs_format_obj_vertices", "cs_scene_create_parts", "cs_tri_tri_intersect",
+    "cs_coplanarity_coefficients", "cs_query_q", "cs_swept_boxes", "cs_dbb_weight", "cs_jacobi_step",
+    "cs_reduced_update", "cs_build_reduced", "cs_reduced_get",
 )
 
 _lib = None
@@ -107,7 +110,7 @@ def load(path: str = LIB_PATH):
         "cs_scene_pairs": (ctypes.c_int, [vp, vp, vp, vp]),
         "cs_ccd_site": (ctypes.c_int, [vp, vp, vp, ctypes.POINTER(ll), ctypes.POINTER(ctypes.c_double), vp]),
         "cs_scene_pair_results": (ctypes.c_int, [vp, vp, vp, vp]),
-        "cs_assemble_rhs": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp]),
+        "cs_assemble_rhs": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp]),
         "cs_ajacobi_smooth": (ctypes.c_int, [vp, vp, vp, ctypes.c_int, ctypes.c_double, vp, vp]),
         "cs_reduced_correction": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, vp]),
         "cs_warmstart_correction": (ctypes.c_int, [vp, vp, vp, vp]),
@@ -118,6 +121,18 @@ def load(path: str = LIB_PATH):
         "cs_scene_set_verify": (ctypes.c_int, [vp, ctypes.c_int]),
         "cs_last_intersections": (ctypes.c_int, [vp, ctypes.POINTER(ll), vp, ctypes.c_int, vp]),
         "cs_version": (ctypes.c_char_p, []),
+        "cs_scene_create_parts": (vp, [ctypes.POINTER(SceneDesc), ctypes.POINTER(StepConfigC), ctypes.c_int,
+                                       c_int_p]),
+        "cs_tri_tri_intersect": (ctypes.c_int, [vp, vp, ll, vp, vp]),
+        "cs_coplanarity_coefficients": (ctypes.c_int, [vp, vp, vp, vp, ll, vp, vp]),
+        "cs_query_q": (ctypes.c_int, [vp, vp, vp, vp, ll, vp, ctypes.c_int, ctypes.c_int, vp, vp]),
+        "cs_swept_boxes": (ctypes.c_int, [vp, vp, ll, ctypes.c_int, ctypes.c_double, vp, vp, vp]),
+        "cs_dbb_weight": (ctypes.c_int, [vp, ll, ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp, vp]),
+        "cs_jacobi_step": (ctypes.c_int, [vp, vp, vp, ctypes.c_double, vp, vp, vp]),
+        "cs_reduced_update": (ctypes.c_int, [vp, vp, vp, ctypes.c_int, vp, vp]),
+        "cs_build_reduced": (ctypes.c_int, [vp, vp, ctypes.c_double, vp, ctypes.POINTER(ctypes.c_double), c_int_p,
+                                            vp]),
+        "cs_reduced_get": (ctypes.c_int, [vp, vp, ctypes.POINTER(ctypes.c_double), c_int_p, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -292,6 +292,7 @@ class CollisionWorld:
     vert_static: np.ndarray
     vert_used: np.ndarray
     edge_static: np.ndarray
+    n_world: int = 0
 
     @classmethod
     def build(cls, triangles, rest_positions, tri_static=None) -> "CollisionWorld":
@@ -329,4 +330,153 @@ class CollisionWorld:
         estat = np.zeros(len(edges), bool)
         estat[tri_edges[stat].ravel()] = True
         return cls(tris, stat, edges, tri_edges, patches, patch_of, slot_of, edge_tris, edge_slot, vstat, used,
-                   estat)
+                   estat, nw)
+
+
+# ------------------------------------------------------------------ module-level drop-ins
+# (reference collision/__init__.py:1-5): same names and signatures; the per-pair
+# arithmetic runs in the device kernels of csrc/stages.cu / narrow.cu / broad.cu.
+
+def coplanarity_coefficients(kind, idx, x_start, x_end) -> np.ndarray:
+    """Monomial coefficients (m,4), lowest order first, of the coplanarity cubic (ccd.py:36-44)."""
+    import torch
+
+    lib = _lib.load()
+    m = len(kind)
+    if m == 0:
+        return np.zeros((0, 4))
+    k, i, (a, b) = _pair_inputs(kind, idx, x_start, x_end)
+    out = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+    _lib.check(lib.cs_coplanarity_coefficients(k.data_ptr(), i.data_ptr(), a.data_ptr(), b.data_ptr(), m,
+                                               out.data_ptr(), _lib.stream_handle()), "cs_coplanarity_coefficients")
+    return out.cpu().numpy()
+
+
+def query_q(kind, idx, x_start, x_end, lam) -> np.ndarray:
+    """Dot product of the pair offset at interval end and start, per sample
+    (partial.py:133-146); lam (m,k,2) or (k,2) shared across pairs -> (m,k)."""
+    import torch
+
+    lib = _lib.load()
+    lam = np.asarray(lam, dtype=np.float64)
+    m = len(kind)
+    shared = lam.ndim == 2
+    kk = lam.shape[-2]
+    if m == 0 or kk == 0:
+        return np.zeros((m, kk))
+    k, i, (a, b) = _pair_inputs(kind, idx, x_start, x_end)
+    ld = _dev(lam, torch.float64)
+    out = torch.empty((m, kk), dtype=torch.float64, device="cuda")
+    _lib.check(lib.cs_query_q(k.data_ptr(), i.data_ptr(), a.data_ptr(), b.data_ptr(), m, ld.data_ptr(), kk,
+                              int(shared), out.data_ptr(), _lib.stream_handle()), "cs_query_q")
+    return out.cpu().numpy()
+
+
+def swept_boxes(points_start: np.ndarray, points_end: np.ndarray, margin: float):
+    """(lo, hi) over both ends of each point group, -/+ margin (bvh.py:140-143)."""
+    import torch
+
+    lib = _lib.load()
+    ps = np.asarray(points_start, dtype=np.float64)
+    pe = np.asarray(points_end, dtype=np.float64)
+    m, kk = ps.shape[0], ps.shape[1]
+    if m == 0:
+        return np.zeros((0, 3)), np.zeros((0, 3))
+    a, b = _dev(ps, torch.float64), _dev(pe, torch.float64)
+    lo = torch.empty((m, 3), dtype=torch.float64, device="cuda")
+    hi = torch.empty_like(lo)
+    _lib.check(lib.cs_swept_boxes(a.data_ptr(), b.data_ptr(), m, kk, float(margin), lo.data_ptr(), hi.data_ptr(),
+                                  _lib.stream_handle()), "cs_swept_boxes")
+    return lo.cpu().numpy(), hi.cpu().numpy()
+
+
+def _dbb(d, d_hat, kappa, gradient):
+    import torch
+
+    lib = _lib.load()
+    arr = np.asarray(d, dtype=np.float64)
+    flat = arr.reshape(-1)
+    out = torch.empty(max(flat.size, 1), dtype=torch.float64, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dd = _dev(flat if flat.size else np.zeros(1), torch.float64)
+    rc = lib.cs_dbb_weight(dd.data_ptr(), flat.size, float(d_hat), float(kappa), int(gradient), out.data_ptr(),
+                           flag.data_ptr(), _lib.stream_handle())
+    if rc == _lib.CS_NONFINITE:
+        raise FloatingPointError("nonpositive pair distance: infeasible state")
+    _lib.check(rc, "cs_dbb_weight")
+    res = out[:flat.size].cpu().numpy().reshape(arr.shape)
+    return res if res.ndim else float(res)
+
+
+def dbb_weight(d, d_hat: float, kappa: float):
+    """Log barrier -kappa (d - d_hat)^2 ln(d / d_hat), zero beyond d_hat (pairs.py:83-98)."""
+    if d_hat <= 0 or kappa <= 0:
+        raise ValueError("need d_hat > 0 and kappa > 0")
+    return _dbb(d, d_hat, kappa, False)
+
+
+def dbb_weight_gradient(d, d_hat: float, kappa: float):
+    """d/dd of dbb_weight, zero at and beyond d_hat (pairs.py:101-108)."""
+    return _dbb(d, d_hat, kappa, True)
+
+
+def _closest(kind_value, *pts):
+    m = len(np.atleast_2d(pts[0]))
+    x = np.concatenate([np.atleast_2d(np.asarray(p, dtype=np.float64)) for p in pts])
+    idx = (np.arange(m)[:, None] + m * np.arange(4)[None, :]).astype(np.int64)
+    return pair_witness(np.full(m, kind_value, np.int8), idx, x)
+
+
+def point_triangle_closest(p, t0, t1, t2):
+    """Closest point on each triangle to each point (geometry.py:10-79):
+    (closest (m,3), bary (m,2), distance (m,))."""
+    _, closest, bary, dist = _closest(VT, p, t0, t1, t2)
+    return closest, bary, dist
+
+
+def segment_segment_closest(a0, a1, b0, b1):
+    """Closest points between segments (geometry.py:82-112): (pa, pb, params (m,2), distance)."""
+    return _closest(EE, a0, a1, b0, b1)
+
+
+def lattice_samples(interval: float, domain: str) -> np.ndarray:
+    """Square lattice over the parameter domain with covering radius <= interval
+    (partial.py:88-102); a sample-pattern generator (setup), not per-pair work."""
+    if interval <= 0:
+        raise ValueError("sample interval must be positive")
+    spacing = interval * np.sqrt(2.0)
+    k = max(int(np.ceil(1.0 / spacing)), 1)
+    u = (np.arange(k) + 0.5) / k
+    gx, gy = np.meshgrid(u, u)
+    pts = np.stack([gx.ravel(), gy.ravel()], axis=1)
+    if domain == "triangle":
+        over = pts.sum(axis=1) > 1.0
+        pts[over] = 1.0 - pts[over][:, ::-1]
+        pts = np.unique(pts, axis=0)
+    return pts
+
+
+PatchBVH = CollisionWorld   # the reference's static-topology structure (bvh.py:54-137)
+
+
+def broad_phase(x_start: np.ndarray, x_end: np.ndarray, bvh: CollisionWorld, margin: float) -> PairSet:
+    """Candidate VT / EE pairs whose margin-inflated swept boxes overlap (bvh.py:207-292):
+    exactly the reference's set (row order is the device's, deterministic), on the
+    device hash grid of a world context for this topology."""
+    import torch
+
+    from . import context
+
+    ctx = context.get(world=bvh)
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")  # noqa: E731
+    a, b = dev(x_start), dev(x_end)
+    count = ctypes.c_longlong(0)
+    _lib.check(ctx.lib.cs_broad_phase(ctx.ptr, a.data_ptr(), b.data_ptr(), float(margin), ctypes.byref(count),
+                                      _lib.stream_handle()), "cs_broad_phase")
+    P = count.value
+    kind = torch.empty(max(P, 1), dtype=torch.int8, device="cuda")
+    idx = torch.empty((max(P, 1), 4), dtype=torch.int32, device="cuda")
+    _lib.check(ctx.lib.cs_scene_pairs(ctx.ptr, kind.data_ptr(), idx.data_ptr(), _lib.stream_handle()),
+               "cs_scene_pairs")
+    return PairSet(kind=kind[:P].cpu().numpy(), idx=idx[:P].cpu().numpy().astype(np.int64),
+                   life_span=np.zeros(P, np.int64), weight=np.zeros(P))

@@ -149,3 +149,38 @@ def project_stretch(x_pair: np.ndarray, rest_length) -> np.ndarray:
     half = 0.5 * rest[:, None] * unit
     out = np.stack([mid - half, mid + half], axis=1)
     return out[0] if one else out
+
+
+def assemble_rhs(system: GlobalSystem, mesh: ClothMesh, elastic: ElasticConstraints, z: np.ndarray, x: np.ndarray,
+                 pinned_positions: np.ndarray, collision_vertices=None, collision_weights=None,
+                 collision_targets=None):
+    """Right-hand side over free vertices plus the collision diagonal delta
+    (constraints.py:229-256), on the device: owner-computes per free vertex over its
+    edge incidence in np.add.at order, M/h^2 z, -H_fp pins, then the collision stamps
+    (stable by row, as np.add.at).  Returns numpy (b (n_free, 3), delta (n_free,))."""
+    import torch
+
+    from . import _lib, context
+
+    ctx = context.get(system=system, mesh=mesh, elastic=elastic)
+    dev = lambda a, t=np.float64: torch.as_tensor(np.ascontiguousarray(a, dtype=t), device="cuda")  # noqa: E731
+    n = mesh.vertex_count
+    pins = None
+    if mesh.pinned.size:
+        full = np.zeros((n, 3))
+        full[mesh.pinned] = np.asarray(pinned_positions, dtype=np.float64).reshape(-1, 3)
+        pins = dev(full)
+    coll = collision_vertices is not None and len(collision_vertices) > 0
+    if coll:
+        ids = dev(np.asarray(collision_vertices), np.int32)
+        w = dev(collision_weights)
+        t = dev(np.asarray(collision_targets, dtype=np.float64).reshape(-1, 3))
+    nf = mesh.free.size
+    b = torch.empty((nf, 3), dtype=torch.float64, device="cuda")
+    delta = torch.empty(nf, dtype=torch.float64, device="cuda")
+    _lib.check(ctx.lib.cs_assemble_rhs(ctx.ptr, dev(z).data_ptr(), dev(x).data_ptr(),
+                                       pins.data_ptr() if pins is not None else None,
+                                       ids.data_ptr() if coll else None, w.data_ptr() if coll else None,
+                                       t.data_ptr() if coll else None, int(len(collision_vertices)) if coll else 0,
+                                       b.data_ptr(), delta.data_ptr(), _lib.stream_handle()), "cs_assemble_rhs")
+    return b.cpu().numpy(), delta.cpu().numpy()

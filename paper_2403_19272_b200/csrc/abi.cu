@@ -43,6 +43,8 @@ using namespace cs;
         if (rc_ != 0) return rc_;  \
     } while (0)
 
+#include "stages.cu"  // scene-free stage kernels + their C entry points
+
 namespace {
 
 // Stream the DBuf (re)allocations of the current call are ordered on.  Buffers come
@@ -1207,7 +1209,9 @@ struct cs_scene {
     // ------------------------------------------------------------ step
     int step(const double* pin_next_h, const double* obs_next_h, cs_step_report* rep);
     int residual_forward(const double* x_final_w, cs_step_report* rep);
-    int create(const cs_scene_desc* d, const cs_step_config* c);
+    int create(const cs_scene_desc* d, const cs_step_config* c, int want);
+    int parts = 0;  // CS_PART_* present
+    bool has(int need) const { return (parts & need) == need; }
     void set_pattern();
     void release();
 };
@@ -1232,8 +1236,9 @@ void cs_scene::set_pattern() {
     }
 }
 
-int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
+int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c, int want) {
     cfg = *c;
+    parts = want;
     n = d->n_cloth;
     nf = d->n_free;
     npin = d->n_pinned;
@@ -1245,20 +1250,25 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
     new_ = d->n_world_edges;
     rb = d->r_bar;
     r = d->r;
-    if (n <= 0 || nf <= 0 || nw != n + nobs || rb <= 0 || r <= 0 || r > rb || rb > 128 || r > 32 || ntw <= 0 ||
-        new_ <= 0)
-        return CS_BAD_ARGUMENT;
+    const bool sys = want & CS_PART_SYSTEM, cloth = want & CS_PART_CLOTH, basis = want & CS_PART_BASIS,
+               world = want & CS_PART_WORLD, state = (want & CS_PART_ALL) == CS_PART_ALL;
+    if (cloth && !sys) return CS_BAD_ARGUMENT;
+    if ((sys || basis) && nf <= 0) return CS_BAD_ARGUMENT;
+    if (cloth && (n <= 0 || nf > n)) return CS_BAD_ARGUMENT;
+    if (basis && (rb <= 0 || r <= 0 || r > rb || rb > 128 || r > 32)) return CS_BAD_ARGUMENT;
+    if (world && (nw <= 0 || ntw <= 0 || new_ <= 0)) return CS_BAD_ARGUMENT;
+    if (state && nw != n + nobs) return CS_BAD_ARGUMENT;
     set_pattern();
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-    CS_RET(free_ids.upload(d->free_ids, nf));
-    CS_RET(free_index.upload(d->free_index, n));
-    CS_RET(pin_ids.upload(d->pin_ids, npin));
-    CS_RET(mass.upload(d->mass, n));
-    CS_RET(fext.upload(d->fext, 3LL * n));
-    CS_RET(mh2.upload(d->mass_over_h2, nf));
-    {
+    if (cloth) {
+        CS_RET(free_ids.upload(d->free_ids, nf));
+        CS_RET(free_index.upload(d->free_index, n));
+        CS_RET(pin_ids.upload(d->pin_ids, npin));
+        CS_RET(mass.upload(d->mass, n));
+        CS_RET(fext.upload(d->fext, 3LL * n));
+        CS_RET(mh2.upload(d->mass_over_h2, nf));
         std::vector<int> a(ne), bb(ne), slot(n, -1);
         for (int i = 0; i < ne; ++i) {
             a[i] = d->edge_v[2 * i];
@@ -1268,80 +1278,87 @@ int cs_scene::create(const cs_scene_desc* d, const cs_step_config* c) {
         CS_RET(e0.upload(a.data(), ne));
         CS_RET(e1.upload(bb.data(), ne));
         CS_RET(pin_slot.upload(slot.data(), n));
+        CS_RET(erest.upload(d->edge_rest, ne));
+        CS_RET(ew.upload(d->edge_w, ne));
+        CS_RET(rinc_ptr.upload(d->rhs_inc_ptr, n + 1));
+        CS_RET(rinc.upload(d->rhs_inc, d->rhs_inc_ptr[n]));
+        CS_RET(ginc_ptr.upload(d->grad_inc_ptr, n + 1));
+        CS_RET(ginc.upload(d->grad_inc, d->grad_inc_ptr[n]));
+        CS_RET(st.upload(d->stencils, 4LL * ns));
+        CS_RET(bk.upload(d->bend_k, 4LL * ns));
+        CS_RET(bw.upload(d->bend_w, ns));
+        CS_RET(binc_ptr.upload(d->bend_inc_ptr, n + 1));
+        CS_RET(binc.upload(d->bend_inc, d->bend_inc_ptr[n]));
+        CS_RET(hfp_ptr.upload(d->hfp_ptr, nf + 1));
+        has_fp = npin > 0 && d->hfp_ptr != nullptr && d->hfp_ptr[nf] > 0;
+        CS_RET(hfp_col.upload(d->hfp_col, std::max(d->hfp_ptr[nf], 1)));
+        CS_RET(hfp_val.upload(d->hfp_val, std::max(d->hfp_ptr[nf], 1)));
     }
-    CS_RET(erest.upload(d->edge_rest, ne));
-    CS_RET(ew.upload(d->edge_w, ne));
-    CS_RET(rinc_ptr.upload(d->rhs_inc_ptr, n + 1));
-    CS_RET(rinc.upload(d->rhs_inc, d->rhs_inc_ptr[n]));
-    CS_RET(ginc_ptr.upload(d->grad_inc_ptr, n + 1));
-    CS_RET(ginc.upload(d->grad_inc, d->grad_inc_ptr[n]));
-    CS_RET(st.upload(d->stencils, 4LL * ns));
-    CS_RET(bk.upload(d->bend_k, 4LL * ns));
-    CS_RET(bw.upload(d->bend_w, ns));
-    CS_RET(binc_ptr.upload(d->bend_inc_ptr, n + 1));
-    CS_RET(binc.upload(d->bend_inc, d->bend_inc_ptr[n]));
-    nslices = d->sell_nslices;
-    CS_RET(sell_ptr.upload(d->sell_slice_ptr, nslices + 1));
-    CS_RET(sell_col.upload(d->sell_col, d->sell_slice_ptr[nslices]));
-    CS_RET(sell_val.upload(d->sell_val, d->sell_slice_ptr[nslices]));
-    CS_RET(diag.upload(d->diag, nf));
-    has_fp = npin > 0 && d->hfp_ptr != nullptr && d->hfp_ptr[nf] > 0;
-    CS_RET(hfp_ptr.upload(d->hfp_ptr, nf + 1));
-    CS_RET(hfp_col.upload(d->hfp_col, std::max(d->hfp_ptr[nf], 1)));
-    CS_RET(hfp_val.upload(d->hfp_val, std::max(d->hfp_ptr[nf], 1)));
-    CS_RET(U.upload(d->U, (size_t)nf * rb));
-    {
+    if (sys) {
+        nslices = d->sell_nslices;
+        CS_RET(sell_ptr.upload(d->sell_slice_ptr, nslices + 1));
+        CS_RET(sell_col.upload(d->sell_col, d->sell_slice_ptr[nslices]));
+        CS_RET(sell_val.upload(d->sell_val, d->sell_slice_ptr[nslices]));
+        CS_RET(diag.upload(d->diag, nf));
+    }
+    if (basis) {
+        CS_RET(U.upload(d->U, (size_t)nf * rb));
         std::vector<double> vv((size_t)nf * r);
         for (long long i = 0; i < nf; ++i)
             for (int j = 0; j < r; ++j) vv[i * r + j] = d->U[i * rb + j];
         CS_RET(V.upload(vv.data(), vv.size()));
+        CS_RET(lam.upload(d->eigenvalues, rb));
     }
-    CS_RET(lam.upload(d->eigenvalues, rb));
-    CS_RET(wtris.upload(d->world_tris, 3LL * ntw));
-    CS_RET(wedges.upload(d->world_edges, 2LL * new_));
-    CS_RET(tri_static.upload(d->tri_static, ntw));
-    CS_RET(vert_static.upload(d->vert_static, nw));
-    CS_RET(vert_used.upload(d->vert_used, nw));
-    CS_RET(edge_static.upload(d->edge_static, new_));
-    CS_RET(edge_tris.upload(d->edge_tris, 2LL * new_));
-    CS_RET(edge_slot.upload(d->edge_slot, 2LL * new_));
-    CS_RET(patch.upload(d->patch, ntw));
-    CS_RET(pslot.upload(d->patch_slot, ntw));
-    CS_RET(eflip.ensure(new_));
-    k_edge_flip_info<<<grid(new_), 256>>>(new_, edge_tris.p, edge_slot.p, tri_static.p, patch.p, pslot.p, eflip.p);
-    CS_TRY(cudaGetLastError());
-    CS_RET(vtab.create(nw, false));
-    CS_RET(ttab.create(ntw, true));
-    CS_RET(etab.create(new_, true));
-    // state
-    CS_RET(x.upload(d->x0, 3LL * n));
-    CS_RET(xprev.upload(d->x0, 3LL * n));
-    CS_RET(v.ensure(3LL * n));
-    CS_RET(df.ensure(3LL * n));
-    CS_TRY(cudaMemset(v.p, 0, sizeof(double) * 3 * n));
-    CS_TRY(cudaMemset(df.p, 0, sizeof(double) * 3 * n));
-    CS_RET(obs.upload(d->obstacle_x0, 3LL * std::max(nobs, 0)));
-    CS_RET(obs.ensure(std::max(3LL * nobs, 1LL)));
-    // work
-    for (DBuf<double>* w : {&xs_w, &xc_w, &anchor_w, &tmp_w}) CS_RET(w->ensure(3LL * nw));
-    for (DBuf<double>* w : {&z, &prev_outer, &grad, &dfn}) CS_RET(w->ensure(3LL * n));
-    for (DBuf<double>* w : {&xf, &xf0, &b, &t, &fr}) CS_RET(w->ensure(3LL * nf));
-    CS_RET(delta.ensure(nf));
-    CS_RET(pins_next_d.ensure(std::max(3 * npin, 1)));
-    CS_RET(obs_next_d.ensure(std::max(3 * nobs, 1)));
-    // page-locked staging for the per-step pin / obstacle targets (a pageable
-    // cudaMemcpyAsync stages through the driver and can stall the stream)
-    CS_TRY(cudaMallocHost(&h_stage, sizeof(double) * (3 * npin + 3 * nobs + 1)));
-    CS_RET(vlo.ensure(3LL * nw));
-    CS_RET(vhi.ensure(3LL * nw));
-    CS_RET(vdisp.ensure(nw, true));
-    CS_RET(fvbox.ensure(16LL * nw, true));
-    CS_RET(ftbox.ensure(16LL * ntw, true));
-    CS_RET(febox.ensure(16LL * new_, true));
-    CS_RET(tdisp.ensure(ntw, true));
-    CS_RET(edisp.ensure(new_, true));
-    CS_RET(seg_beg.ensure(nf));
-    CS_RET(seg_end.ensure(nf));
+    if (world) {
+        CS_RET(wtris.upload(d->world_tris, 3LL * ntw));
+        CS_RET(wedges.upload(d->world_edges, 2LL * new_));
+        CS_RET(tri_static.upload(d->tri_static, ntw));
+        CS_RET(vert_static.upload(d->vert_static, nw));
+        CS_RET(vert_used.upload(d->vert_used, nw));
+        CS_RET(edge_static.upload(d->edge_static, new_));
+        CS_RET(edge_tris.upload(d->edge_tris, 2LL * new_));
+        CS_RET(edge_slot.upload(d->edge_slot, 2LL * new_));
+        CS_RET(patch.upload(d->patch, ntw));
+        CS_RET(pslot.upload(d->patch_slot, ntw));
+        CS_RET(eflip.ensure(new_));
+        k_edge_flip_info<<<grid(new_), 256>>>(new_, edge_tris.p, edge_slot.p, tri_static.p, patch.p, pslot.p,
+                                               eflip.p);
+        CS_TRY(cudaGetLastError());
+        CS_RET(vtab.create(nw, false));
+        CS_RET(ttab.create(ntw, true));
+        CS_RET(etab.create(new_, true));
+        for (DBuf<double>* w : {&xs_w, &xc_w, &anchor_w, &tmp_w}) CS_RET(w->ensure(3LL * nw));
+        CS_RET(vlo.ensure(3LL * nw));
+        CS_RET(vhi.ensure(3LL * nw));
+        CS_RET(vdisp.ensure(nw, true));
+        CS_RET(fvbox.ensure(16LL * nw, true));
+        CS_RET(ftbox.ensure(16LL * ntw, true));
+        CS_RET(febox.ensure(16LL * new_, true));
+        CS_RET(tdisp.ensure(ntw, true));
+        CS_RET(edisp.ensure(new_, true));
+    }
+    if (state) {
+        CS_RET(x.upload(d->x0, 3LL * n));
+        CS_RET(xprev.upload(d->x0, 3LL * n));
+        CS_RET(v.ensure(3LL * n));
+        CS_RET(df.ensure(3LL * n));
+        CS_TRY(cudaMemset(v.p, 0, sizeof(double) * 3 * n));
+        CS_TRY(cudaMemset(df.p, 0, sizeof(double) * 3 * n));
+        CS_RET(obs.upload(d->obstacle_x0, 3LL * std::max(nobs, 0)));
+        CS_RET(obs.ensure(std::max(3LL * nobs, 1LL)));
+        CS_RET(pins_next_d.ensure(std::max(3 * npin, 1)));
+        CS_RET(obs_next_d.ensure(std::max(3 * nobs, 1)));
+        // page-locked staging for the per-step pin / obstacle targets (a pageable
+        // cudaMemcpyAsync stages through the driver and can stall the stream)
+        CS_TRY(cudaMallocHost(&h_stage, sizeof(double) * (3 * npin + 3 * nobs + 1)));
+    }
+    if (cloth) for (DBuf<double>* w : {&z, &prev_outer, &grad, &dfn}) CS_RET(w->ensure(3LL * n));
+    if (sys) {
+        for (DBuf<double>* w : {&xf, &xf0, &b, &t, &fr}) CS_RET(w->ensure(3LL * nf));
+        CS_RET(delta.ensure(nf));
+        CS_RET(seg_beg.ensure(nf));
+        CS_RET(seg_end.ensure(nf));
+    }
     CS_RET(rhs_red.ensure(3 * 128));
     CS_RET(gram_red.ensure(32 * 32));
     CS_RET(q.ensure(3 * 128));
@@ -1804,9 +1821,17 @@ cs_scene* cs_scene_create(const cs_scene_desc* desc, const cs_step_config* cfg, 
             cudaGetLastError();
         }
     }
+    return cs_scene_create_parts(desc, cfg, CS_PART_ALL, status);
+}
+
+cs_scene* cs_scene_create_parts(const cs_scene_desc* desc, const cs_step_config* cfg, int parts, int* status) {
+    if (!desc || !cfg) {
+        if (status) *status = CS_BAD_ARGUMENT;
+        return nullptr;
+    }
     t_alloc_stream = nullptr;
     cs_scene* sc = new cs_scene();
-    int rc = sc->create(desc, cfg);
+    int rc = sc->create(desc, cfg, parts);
     if (status) *status = rc;
     if (rc != 0) {
         sc->release();
@@ -1832,6 +1857,7 @@ int cs_scene_set_config(cs_scene* scene, const cs_step_config* cfg) {
 
 int cs_step(cs_scene* scene, const double* pin_next, const double* obstacle_next, cs_step_report* report,
             void* stream) {
+    if (scene && !scene->has(CS_PART_ALL)) return CS_BAD_ARGUMENT;
     if (!scene) return CS_BAD_ARGUMENT;
     static const bool trace_host = std::getenv("CS_TRACE_HOST") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
@@ -1853,6 +1879,7 @@ int cs_step(cs_scene* scene, const double* pin_next, const double* obstacle_next
 
 int cs_get_state(cs_scene* sc, double* x, double* x_dot, double* x_prev, double* delta_f, double* obstacle_x,
                  int* step_index, void* stream) {
+    if (sc && !sc->has(CS_PART_ALL)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
     t_alloc_stream = s;
@@ -1870,6 +1897,7 @@ int cs_get_state(cs_scene* sc, double* x, double* x_dot, double* x_prev, double*
 
 int cs_set_state(cs_scene* sc, const double* x, const double* x_dot, const double* x_prev, const double* delta_f,
                  const double* obstacle_x, int step_index, void* stream) {
+    if (sc && !sc->has(CS_PART_ALL)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
     t_alloc_stream = s;
@@ -1886,6 +1914,7 @@ int cs_set_state(cs_scene* sc, const double* x, const double* x_dot, const doubl
 }
 
 int cs_state_device(cs_scene* sc, double** x, double** x_dot, double** delta_f, double** obstacle_x) {
+    if (sc && !sc->has(CS_PART_ALL)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     if (x) *x = sc->x.p;
     if (x_dot) *x_dot = sc->v.p;
@@ -1900,6 +1929,7 @@ int cs_state_device(cs_scene* sc, double** x, double** x_dot, double** delta_f, 
 // copied to the caller's page-locked buffer on a separate copy stream while the
 // next steps run.  cs_frame_wait(ticket) blocks until that copy has landed.
 int cs_frame_async(cs_scene* sc, double* host_x, int* ticket, void* stream) {
+    if (sc && !sc->has(CS_PART_ALL)) return CS_BAD_ARGUMENT;
     if (!sc || !host_x || !ticket) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
     t_alloc_stream = s;
@@ -1997,6 +2027,7 @@ int cs_pair_witness(const int8_t* kind, const int* idx4, const double* x, long l
 
 int cs_broad_phase(cs_scene* sc, const double* x_start_w, const double* x_end_w, double margin, long long* count,
                    void* stream) {
+    if (sc && !sc->has(CS_PART_WORLD)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;
@@ -2008,6 +2039,7 @@ int cs_broad_phase(cs_scene* sc, const double* x_start_w, const double* x_end_w,
 
 int cs_ccd_site(cs_scene* sc, const double* x_start_w, const double* x_end_w, long long* count, double* clamp,
                 void* stream) {
+    if (sc && !sc->has(CS_PART_WORLD)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;
@@ -2020,6 +2052,7 @@ int cs_ccd_site(cs_scene* sc, const double* x_start_w, const double* x_end_w, lo
 }
 
 int cs_scene_pair_results(cs_scene* sc, double* toi, double* toi_filter, void* stream) {
+    if (sc && !sc->has(CS_PART_WORLD)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
     t_alloc_stream = s;
@@ -2037,6 +2070,7 @@ int cs_scene_set_verify(cs_scene* sc, int on) {
 }
 
 int cs_intersections(cs_scene* sc, const double* x_world, long long* count, int* pairs, int cap, void* stream) {
+    if (sc && !sc->has(CS_PART_WORLD)) return CS_BAD_ARGUMENT;
     if (!sc || cap < 0) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;
@@ -2069,6 +2103,7 @@ int cs_last_intersections(cs_scene* sc, long long* count, int* pairs, int cap, d
 }
 
 int cs_scene_pairs(cs_scene* sc, int8_t* kind, int* idx4, void* stream) {
+    if (sc && !sc->has(CS_PART_WORLD)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
     t_alloc_stream = s;
@@ -2079,8 +2114,9 @@ int cs_scene_pairs(cs_scene* sc, int8_t* kind, int* idx4, void* stream) {
     return 0;
 }
 
-int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const int* coll_ids, const double* coll_w,
-                    const double* coll_t, int n_coll, double* b, double* delta, void* stream) {
+int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const double* pins, const int* coll_ids,
+                    const double* coll_w, const double* coll_t, int n_coll, double* b, double* delta, void* stream) {
+    if (sc && !sc->has(CS_PART_CLOTH | CS_PART_SYSTEM)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;
@@ -2111,8 +2147,9 @@ int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const int* c
     }
     k_assemble_rhs<<<sc->grid(sc->nf), 256, 0, s>>>(sc->nf, sc->free_ids.p, x, z, sc->mh2.p, sc->edges(),
                                                     sc->rinc_ptr.p, sc->rinc.p, sc->has_fp ? sc->hfp_ptr.p : nullptr,
-                                                    sc->hfp_col.p, sc->hfp_val.p, x, with ? sc->seg_beg.p : nullptr,
-                                                    sc->seg_end.p, sc->ssrc_s.p, sc->stamp.p, b, delta);
+                                                    sc->hfp_col.p, sc->hfp_val.p, pins ? pins : x,
+                                                    with ? sc->seg_beg.p : nullptr, sc->seg_end.p, sc->ssrc_s.p,
+                                                    sc->stamp.p, b, delta);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(s));
     return 0;
@@ -2121,6 +2158,7 @@ int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const int* c
 int cs_collision_terms(cs_scene* sc, const int8_t* kind, const int* idx4, const double* bary, const double* normal,
                        const double* weight, const uint8_t* engaged, long long P, const double* x_world, int* ids,
                        double* w, double* targets, long long* count, void* stream) {
+    if (sc && !sc->has(CS_PART_CLOTH | CS_PART_SYSTEM)) return CS_BAD_ARGUMENT;
     if (!sc || P < 0) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;
@@ -2167,6 +2205,7 @@ int cs_collision_terms(cs_scene* sc, const int8_t* kind, const int* idx4, const 
 }
 
 int cs_residual(cs_scene* sc, const double* b, const double* x, const double* delta, double* r, void* stream) {
+    if (sc && !sc->has(CS_PART_SYSTEM)) return CS_BAD_ARGUMENT;
     if (!sc || !delta) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;
@@ -2178,6 +2217,7 @@ int cs_residual(cs_scene* sc, const double* b, const double* x, const double* de
 
 int cs_ajacobi_smooth(cs_scene* sc, const double* b, double* x, int iterations, double omega, const double* delta,
                       void* stream) {
+    if (sc && !sc->has(CS_PART_SYSTEM)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;
@@ -2191,6 +2231,7 @@ int cs_ajacobi_smooth(cs_scene* sc, const double* b, double* x, int iterations, 
 }
 
 int cs_reduced_correction(cs_scene* sc, const double* b, double* x, const double* delta, int reuse, void* stream) {
+    if (sc && !sc->has(CS_PART_SYSTEM | CS_PART_BASIS)) return CS_BAD_ARGUMENT;
     if (!sc || !delta) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;
@@ -2214,7 +2255,79 @@ int cs_reduced_correction(cs_scene* sc, const double* b, double* x, const double
     return 0;
 }
 
+// jacobi_step (smoothing.py:69-78): out = x + (1 - omega) D^-1 (b - (H + delta) x)
+int cs_jacobi_step(cs_scene* sc, const double* b, const double* x, double omega, const double* delta, double* out,
+                   void* stream) {
+    if (sc && !sc->has(CS_PART_SYSTEM)) return CS_BAD_ARGUMENT;
+    if (!sc) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
+    const double* dl = delta;
+    if (dl == nullptr) {
+        CS_TRY(cudaMemsetAsync(sc->delta.p, 0, sizeof(double) * sc->nf, sc->s));
+        dl = sc->delta.p;
+    }
+    k_jacobi_a<<<sc->grid(sc->nf, 128), 128, 0, sc->s>>>(sc->sell(), sc->diag.p, dl, b, x, sc->t.p, nullptr);
+    k_axpy_step<<<sc->grid(3LL * sc->nf), 256, 0, sc->s>>>(x, sc->t.p, 1.0 - omega, 3LL * sc->nf, out);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaStreamSynchronize(sc->s));
+    return 0;
+}
+
+// reduced_update (subspace.py:97-106): G (r*r) = sum_j w_j V_j V_j^T over rows[j] (DEVICE)
+int cs_reduced_update(cs_scene* sc, const int* rows, const double* weights, int m, double* G, void* stream) {
+    if (sc && !sc->has(CS_PART_BASIS)) return CS_BAD_ARGUMENT;
+    if (!sc || m < 0) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
+    const int r = sc->r;
+    if (m == 0) {
+        CS_TRY(cudaMemsetAsync(G, 0, sizeof(double) * r * r, sc->s));
+        return 0;
+    }
+    CS_TRY(cudaMemcpyAsync(sc->d_iscal.p + I_FLAG, &m, sizeof(int), cudaMemcpyHostToDevice, sc->s));
+    const int gg = std::min(cs_div_up(m, 8), sc->sm_count);
+    CS_RET(sc->part2.ensure((size_t)gg * r * r));
+    k_gram_partial<<<gg, kGramThreads, 0, sc->s>>>(rows, sc->d_iscal.p + I_FLAG, nullptr, sc->V.p, r, sc->part2.p,
+                                                   weights);
+    k_reduce_partials<<<cs_div_up(r * r, 32), 256, 0, sc->s>>>(sc->part2.p, gg, r * r, G);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaStreamSynchronize(sc->s));
+    return 0;
+}
+
+// build_reduced (subspace.py:122-140): A = diag(lambda_r) + G (G DEVICE r*r, may be NULL),
+// beta = rhs_scale (1 if <= 0), inverse X with A X = I / beta (LU, pinv fallback) ->
+// inverse (DEVICE r*r); beta / fallback (HOST).  The context keeps it as its current
+// reduced system (cs_reduced_correction with reuse != 0 applies it).
+int cs_build_reduced(cs_scene* sc, const double* G, double rhs_scale, double* inverse, double* beta, int* fallback,
+                     void* stream) {
+    if (sc && !sc->has(CS_PART_BASIS)) return CS_BAD_ARGUMENT;
+    if (!sc) return CS_BAD_ARGUMENT;
+    sc->s = (cudaStream_t)stream;
+    t_alloc_stream = sc->s;
+    ReducedState rs{sc->Xred.p, sc->beta_red.p, sc->fallback.p};
+    k_reduced_solve<<<1, 256, 0, sc->s>>>(sc->rhs_red.p, G, sc->lam.p, sc->r, 0, 1, rs, sc->q.p,
+                                           rhs_scale > 0.0 ? rhs_scale : 0.0);
+    CS_CHECK_LAUNCH();
+    return cs_reduced_get(sc, inverse, beta, fallback, stream);
+}
+
+// the context's current reduced system (after cs_reduced_correction / cs_build_reduced)
+int cs_reduced_get(cs_scene* sc, double* inverse, double* beta, int* fallback, void* stream) {
+    if (sc && !sc->has(CS_PART_BASIS)) return CS_BAD_ARGUMENT;
+    if (!sc) return CS_BAD_ARGUMENT;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int r = sc->r;
+    if (inverse) CS_TRY(cudaMemcpyAsync(inverse, sc->Xred.p, sizeof(double) * r * r, cudaMemcpyDeviceToDevice, s));
+    if (beta) CS_TRY(cudaMemcpyAsync(beta, sc->beta_red.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (fallback) CS_TRY(cudaMemcpyAsync(fallback, sc->fallback.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CS_TRY(cudaStreamSynchronize(s));
+    return 0;
+}
+
 int cs_warmstart_correction(cs_scene* sc, const double* b, double* x, void* stream) {
+    if (sc && !sc->has(CS_PART_SYSTEM | CS_PART_BASIS)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;
@@ -2225,6 +2338,7 @@ int cs_warmstart_correction(cs_scene* sc, const double* b, double* x, void* stre
 
 int cs_energy_gradient(cs_scene* sc, const double* x, const double* z, const int* q_ids, const double* q_w,
                        const double* q_t, int n_q, double* grad, void* stream) {
+    if (sc && !sc->has(CS_PART_CLOTH | CS_PART_SYSTEM)) return CS_BAD_ARGUMENT;
     if (!sc) return CS_BAD_ARGUMENT;
     sc->s = (cudaStream_t)stream;
     t_alloc_stream = sc->s;

@@ -149,12 +149,9 @@ __device__ __forceinline__ bool separated_sides(int kd, const Corners& a, const 
     return gap > bound * (1.0 + 1e-6) + 1e-9 * mag;
 }
 
-// full_ccd for one pair (ccd.py:138-196); NaN = miss
-__device__ double full_ccd_pair(int kd, const Corners& a, const Corners& b, int single, double tol) {
-    const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
-    if (separated_sides(kd, a, b, tol)) return NaN;
-
-    // coplanarity samples at t = 0, 1/3, 2/3, 1 and the monomial fit (ccd.py:36-44)
+// coplanarity samples at t = 0, 1/3, 2/3, 1 and the monomial fit (coplanarity_coefficients,
+// ccd.py:36-44), lowest order first
+__device__ __forceinline__ void coplanarity_fit(int kd, const Corners& a, const Corners& b, int single, double c[4]) {
     const double nodes[4] = {0.0, 1.0 / 3.0, 2.0 / 3.0, 1.0};
     double f[4];
 #pragma unroll
@@ -164,7 +161,6 @@ __device__ double full_ccd_pair(int kd, const Corners& a, const Corners& b, int 
         for (int k = 0; k < 4; ++k) q[k] = lerp_node(a.p[k], b.p[k], nodes[j]);
         f[j] = triple(kd, q);
     }
-    double c[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         if (!single) {  // OpenBLAS dgemm k=4 kernel: forward FMA chain
@@ -178,6 +174,14 @@ __device__ double full_ccd_pair(int kd, const Corners& a, const Corners& b, int 
             c[j] = even + odd;
         }
     }
+}
+
+// full_ccd for one pair (ccd.py:138-196); NaN = miss
+__device__ double full_ccd_pair(int kd, const Corners& a, const Corners& b, int single, double tol) {
+    const double NaN = __longlong_as_double(0x7ff8000000000000ULL);
+    if (separated_sides(kd, a, b, tol)) return NaN;
+    double c[4];
+    coplanarity_fit(kd, a, b, single, c);
     const double csum = ((fabs(c[0]) + fabs(c[1])) + fabs(c[2])) + fabs(c[3]);
     const double ext = pair_extent(a, b);
     const bool flat = csum <= 1e-12 * np_max(cube_rn(fabs(ext)), 1e-30);

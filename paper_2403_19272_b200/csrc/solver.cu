@@ -248,6 +248,13 @@ __global__ void k_jacobi_b(Sell H, const double* __restrict__ diag, const double
     st3(x, i, ld3(x, i) + upd);
 }
 
+// out = x + c t (jacobi_step's update, smoothing.py:78)
+__global__ void k_axpy_step(const double* __restrict__ x, const double* __restrict__ t, double c, int64_t n,
+                            double* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = x[i] + c * t[i];
+}
+
 // divergence guard between the k=0 and k=10 residual norms (smoothing.py:57-63)
 __global__ void k_norm_final(const double* __restrict__ part, int nparts, double* __restrict__ slot) {
     __shared__ double sm[256];
@@ -357,7 +364,10 @@ __global__ void __launch_bounds__(kGramThreads) k_gram_partial(const int* __rest
                                                                const int* __restrict__ nrows_ptr,
                                                                const double* __restrict__ delta,
                                                                const double* __restrict__ V, int r,
-                                                               double* __restrict__ part) {
+                                                               double* __restrict__ part,
+                                                               const double* __restrict__ wlist = nullptr) {
+    // weight of list entry j: delta[rows[j]] (the step), or wlist[j] (reduced_update's
+    // explicit (active_vertices, weights), subspace.py:97-106)
     constexpr int kT = 64;
     __shared__ __align__(16) double sv[kT][32];
     __shared__ __align__(16) double sw[kT][32];
@@ -384,7 +394,7 @@ __global__ void __launch_bounds__(kGramThreads) k_gram_partial(const int* __rest
             if (k < nt && c < r) {
                 const int row = rows[t0 + k];
                 v[u] = V[(int64_t)row * r + c];
-                d[u] = delta[row];
+                d[u] = wlist != nullptr ? wlist[t0 + k] : delta[row];
             }
         }
 #pragma unroll
@@ -507,7 +517,10 @@ __device__ void jacobi_eig_pinv(double* A, double* Q, double* w, int r, double* 
 __global__ void __launch_bounds__(256) k_reduced_solve(const double* __restrict__ rhs_in,
                                                        const double* __restrict__ gram_in,
                                                        const double* __restrict__ lam, int rb, int mode,
-                                                       int refactor, ReducedState st, double* __restrict__ q_out) {
+                                                       int refactor, ReducedState st, double* __restrict__ q_out,
+                                                       double beta_given = -1.0) {
+    // beta_given >= 0: build_reduced(sub, G, rhs_scale) - beta = rhs_scale (1 if <= 0),
+    // factor only (q_out unused)
     __shared__ double rhs[3 * 128];
     __shared__ double A[32 * 32], LU[32 * 32], X[32 * 32], Q[32 * 32], wv[32];
     __shared__ int piv[32];
@@ -530,9 +543,12 @@ __global__ void __launch_bounds__(256) k_reduced_solve(const double* __restrict_
         }
         __syncthreads();
         if (tid == 0) {
-            double s = 0.0;
-            for (int o = 0; o < 3 * r; ++o) s += fabs(rhs[o]);
-            double bt = s / (3.0 * r);
+            double bt = beta_given;
+            if (bt < 0.0) {
+                double s = 0.0;
+                for (int o = 0; o < 3 * r; ++o) s += fabs(rhs[o]);
+                bt = s / (3.0 * r);
+            }
             beta_sm = bt > 0.0 ? bt : 1.0;
             singular = 0;
         }
@@ -634,6 +650,7 @@ __global__ void __launch_bounds__(256) k_reduced_solve(const double* __restrict_
         if (tid == 0) beta_sm = *st.beta;
         __syncthreads();
     }
+    if (beta_given >= 0.0) return;  // build only
     // q = beta * (X @ rhs)
     const double bt = beta_sm;
     for (int o = tid; o < 3 * r; o += blockDim.x) {

@@ -77,22 +77,21 @@ def step_config_c(cfg, k: float, kappa: float = 0.0) -> _lib.StepConfigC:
     return c
 
 
-def scene_desc(mesh, elastic, system, subspace, world, obstacle_x, gravity_force, x0):
-    """Build (SceneDesc, keepalive) for cs_scene_create."""
-    keep = _Keep()
-    I, D, U8 = ctypes.c_int, ctypes.c_double, ctypes.c_uint8
-    d = _lib.SceneDesc()
+def _fill_system(d, keep, system):
+    I, D = ctypes.c_int, ctypes.c_double
+    d.n_free = system.H.shape[0]
+    nsl, sptr, scol, sval = sell32(system.H)
+    d.sell_nslices = nsl
+    d.sell_slice_ptr, d.sell_col, d.sell_val = keep.ptr(sptr, I), keep.ptr(scol, I), keep.ptr(sval, D)
+    d.diag = keep.ptr(system.diag, D)
+
+
+def _fill_cloth(d, keep, mesh, elastic, system, gravity_force):
+    I, D = ctypes.c_int, ctypes.c_double
     n = mesh.vertex_count
-    nf = mesh.free.size
-    nobs = len(obstacle_x)
-    d.n_cloth, d.n_free, d.n_pinned, d.n_obstacle = n, nf, mesh.pinned.size, nobs
-    d.n_world = n + nobs
+    d.n_cloth, d.n_pinned = n, mesh.pinned.size
     d.n_edges = len(elastic.edges)
     d.n_stencils = len(elastic.stencils)
-    d.n_world_tris = len(world.triangles)
-    d.n_world_edges = len(world.edges)
-    d.r_bar = subspace.U.shape[1]
-    d.r = subspace.r
     d.free_ids = keep.ptr(mesh.free.astype(np.int32), I)
     d.free_index = keep.ptr(mesh.free_index.astype(np.int32), I)
     d.pin_ids = keep.ptr(np.concatenate([mesh.pinned, [0]]).astype(np.int32), I)
@@ -117,17 +116,26 @@ def scene_desc(mesh, elastic, system, subspace, world, obstacle_x, gravity_force
     d.bend_w = keep.ptr(np.concatenate([elastic.bend_w, [0.0]]), D)
     ptr, codes = incidence(n, st.ravel(), np.arange(st.size, dtype=np.int64))
     d.bend_inc_ptr, d.bend_inc = keep.ptr(ptr, I), keep.ptr(np.concatenate([codes, [0]]).astype(np.int32), I)
-    nsl, sptr, scol, sval = sell32(system.H)
-    d.sell_nslices = nsl
-    d.sell_slice_ptr, d.sell_col, d.sell_val = keep.ptr(sptr, I), keep.ptr(scol, I), keep.ptr(sval, D)
-    d.diag = keep.ptr(system.diag, D)
     hfp = system.H_fp
     d.hfp_ptr = keep.ptr(np.asarray(hfp.indptr, dtype=np.int32), I)
     fp_cols = mesh.pinned[hfp.indices] if mesh.pinned.size else np.zeros(0, np.int64)
     d.hfp_col = keep.ptr(np.concatenate([fp_cols, [0]]).astype(np.int32), I)
     d.hfp_val = keep.ptr(np.concatenate([hfp.data, [0.0]]), D)
+
+
+def _fill_basis(d, keep, subspace):
+    D = ctypes.c_double
+    d.r_bar = subspace.U.shape[1]
+    d.r = subspace.r
     d.U = keep.ptr(np.ascontiguousarray(subspace.U, dtype=np.float64), D)
     d.eigenvalues = keep.ptr(subspace.eigenvalues, D)
+
+
+def _fill_world(d, keep, world, n_world):
+    I, U8 = ctypes.c_int, ctypes.c_uint8
+    d.n_world = n_world
+    d.n_world_tris = len(world.triangles)
+    d.n_world_edges = len(world.edges)
     d.world_tris = keep.ptr(world.triangles.astype(np.int32), I)
     d.world_edges = keep.ptr(world.edges.astype(np.int32), I)
     d.tri_static = keep.ptr(world.tri_static.astype(np.uint8), U8)
@@ -138,6 +146,43 @@ def scene_desc(mesh, elastic, system, subspace, world, obstacle_x, gravity_force
     d.edge_slot = keep.ptr(world.edge_slot.astype(np.int32), I)
     d.patch = keep.ptr(world.patch_of_tri.astype(np.int32), I)
     d.patch_slot = keep.ptr(world.slot_of_tri.astype(np.int32), I)
+
+
+def parts_desc(system=None, mesh=None, elastic=None, subspace=None, world=None, n_world=0, gravity_force=None):
+    """(SceneDesc, keepalive, parts) of a partial context (cs_scene_create_parts) from
+    whichever reference setup objects are given."""
+    keep = _Keep()
+    d = _lib.SceneDesc()
+    parts = 0
+    if system is not None:
+        _fill_system(d, keep, system)
+        parts |= _lib.CS_PART_SYSTEM
+        if mesh is not None and elastic is not None:
+            g = gravity_force if gravity_force is not None else np.zeros((mesh.vertex_count, 3))
+            _fill_cloth(d, keep, mesh, elastic, system, g)
+            parts |= _lib.CS_PART_CLOTH
+    if subspace is not None:
+        _fill_basis(d, keep, subspace)
+        if system is None:
+            d.n_free = subspace.U.shape[0]
+        parts |= _lib.CS_PART_BASIS
+    if world is not None:
+        _fill_world(d, keep, world, n_world or getattr(world, "n_world", 0) or int(world.triangles.max()) + 1)
+        parts |= _lib.CS_PART_WORLD
+    return d, keep, parts
+
+
+def scene_desc(mesh, elastic, system, subspace, world, obstacle_x, gravity_force, x0):
+    """Build (SceneDesc, keepalive) for cs_scene_create (every part + the state)."""
+    keep = _Keep()
+    D = ctypes.c_double
+    d = _lib.SceneDesc()
+    nobs = len(obstacle_x)
+    _fill_system(d, keep, system)
+    _fill_cloth(d, keep, mesh, elastic, system, gravity_force)
+    _fill_basis(d, keep, subspace)
+    _fill_world(d, keep, world, mesh.vertex_count + nobs)
+    d.n_obstacle = nobs
     d.x0 = keep.ptr(np.asarray(x0, dtype=np.float64), D)
     d.obstacle_x0 = keep.ptr(np.concatenate([np.asarray(obstacle_x, dtype=np.float64).ravel(), [0.0]]), D)
     return d, keep

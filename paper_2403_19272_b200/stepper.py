@@ -445,7 +445,7 @@ class Simulation:
         free = torch.as_tensor(mesh.free, device="cuda")
         its = 0
         for _ in range(cfg.warm_start_cap):
-            _lib.check(self._lib.cs_assemble_rhs(self._scene, zd.data_ptr(), xd.data_ptr(), None, None, None, 0,
+            _lib.check(self._lib.cs_assemble_rhs(self._scene, zd.data_ptr(), xd.data_ptr(), None, None, None, None, 0,
                                                  b.data_ptr(), delta.data_ptr(), self._stream()), "cs_assemble_rhs")
             xf = xd[free].contiguous()
             x0 = xf.clone()
@@ -633,7 +633,7 @@ class Simulation:
             w_d, t_d = self._dbuf(quad[2]), self._dbuf(quad[3])
             b = torch.empty((nf, 3), dtype=torch.float64, device="cuda")
             zz = self._dbuf(z)
-            _lib.check(self._lib.cs_assemble_rhs(self._scene, zz.data_ptr(), zz.data_ptr(), ids_d.data_ptr(),
+            _lib.check(self._lib.cs_assemble_rhs(self._scene, zz.data_ptr(), zz.data_ptr(), None, ids_d.data_ptr(),
                                                  w_d.data_ptr(), t_d.data_ptr(), len(quad[1]), b.data_ptr(),
                                                  delta.data_ptr(), self._stream()), "cs_assemble_rhs")
         dx = torch.zeros((nf, 3), dtype=torch.float64, device="cuda")

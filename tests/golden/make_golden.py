@@ -177,6 +177,68 @@ def dbb_fixture(steps=18):
     traj_fixture("sphere14_dbb", "sphere_drape", steps, {"barrier_mode": "dbb"}, resolution=14, size=0.2)
 
 
+def stages_fixture():
+    """Module-level stage helpers the drop-in re-exports (collision/__init__.py,
+    oracles.py): coplanarity coefficients (batched and single-pair BLAS paths), query_q
+    (shared and per-pair samples), closest points, swept boxes, DBB weights, the float
+    SAT on near-degenerate pairs (+ the exact rational verdict), lattice samples."""
+    from clothsim.collision import (coplanarity_coefficients, dbb_weight, dbb_weight_gradient,
+                                    lattice_samples, point_triangle_closest, query_q,
+                                    segment_segment_closest, swept_boxes)
+    from clothsim.oracles import tri_tri_intersect, tri_tri_intersect_exact
+
+    rng = np.random.default_rng(11)
+    n = 2000
+    kind = (rng.random(n) < 0.5).astype(np.int8)
+    x0 = rng.uniform(-1.0, 1.0, size=(4 * n, 3))
+    x1 = x0 + 0.3 * rng.normal(size=(4 * n, 3))
+    idx = np.arange(4 * n).reshape(n, 4)
+    out = dict(kind=kind, idx=idx, x0=x0, x1=x1)
+    out["coef"] = coplanarity_coefficients(kind, idx, x0, x1)
+    out["coef_single"] = np.stack([coplanarity_coefficients(kind[i:i + 1], idx[:1], x0[4 * i:4 * i + 4],
+                                                            x1[4 * i:4 * i + 4])[0] for i in range(50)])
+    lam_shared = np.array([[0.25, 0.25], [0.5, 0.1], [0.1, 0.7]])
+    lam_pair = rng.uniform(0.0, 0.5, size=(n, 4, 2))
+    out.update(lam_shared=lam_shared, lam_pair=lam_pair, q_shared=query_q(kind, idx, x0, x1, lam_shared),
+               q_pair=query_q(kind, idx, x0, x1, lam_pair))
+    q = x0[idx]
+    out["ptc"] = np.concatenate([np.asarray(a).reshape(n, -1) for a in point_triangle_closest(q[:, 0], q[:, 1],
+                                                                                            q[:, 2], q[:, 3])], 1)
+    out["ssc"] = np.concatenate([np.asarray(a).reshape(n, -1) for a in segment_segment_closest(q[:, 0], q[:, 1],
+                                                                                             q[:, 2], q[:, 3])], 1)
+    lo, hi = swept_boxes(x0[idx], x1[idx], 1e-3)
+    out.update(sb_lo=lo, sb_hi=hi)
+    d = np.concatenate([10.0 ** rng.uniform(-9, -2, 500), [1e-3, 2e-3]])
+    out.update(dbb_d=d, dbb_w=dbb_weight(d, 1e-3, 3.0), dbb_g=dbb_weight_gradient(d, 1e-3, 3.0))
+    # near-degenerate SAT pairs (the reference's tests/test_harness.py:_near_degenerate_pairs
+    # mix: coplanar-offset, shared edge, vertex on plane, generic small separation)
+    m = 1500
+    p = rng.uniform(-1.0, 1.0, size=(m, 3, 3))
+    qq = np.empty_like(p)
+    mode = rng.integers(0, 4, size=m)
+    for i in range(m):
+        if mode[i] == 0:
+            qq[i] = p[i][[1, 2, 0]] + rng.normal(scale=1e-9, size=(3, 3))
+        elif mode[i] == 1:
+            qq[i, 0], qq[i, 1], qq[i, 2] = p[i, 0], p[i, 1], rng.uniform(-1.0, 1.0, size=3)
+        elif mode[i] == 2:
+            nrm = np.cross(p[i, 1] - p[i, 0], p[i, 2] - p[i, 0])
+            nrm /= np.linalg.norm(nrm)
+            base = p[i, 0] + 0.3 * (p[i, 1] - p[i, 0]) + 0.3 * (p[i, 2] - p[i, 0])
+            qq[i, 0] = base
+            qq[i, 1] = base + rng.uniform(-0.5, 0.5, size=3)
+            qq[i, 2] = base + rng.uniform(-0.5, 0.5, size=3)
+        else:
+            qq[i] = p[i] + rng.normal(scale=1e-3, size=(3, 3))
+    p, qq = np.round(p, 6), np.round(qq, 6)
+    out.update(sat_p=p, sat_q=qq, sat=tri_tri_intersect(p, qq),
+               sat_exact=np.array([tri_tri_intersect_exact(p[i], qq[i]) for i in range(m)]))
+    for dom in ("triangle", "box"):
+        for iv in (0.3, 0.1):
+            out[f"lattice_{dom}_{iv}"] = lattice_samples(iv, dom)
+    save("stages.npz", **out)
+
+
 def two_corner_fixture(steps=20):
     """BASELINE config 1: 64x64 grid pinned at two corners, h = 1/200."""
     v, t = grid_cloth(64, 1.0)
@@ -275,6 +337,7 @@ if __name__ == "__main__":
     traj_fixture("twist10", "twist", 6, {}, resolution=10, size=0.3)
     two_corner_fixture()
     sphere_ground_fixture()
+    stages_fixture()
     contact_state_fixture()
     dbb_fixture()
     io_fixture()

@@ -58,7 +58,7 @@ def test_assemble_rhs_bitwise(sim, rng):
     for with_coll in (False, True):
         args = (_dev(ids.astype(np.int32)), _dev(w), _dev(t)) if with_coll else None
         lib = sim._lib
-        rc = lib.cs_assemble_rhs(sim._scene, _dev(z).data_ptr(), _dev(x).data_ptr(),
+        rc = lib.cs_assemble_rhs(sim._scene, _dev(z).data_ptr(), _dev(x).data_ptr(), None,
                                  args[0].data_ptr() if args else None, args[1].data_ptr() if args else None,
                                  args[2].data_ptr() if args else None, len(ids) if args else 0,
                                  b.data_ptr(), d.data_ptr(), _lib.stream_handle())

@@ -137,3 +137,42 @@ def test_trajectory_golden(tag, kind, cfg_kw, scene_kw):
         rep = o.step()
         assert rep["lg_iterations"] == g["lg"][s]
         assert np.abs(o.state.x - g["x"][s]).max() <= 1e-12, (tag, s)
+
+
+def test_intersection_oracle_pinned_to_reference_counts():
+    """oracle/intersect.py against the reference's own per-step intersection counts of
+    its 25-step sphere drape (tests/golden/contact_sphere14.npz: oracle_intersect run by
+    the reference on its states; steps 22-24 carry its transient intersections)."""
+    from oracle.intersect import intersecting_pairs
+    from paper_2403_19272_b200 import StepConfig
+    from paper_2403_19272_b200.scenes import scene_parts
+
+    g = golden("contact_sphere14.npz")
+    parts = scene_parts("sphere_drape", resolution=14, size=0.2, config=StepConfig())
+    n = parts["mesh"].vertex_count
+    ov, ot = parts["obstacles"][0]
+    tris = np.concatenate([parts["mesh"].triangles, np.asarray(ot) + n])
+    counts = g["intersections"]
+    assert counts.max() > 0
+    for s in range(len(counts)):
+        xw = np.concatenate([g["x"][s + 1], g["obstacle_x"][s + 1]])
+        assert len(intersecting_pairs(xw, tris)) == counts[s], s
+
+
+def test_float_sat_golden_and_exact_arithmetic():
+    """The float 17-axis SAT restatement reproduces the reference's verdicts on its
+    near-degenerate pair mix bit for bit, and is conservative against the exact rational
+    test as the reference requires (tests/test_harness.py:166-181)."""
+    from oracle.intersect import exact_separation_margin, tri_tri_intersect, tri_tri_intersect_exact
+
+    g = golden("stages.npz")
+    p, q = g["sat_p"], g["sat_q"]
+    got = tri_tri_intersect(p, q)
+    assert np.array_equal(got, g["sat"])
+    for i in range(0, len(p), 5):
+        ex = tri_tri_intersect_exact(p[i], q[i])
+        assert ex == bool(g["sat_exact"][i])
+        if got[i] != ex:
+            assert got[i] and not ex
+            scale = float(np.abs(np.concatenate([p[i], q[i]])).max()) + 1.0
+            assert exact_separation_margin(p[i], q[i]) <= 1e-12 * scale
