@@ -178,7 +178,8 @@ def assemble_rhs(system: GlobalSystem, mesh: ClothMesh, elastic: ElasticConstrai
     nf = mesh.free.size
     b = torch.empty((nf, 3), dtype=torch.float64, device="cuda")
     delta = torch.empty(nf, dtype=torch.float64, device="cuda")
-    _lib.check(ctx.lib.cs_assemble_rhs(ctx.ptr, dev(z).data_ptr(), dev(x).data_ptr(),
+    zd, xd = dev(z), dev(x)   # keep the device copies alive across the call
+    _lib.check(ctx.lib.cs_assemble_rhs(ctx.ptr, zd.data_ptr(), xd.data_ptr(),
                                        pins.data_ptr() if pins is not None else None,
                                        ids.data_ptr() if coll else None, w.data_ptr() if coll else None,
                                        t.data_ptr() if coll else None, int(len(collision_vertices)) if coll else 0,
