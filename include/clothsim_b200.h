@@ -90,7 +90,10 @@ typedef struct {
     int warm_start_cap, inner_cap, outer_cap, rf_iterations;
     double dbb_kappa;
     int barrier_mode;
+    int smoother;  /* CS_SMOOTHER_AJACOBI (reference) or CS_SMOOTHER_CHEBYSHEV (opt-in) */
 } cs_step_config;
+#define CS_SMOOTHER_AJACOBI 0
+#define CS_SMOOTHER_CHEBYSHEV 1
 
 /* Mirrors reference StepReport (stepper.py:81-92) + device-side diagnostics. */
 typedef struct {

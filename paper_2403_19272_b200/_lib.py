@@ -46,7 +46,8 @@ class StepConfigC(ctypes.Structure):
         "ndb_k", "ndb_base", "d_hat", "omega", "rf_tolerance", "delta_f_cap")] + [
         (name, ctypes.c_int) for name in (
             "iteration_cap", "samples", "smoothing_iterations", "warm_start_cap", "inner_cap", "outer_cap",
-            "rf_iterations")] + [("dbb_kappa", ctypes.c_double), ("barrier_mode", ctypes.c_int)]
+            "rf_iterations")] + [("dbb_kappa", ctypes.c_double), ("barrier_mode", ctypes.c_int),
+                                 ("smoother", ctypes.c_int)]
 
 
 class StepReportC(ctypes.Structure):

@@ -387,7 +387,49 @@ struct cs_scene {
         }
     }
 
+    // Chebyshev-accelerated Jacobi (StepConfig.smoother = "chebyshev", opt-in): `iterations`
+    // fused SELL passes (the same SpMV count as the A-Jacobi's rank-2 steps) over three
+    // rotating x buffers; interval [max(1 - rho, 0.02), 1 + rho] from the Gershgorin
+    // radius rho of D^-1 H (computed once per scene: delta >= 0 only shrinks it).
+    double cheb_rho = -1.0;
+    DBuf<double> cheb_b1, cheb_b2;
+    void cheb_launch(cudaStream_t st, const double* bb, double* xx, int iterations, const double* dl) {
+        const double lmax = 1.0 + cheb_rho, lmin = std::max(1.0 - cheb_rho, 0.02);
+        const double g = 2.0 / (lmax + lmin), sg = (lmax - lmin) / (lmax + lmin);
+        const int g2 = grid(nf, 128);
+        double* buf[3] = {xx, cheb_b1.p, cheb_b2.p};
+        double w = 1.0;
+        int cur = 0, prev = 0;
+        for (int k = 0; k < iterations; ++k) {
+            if (k == 1) w = 1.0 / (1.0 - 0.5 * sg * sg);
+            else if (k > 1) w = 1.0 / (1.0 - 0.25 * sg * sg * w);
+            const int nxt = (cur + 1) % 3 == prev ? (cur + 2) % 3 : (cur + 1) % 3;
+            const bool chk = (k % 20) == 0;
+            k_cheb_step<<<g2, 128, 0, st>>>(sell(), diag.p, dl, bb, buf[cur], buf[prev], w, g, buf[nxt],
+                                            chk ? spart.p : nullptr);
+            if (chk) k_norm_final<<<1, 256, 0, st>>>(spart.p, g2, norms.p + k / 20);
+            prev = cur;
+            cur = nxt;
+        }
+        if (cur != 0) cudaMemcpyAsync(xx, buf[cur], sizeof(double) * 3 * nf, cudaMemcpyDeviceToDevice, st);
+    }
+    int cheb_bounds() {
+        if (cheb_rho >= 0.0) return 0;
+        const int g = grid(nf);
+        CS_RET(part.ensure(g));
+        k_gershgorin<<<g, 256, 0, s>>>(sell(), diag.p, part.p);
+        CS_CHECK_LAUNCH();
+        std::vector<double> hp(g);
+        CS_TRY(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * g, cudaMemcpyDeviceToHost, s));
+        CS_TRY(hsync());
+        double rho = 0.0;
+        for (double v : hp) rho = std::max(rho, v);
+        cheb_rho = rho;
+        return 0;
+    }
+
     int smooth(const double* bb, double* xx, int iterations, double omega, const double* dl) {
+        if (cfg.smoother == CS_SMOOTHER_CHEBYSHEV) return smooth_cheb(bb, xx, iterations, dl);
         const int steps = (iterations + 1) / 2;
         const double c = 1.0 - omega;
         CS_RET(spart.ensure(grid(nf, 128)));
@@ -415,6 +457,40 @@ struct cs_scene {
             smooth_graphs.erase(smooth_graphs.begin());
         }
         smooth_graphs.push_back(SmoothGraph{bb, xx, dl, spart.p, norms.p, steps, c, exec});
+        CS_TRY(cudaGraphLaunch(exec, s));
+        return 0;
+    }
+
+    int smooth_cheb(const double* bb, double* xx, int iterations, const double* dl) {
+        CS_RET(cheb_bounds());
+        CS_RET(spart.ensure(grid(nf, 128)));
+        CS_RET(cheb_b1.ensure(3LL * nf));
+        CS_RET(cheb_b2.ensure(3LL * nf));
+        const int nchk = (iterations + 19) / 20;
+        CS_RET(norms.ensure(std::max(nchk, 1)));
+        launches += iterations + nchk;
+        pending_checks = nchk;
+        const double c = -1.0;  // graph-cache tag for the Chebyshev sequence
+        for (auto& sg : smooth_graphs)
+            if (sg.bb == bb && sg.xx == xx && sg.dl == dl && sg.part == spart.p && sg.norms == norms.p &&
+                sg.steps == iterations && sg.c == c) {
+                CS_TRY(cudaGraphLaunch(sg.exec, s));
+                return 0;
+            }
+        if (!cap_stream) CS_TRY(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+        cudaGraph_t graph;
+        CS_TRY(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+        cheb_launch(cap_stream, bb, xx, iterations, dl);
+        CS_TRY(cudaStreamEndCapture(cap_stream, &graph));
+        cudaGraphExec_t exec;
+        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CS_TRY(e);
+        if (smooth_graphs.size() >= 8) {
+            cudaGraphExecDestroy(smooth_graphs.front().exec);
+            smooth_graphs.erase(smooth_graphs.begin());
+        }
+        smooth_graphs.push_back(SmoothGraph{bb, xx, dl, spart.p, norms.p, iterations, c, exec});
         CS_TRY(cudaGraphLaunch(exec, s));
         return 0;
     }
@@ -1439,6 +1515,8 @@ void cs_scene::release() {
     ftbox.release();
     febox.release();
     stamp.release();
+    cheb_b1.release();
+    cheb_b2.release();
     hkeys.release();
     cub_tmp.release();
     pa.release();

@@ -248,6 +248,65 @@ __global__ void k_jacobi_b(Sell H, const double* __restrict__ diag, const double
     st3(x, i, ld3(x, i) + upd);
 }
 
+// ---------------------------------------------------------------- Chebyshev (opt-in)
+// Chebyshev-accelerated Jacobi for (H + delta) x = b, D = diag + delta: one fused SELL
+// pass per iteration - SpMV, the Jacobi residual step, the three-term Chebyshev
+// extrapolation and (when norm_part) the residual-norm block partials:
+//   x_{k+1} = w_{k+1} (g D^-1 (b - (H + delta) x_k) + x_k - x_{k-1}) + x_{k-1}
+// (x_{-1} = x_0, w_1 = 1).  Not the reference's smoother: opt-in only.
+__global__ void k_cheb_step(Sell H, const double* __restrict__ diag, const double* __restrict__ delta,
+                            const double* __restrict__ b, const double* __restrict__ xk,
+                            const double* __restrict__ xkm1, double w, double g, double* __restrict__ xk1,
+                            double* __restrict__ norm_part) {
+    __shared__ double red[8];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double r2 = 0.0;
+    if (i < H.nrows) {
+        const d3 hx = sell_row(H, i, xk);
+        const double dl = delta[i];
+        const double inv = 1.0 / (diag[i] + dl);
+        const d3 xi = ld3(xk, i), xp = ld3(xkm1, i);
+        const d3 r = ld3(b, i) - (hx + dl * xi);
+        st3(xk1, i, w * ((g * (inv * r) + xi) - xp) + xp);
+        if (norm_part) r2 = fma(r.z, r.z, fma(r.y, r.y, r.x * r.x));
+    }
+    if (norm_part) {
+        for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = r2;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+            if (threadIdx.x == 0) norm_part[blockIdx.x] = s;
+        }
+    }
+}
+
+// Gershgorin radius of D^-1 H: max_i sum_{j != i} |h_ij| / h_ii (block maxima); the
+// Chebyshev interval is [1 - rho, 1 + rho] (delta >= 0 only shrinks it)
+__global__ void k_gershgorin(Sell H, const double* __restrict__ diag, double* __restrict__ part) {
+    __shared__ double sm[256];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double rho = 0.0;
+    if (i < H.nrows) {
+        const int s = i >> 5, lane = i & 31;
+        const int beg = H.slice_ptr[s], width = (H.slice_ptr[s + 1] - beg) >> 5;
+        double off = 0.0;
+        for (int k = 0; k < width; ++k) {
+            const int c = H.col[beg + 32 * k + lane];
+            if (c >= 0 && c != i) off += fabs(H.val[beg + 32 * k + lane]);
+        }
+        rho = off / diag[i];
+    }
+    sm[threadIdx.x] = rho;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+
 // out = x + c t (jacobi_step's update, smoothing.py:78)
 __global__ void k_axpy_step(const double* __restrict__ x, const double* __restrict__ t, double c, int64_t n,
                             double* __restrict__ out) {

@@ -74,6 +74,7 @@ def step_config_c(cfg, k: float, kappa: float = 0.0) -> _lib.StepConfigC:
         setattr(c, name, int(getattr(cfg, name)))
     c.dbb_kappa = float(kappa)
     c.barrier_mode = 1 if cfg.barrier_mode == "dbb" else 0
+    c.smoother = 1 if getattr(cfg, "smoother", "ajacobi") == "chebyshev" else 0
     return c
 
 

@@ -34,6 +34,10 @@ class StepConfig:
     r_bar: int = 120
     r: int = 30
     verify: bool = False
+    # opt-in (not the reference's smoother; SPEC.md:407 lists Chebyshev as a non-goal):
+    # "chebyshev" replaces the rank-2 A-Jacobi updates by Chebyshev-accelerated Jacobi
+    # iterations, one fused SELL pass each; "ajacobi" (default) is the parity path
+    smoother: str = "ajacobi"
 
     def __post_init__(self):
         if self.h <= 0 or not (0 < self.alpha < 1):
@@ -43,6 +47,8 @@ class StepConfig:
                 raise ValueError(f"{name} must be positive")
         if self.barrier_mode not in ("ndb", "dbb"):
             raise ValueError("barrier_mode must be 'ndb' or 'dbb'")
+        if self.smoother not in ("ajacobi", "chebyshev"):
+            raise ValueError("smoother must be 'ajacobi' or 'chebyshev'")
 
 
 @dataclass

@@ -184,3 +184,36 @@ def test_energy_gradient_close(sim, rng):
         er, gr, _ = O.energy(mesh, sim.elastic, sim.config.h, x, z, None if quad is None else quad[1:])
         assert np.isclose(e, er, rtol=1e-12)
         assert np.abs(g - gr).max() <= 1e-11 * max(np.abs(gr).max(), 1.0)
+
+
+def test_chebyshev_smoother_opt_in(cuda, rng):
+    """StepConfig(smoother="chebyshev") (opt-in; the reference's smoother is the rank-2
+    A-Jacobi): on the cloth system with a collision diagonal, the same
+    number of SpMV passes leaves a smaller residual than A-Jacobi, and a contact run in
+    that mode stays penetration free (device intersection check every step)."""
+    import dataclasses
+
+    import paper_2403_19272_b200 as P
+    from paper_2403_19272_b200 import _lib
+
+    sims = {}
+    res = {}
+    for mode in ("ajacobi", "chebyshev"):
+        sim = P.build_scene("sphere_drape", resolution=24, size=0.3, config=P.StepConfig(smoother=mode))
+        sims[mode] = sim
+        nf = sim.mesh.free.size
+        r2 = np.random.default_rng(5)
+        b = r2.normal(size=(nf, 3))
+        delta = np.where(r2.random(nf) < 0.2, r2.uniform(0, 500, nf), 0.0)
+        xd = _dev(np.zeros((nf, 3)))
+        _lib.check(sim._lib.cs_ajacobi_smooth(sim._scene, _dev(b).data_ptr(), xd.data_ptr(), 32, 0.0,
+                                              _dev(delta).data_ptr(), _lib.stream_handle()))
+        x = xd.cpu().numpy()
+        H = sim.system.H
+        res[mode] = np.linalg.norm(b - H @ x - delta[:, None] * x) / np.linalg.norm(b)
+    assert res["chebyshev"] < res["ajacobi"], res
+    sim = sims["chebyshev"]
+    sim.config = dataclasses.replace(sim.config, verify=True)
+    for _ in range(12):
+        r = sim.step()
+        assert r.penetration_free
