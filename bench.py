@@ -601,6 +601,11 @@ def run_ours(args, ws, rank, local):
         s0.obstacle_x = ob
         base_cfg = s0.config
         s0.config = dataclasses.replace(base_cfg, eps_inner=1e-9, eps_outer=1e-9, iteration_cap=67)
+        # one untimed step first (buffers of the 67-iteration regime sized once), then the
+        # same snapshot again
+        s0.step()
+        s0.state = st
+        s0.obstacle_x = ob
         preps = []
         torch.cuda.synchronize()
         q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -614,11 +619,13 @@ def run_ours(args, ws, rank, local):
         s0.config = base_cfg
         ms = q0.elapsed_time(q1) / len(preps)
         lgp = float(np.mean([r.lg_iterations for r in preps]))
-        paper = {"config": "StepConfig(eps_inner=1e-9, eps_outer=1e-9, iteration_cap=67), same snapshot",
+        paper = {"config": "StepConfig(eps_inner=1e-9, eps_outer=1e-9, iteration_cap=67), same snapshot "
+                           "(one untimed warm-up step from it first)",
                  "steps": len(preps),
                  "ms_per_step": ms, "fps": 1e3 / ms, "lg_iterations_per_step": lgp,
                  "ms_per_lg_iteration": ms / max(lgp, 1.0), "paper_fps": PAPER_FPS,
                  "host_syncs_per_step": float(np.mean([c.host_syncs for c in creps])),
+                 "stamp_plan_reuses_per_step": float(np.mean([c.stamp_plan_reuses for c in creps])),
                  "stages_ms_per_frame": {k: float(np.mean([r.timings[k] for r in preps]))
                                          for k in ("warm_start", "local", "global", "smoothing", "broad",
                                                    "narrow_partial", "narrow_full", "rf")}}

@@ -111,6 +111,8 @@ typedef struct {
     int subset_sites;           /* moving CCD sites served from the step's base site (+ violator queries) */
     int verified_sites;         /* subset / motion-free sites re-checked against a full broad phase (CS_VERIFY_STATIC_SITE) */
     int host_syncs;             /* host<->device synchronisations inside this cs_step */
+    int stamp_plan_reuses;      /* LG iterations whose collision stamps reused the cached row order
+                                   (engaged set unchanged since the previous rhs) */
 } cs_step_report;
 
 /* ---- scene lifetime ---------------------------------------------------- */

@@ -11,6 +11,7 @@
 //
 // Single translation unit (unity build) so kernels stay in one module.
 #include <cub/cub.cuh>
+#include <cub/device/device_merge.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -106,6 +107,22 @@ struct DBuf {
             return 1000 + (int)e;
         }
         n = want;
+        return 0;
+    }
+    // grow to >= m elements keeping the first `used` (stream-ordered copy)
+    int grow_keep(size_t m, size_t used) {
+        if (m <= n && p) return 0;
+        T* old = p;
+        p = nullptr;
+        n = 0;
+        CS_RET(ensure(2 * m, true));
+        if (old) {
+            if (used) {
+                cudaError_t e = cudaMemcpyAsync(p, old, used * sizeof(T), cudaMemcpyDeviceToDevice, t_alloc_stream);
+                if (e != cudaSuccess) return 1000 + (int)e;
+            }
+            cudaFreeAsync(old, t_alloc_stream);
+        }
         return 0;
     }
     int upload(const T* host, size_t m) {
@@ -206,7 +223,7 @@ struct PairBuf {
 enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_NORM1 = 5, S_NORM_F = 6,
        S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_MINBITS = 10, S_COUNT = 16 };
 enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_FLAG = 7, I_WLF = 8,
-       I_COUNT = 10 };
+       I_NEW = 9, I_COUNT = 10 };
 
 const int kStages = 8;
 enum { T_WARM = 0, T_LOCAL, T_GLOBAL, T_SMOOTH, T_BROAD, T_PARTIAL, T_FULL, T_RF };
@@ -286,6 +303,24 @@ struct cs_scene {
     int sm_count = 148;
     bool stamps_valid = false;   // seg_beg/seg_end hold stamps for the current rhs
     int n_stamp_rows = 0;
+    // stamp plan (engaged-pair list `sel`, row-sorted entry permutation, row segments,
+    // active rows) of pair set plan_pr: valid while that set's engaged mask is unchanged
+    // (k_partial_ndb raises I_FLIP on any change; every site engagement drops it)
+    // The plan is a superset: pairs that leave the engaged set keep their entries (w = 0,
+    // skipped); pairs that join (counted into I_NEW by k_partial_ndb) are merged in.
+    bool plan_valid = false;
+    const PairBuf* plan_pr = nullptr;
+    long long plan_U = 0;        // pairs in the plan (sel[0, plan_U))
+    long long plan_M = 0;        // plan entries (row-sorted, incl. trailing sentinels)
+    long long plan_new = 0;      // engaged pairs outside the plan at the last partial CCD
+    long long plan_reuses = 0;
+    bool rows_from_delta = false;  // rows_act must be rebuilt from delta after the rhs
+    bool plan_enabled = std::getenv("CS_NO_STAMP_PLAN") == nullptr;  // read at scene creation
+    DBuf<unsigned long long> pkey, pkey2, nkey, nkey_s;
+    DBuf<int> psrc2, nsrc, nsrc_s, newsel, pdst;
+    DBuf<double4> stamp_p;          // stamps in plan (row-sorted) order, written by reuse iterations
+    bool stamps_plan_order = false;  // the current rhs streams stamp_p instead of gathering stamp
+    DBuf<uint8_t> inplan, rowpos;
 
     // ------------------------------------------------------------ utilities
     cudaEvent_t ev() {
@@ -343,7 +378,8 @@ struct cs_scene {
         const int* sb = with_stamps ? seg_beg.p : nullptr;
         k_assemble_rhs<<<grid(nf), 256, 0, s>>>(nf, free_ids.p, xcl, zc, mh2.p, edges(), rinc_ptr.p, rinc.p,
                                                 has_fp ? hfp_ptr.p : nullptr, hfp_col.p, hfp_val.p, xcl, sb,
-                                                seg_end.p, ssrc_s.p, stamp.p, b.p, delta.p);
+                                                seg_end.p, stamps_plan_order ? nullptr : ssrc_s.p,
+                                                stamps_plan_order ? stamp_p.p : stamp.p, b.p, delta.p);
         ++launches;
         CS_CHECK_LAUNCH();
         return 0;
@@ -1146,6 +1182,7 @@ struct cs_scene {
 
     // engaged set + weights after a site; count lands in I_ENG
     int engage(PairBuf& pr) {
+        plan_valid = false;
         CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
         if (pr.P == 0) return 0;
         if (cfg.barrier_mode == CS_BARRIER_DBB)  // log barrier of the witness distance (stepper.py:489-491)
@@ -1188,7 +1225,33 @@ struct cs_scene {
     // collision stamps from engaged pairs at world positions xw (stepper.py:238-285);
     // A = number of engaged pairs (known on host).  Fills seg_beg/seg_end, rows_act.
     int stamps(PairBuf& pr, long long A, const double* xw) {
+        if (plan_valid && plan_pr == &pr && A > 0 && stamps_valid) {
+            if (plan_new > 0) {
+                // a union drifting far from the engaged set costs more per iteration than a
+                // rebuild; an overflowing append list means the list is incomplete
+                if (plan_new <= (long long)newsel.n && plan_U + plan_new <= A + A / 2 + (1 << 16))
+                    CS_RET(plan_extend(pr, plan_new));
+                else
+                    plan_valid = false;
+                plan_new = 0;
+            }
+            if (plan_valid) {
+                // same row order: only the stamp payload (targets at xw, weights) changes
+                CS_RET(stamp_p.ensure(plan_M));
+                k_collision_terms<<<grid(plan_U), 256, 0, s>>>(sel.p, plan_U, pr.kind.p, pr.idx.p, xw, pr.bary.p,
+                                                               pr.normal.p, pr.weight.p, cfg.d_hat, n,
+                                                               free_index.p, 0, nullptr, stamp_p.p, pdst.p);
+                stamps_plan_order = true;
+                ++launches;
+                ++plan_reuses;
+                rows_from_delta = true;
+                CS_CHECK_LAUNCH();
+                return 0;
+            }
+        }
+        plan_valid = false;
         stamps_valid = false;
+        stamps_plan_order = false;
         n_stamp_rows = 0;
         CS_TRY(cudaMemsetAsync(seg_beg.p, 0, sizeof(int) * nf, s));
         CS_TRY(cudaMemsetAsync(seg_end.p, 0, sizeof(int) * nf, s));
@@ -1210,7 +1273,8 @@ struct cs_scene {
         CS_RET(cub_tmp.ensure(bytes));
         CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, pr.engaged.p, sel.p, d_iscal.p + I_BAD, (int)pr.P, s));
         k_collision_terms<<<grid(A), 256, 0, s>>>(sel.p, A, pr.kind.p, pr.idx.p, xw, pr.bary.p, pr.normal.p,
-                                                  pr.weight.p, cfg.d_hat, n, free_index.p, 0, skey.p, stamp.p);
+                                                  pr.weight.p, cfg.d_hat, n, free_index.p, 0, skey.p, stamp.p,
+                                                  nullptr);
         ++launches;
         // entries on a free row (a third of them are not: obstacle / pinned endpoints,
         // zero weight), compacted in order: indices, then their keys
@@ -1251,6 +1315,85 @@ struct cs_scene {
         CS_CHECK_LAUNCH();
         stamps_valid = true;
         n_stamp_rows = (int)std::min<long long>(m, nf);  // upper bound; exact count read on device
+        rows_from_delta = false;
+        if (plan_enabled && cfg.barrier_mode != CS_BARRIER_DBB && &pr == cur) {
+            // cache the plan for the next LG iterations on this pair set
+            CS_RET(pkey.ensure(mc));
+            CS_RET(pdst.ensure(m));
+            CS_TRY(cudaMemsetAsync(pdst.p, 0xff, sizeof(int) * m, s));
+            k_plan_keys<<<grid(mc), 256, 0, s>>>(skey_s.p, ssrc_s.p, sel.p, (int)mc, pkey.p, pdst.p);
+            CS_RET(inplan.ensure(pr.P));
+            CS_TRY(cudaMemcpyAsync(inplan.p, pr.engaged.p, pr.P, cudaMemcpyDeviceToDevice, s));
+            CS_RET(newsel.ensure(std::max<long long>(pr.P / 8, 1 << 16)));
+            ++launches;
+            CS_CHECK_LAUNCH();
+            plan_valid = true;
+            plan_pr = &pr;
+            plan_U = A;
+            plan_M = mc;
+            plan_new = 0;
+        }
+        return 0;
+    }
+
+    // merge the N pairs that joined the engaged set into the cached plan: append them to
+    // the plan's pair list, sort their entries by merge key, merge with the plan's
+    // entries, rebuild the row segments (sentinels trail)
+    int plan_extend(PairBuf& pr, long long N) {
+        int rb = 1;
+        while ((1LL << rb) <= (long long)nf) ++rb;
+        const int end_bit = kPlanRowShift + rb;
+        const unsigned long long sentinel = (1ull << end_bit) - 1;
+        const long long m4 = 4 * N;
+        CS_RET(sel.grow_keep(plan_U + N, plan_U));
+        CS_RET(nkey.ensure(m4));
+        CS_RET(nsrc.ensure(m4));
+        CS_RET(nkey_s.ensure(m4));
+        CS_RET(nsrc_s.ensure(m4));
+        // the append order of newsel is arbitrary; the plan order is the merge key's
+        k_plan_new<<<grid(N), 256, 0, s>>>(newsel.p, (int)N, (int)plan_U, pr.kind.p, pr.idx.p, pr.bary.p, n,
+                                           free_index.p, sentinel, sel.p, inplan.p, nkey.p, nsrc.p);
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, nkey.p, nkey_s.p, nsrc.p, nsrc_s.p, (int)m4, 0, end_bit, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, nkey.p, nkey_s.p, nsrc.p, nsrc_s.p, (int)m4, 0,
+                                               end_bit, s));
+        const long long M2 = plan_M + m4;
+        CS_RET(pkey2.ensure(M2));
+        CS_RET(psrc2.ensure(M2));
+        bytes = 0;
+        cub::DeviceMerge::MergePairs(nullptr, bytes, pkey.p, ssrc_s.p, (int)plan_M, nkey_s.p, nsrc_s.p, (int)m4,
+                                     pkey2.p, psrc2.p, U64Less{}, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceMerge::MergePairs(cub_tmp.p, bytes, pkey.p, ssrc_s.p, (int)plan_M, nkey_s.p, nsrc_s.p,
+                                            (int)m4, pkey2.p, psrc2.p, U64Less{}, s));
+        std::swap(pkey, pkey2);
+        std::swap(ssrc_s, psrc2);
+        CS_TRY(cudaMemsetAsync(seg_beg.p, 0, sizeof(int) * nf, s));
+        CS_TRY(cudaMemsetAsync(seg_end.p, 0, sizeof(int) * nf, s));
+        CS_RET(pdst.ensure(4 * (plan_U + N)));
+        CS_TRY(cudaMemsetAsync(pdst.p, 0xff, sizeof(int) * 4 * (plan_U + N), s));
+        k_plan_segments<<<grid(M2), 256, 0, s>>>(pkey.p, ssrc_s.p, (int)M2, nf, seg_beg.p, seg_end.p, pdst.p);
+        launches += 4;
+        CS_CHECK_LAUNCH();
+        plan_U += N;
+        plan_M = M2;
+        return 0;
+    }
+
+    // rows_act = rows with delta > 0 (a plan reused across iterations can hold rows
+    // whose pairs all left the engaged set); same list as the fresh plan's
+    int rows_act_from_delta() {
+        CS_RET(rowpos.ensure(nf));
+        CS_RET(rows_act.ensure(nf));
+        k_flag_positive<<<grid(nf), 256, 0, s>>>(delta.p, nf, rowpos.p);
+        size_t bytes = 0;
+        cub::CountingInputIterator<int> it(0);
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, rowpos.p, rows_act.p, d_iscal.p + I_ROWS, nf, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, rowpos.p, rows_act.p, d_iscal.p + I_ROWS, nf, s));
+        ++launches;
+        CS_CHECK_LAUNCH();
         return 0;
     }
 
@@ -1259,6 +1402,7 @@ struct cs_scene {
         stage(T_LOCAL);
         CS_RET(stamps(*cur, A, xc_w.p));
         CS_RET(assemble_rhs(z.p, xc_w.p, stamps_valid));
+        if (stamps_valid && rows_from_delta) CS_RET(rows_act_from_delta());
         k_gather_rows<<<grid(nf), 256, 0, s>>>(xc_w.p, free_ids.p, nf, xf0.p);
         CS_TRY(cudaMemcpyAsync(xf.p, xf0.p, sizeof(double) * 3 * nf, cudaMemcpyDeviceToDevice, s));
         ++launches;
@@ -1534,6 +1678,7 @@ void cs_scene::release() {
 int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_report* rep) {
     launches = 0;
     n_syncs = 0;
+    const long long plan_reuses0 = plan_reuses;
     ev_used = 0;
     spans.clear();
     active_stage = -1;
@@ -1660,11 +1805,16 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             // partial CCD + NDB life-span update (stepper.py:511-523)
             stage(T_PARTIAL);
             CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
+            CS_TRY(cudaMemsetAsync(d_iscal.p + I_NEW, 0, sizeof(int), s));
+            const bool track = plan_valid && plan_pr == cur;  // collect pairs joining the stamp plan
             if (cur->P) {
                 k_partial_ndb<<<grid(cur->P, 128), 128, 0, s>>>(cur->kind.p, cur->idx.p, anchor_w.p, xc_w.p, cur->P,
                                                                 pat, cur->bary.p, cur->normal.p, cfg.d_hat, cfg.ndb_k,
                                                                 cfg.ndb_base, cur->life.p, cur->weight.p,
-                                                                cur->engaged.p, 0, nullptr, d_iscal.p + I_ENG);
+                                                                cur->engaged.p, 0, nullptr, d_iscal.p + I_ENG,
+                                                                track ? inplan.p : nullptr,
+                                                                track ? d_iscal.p + I_NEW : nullptr, newsel.p,
+                                                                (int)newsel.n, 1);
                 ++launches;
                 CS_CHECK_LAUNCH();
             }
@@ -1672,6 +1822,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             CS_RET(sync_scalars());
             dx_last = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
             A = h_iscal[I_ENG];
+            plan_new = h_iscal[I_NEW];
             if (cfg.iteration_cap && lg >= cfg.iteration_cap) {
                 cap_hit = true;
                 break;
@@ -1761,6 +1912,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         rep->gpu_launches = launches;
         CS_TRY(hsync());
         rep->host_syncs = n_syncs;
+        rep->stamp_plan_reuses = (int)(plan_reuses - plan_reuses0);
         double acc[kStages] = {0};
         for (auto& sp : spans) {
             float ms = 0.f;
@@ -2082,7 +2234,7 @@ int cs_partial_ccd(const int8_t* kind, const int* idx4, const double* x_start, c
     CS_TRY(cudaMemsetAsync(life.p, 0, sizeof(int) * P, s));
     k_partial_ndb<<<(int)((P + 127) / 128), 128, 0, s>>>(kind, (const int4*)idx4, x_start, x_end, P, tmp.pat, bary.p,
                                                          normal.p, -1.0, 1.0, 2.0, life.p, weight.p, eng.p, 1, active,
-                                                         nullptr);
+                                                         nullptr, nullptr, nullptr, nullptr, 0, 0);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(s));
     bary.release();
@@ -2208,6 +2360,7 @@ int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const double
         CS_RET(sc->ssrc.ensure(m));
         CS_RET(sc->skey_s.ensure(m));
         CS_RET(sc->ssrc_s.ensure(m));
+        sc->plan_valid = false;
         CS_RET(sc->stamp.ensure(m));
         CS_RET(sc->rowflag.ensure(m));
         k_pack_stamps<<<sc->grid(m), 256, 0, s>>>(coll_w, coll_t, m, sc->stamp.p);
@@ -2260,12 +2413,13 @@ int cs_collision_terms(cs_scene* sc, const int8_t* kind, const int* idx4, const 
     if (A == 0) return 0;
     const long long m = 4 * A;
     CS_RET(sc->skey.ensure(m));
+    sc->plan_valid = false;
     CS_RET(sc->stamp.ensure(m));
     CS_RET(sc->rowflag.ensure(m));
     CS_RET(sc->rows_act.ensure(m));
     k_collision_terms<<<sc->grid(A), 256, 0, s>>>(sc->sel.p, A, kind, (const int4*)idx4, x_world, bary, normal, weight,
                                                   sc->cfg.d_hat, sc->n, sc->free_index.p, 0, sc->skey.p,
-                                                  sc->stamp.p);
+                                                  sc->stamp.p, nullptr);
     CS_RET(sc->keep_flag.ensure(m));
     k_key_kept<<<sc->grid(m), 256, 0, s>>>(sc->skey.p, (int)m, sc->nf, sc->keep_flag.p);
     bytes = 0;
@@ -2430,6 +2584,7 @@ int cs_energy_gradient(cs_scene* sc, const double* x, const double* z, const int
         CS_RET(sc->ssrc.ensure(m));
         CS_RET(sc->skey_s.ensure(m));
         CS_RET(sc->ssrc_s.ensure(m));
+        sc->plan_valid = false;
         CS_RET(sc->stamp.ensure(m));
         CS_RET(sc->rowflag.ensure(m));
         k_pack_stamps<<<sc->grid(m), 256, 0, s>>>(q_w, q_t, m, sc->stamp.p);

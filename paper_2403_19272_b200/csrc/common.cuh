@@ -88,6 +88,7 @@ __device__ __forceinline__ void load_box(const double* __restrict__ box, int p, 
 // the result is order independent).
 __device__ __forceinline__ void block_count(bool flag, int* __restrict__ count) {
     __shared__ int sh_cnt[32];
+    __syncthreads();  // a previous block_count in the same kernel may still be reading sh_cnt
     const unsigned ballot = __ballot_sync(0xffffffffu, flag);
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) sh_cnt[w] = __popc(ballot);

@@ -812,16 +812,25 @@ __global__ void __launch_bounds__(128, 6) k_partial_ndb(const int8_t* __restrict
                               const double* __restrict__ normal, double d_hat, double k_ndb, double base,
                               int* __restrict__ life, double* __restrict__ weight,
                               uint8_t* __restrict__ engaged, int write_active, uint8_t* __restrict__ active_out,
-                              int* __restrict__ eng_count) {
+                              int* __restrict__ eng_count, const uint8_t* __restrict__ inplan,
+                              int* __restrict__ n_new, int* __restrict__ new_list, int new_cap,
+                              int proj_is_witness) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    bool eng = false;
+    bool eng = false, fresh = false;
     if (i < P) {
     const int kd = kind[i];
     const int4 id = idx[i];
     Corners s = gather4(xa, id), e = gather4(xc, id);
-    // projection sample: closest point at the interval start (partial.py:170-178)
+    const double w1 = bary[2 * i], w2 = bary[2 * i + 1];
+    // projection sample: closest point at the interval start (partial.py:170-178).  In the
+    // step the interval starts at the anchor, where the frozen witness (bary) was computed
+    // by the same closest-point routines on the same coordinates (stepper.py:483-487,
+    // 564-565 -> 511-516): proj_is_witness reuses it bit for bit.
     double pl1, pl2;
-    {
+    if (proj_is_witness) {
+        pl1 = w1;
+        pl2 = w2;
+    } else {
         d3 tmp1, tmp2;
         if (kd == CS_VT)
             pt_tri_closest(s.p[0], s.p[1], s.p[2], s.p[3], pl1, pl2, tmp1);
@@ -861,17 +870,31 @@ __global__ void __launch_bounds__(128, 6) k_partial_ndb(const int8_t* __restrict
     }
     // gap along the frozen witness direction at the candidate (stepper.py:218-236)
     d3 s1, s2;
-    witness_sides(kd, e, bary[2 * i], bary[2 * i + 1], s1, s2);
+    witness_sides(kd, e, w1, w2, s1, s2);
     const double gap = dot3(s1 - s2, ld3(normal, i));
     act = act || (gap < d_hat);
     int lf = act ? min(life[i] + 1, 64) : 0;
     eng = act || (gap < 2.0 * d_hat);
+    fresh = eng && inplan != nullptr && !inplan[i];
     life[i] = lf;
     engaged[i] = eng;
     weight[i] = eng ? ndb_weight(lf, k_ndb, base) : 0.0;
     if (write_active) active_out[i] = act;
     }
     if (eng_count != nullptr) block_count(eng, eng_count);
+    // engaged pairs outside the driver's stamp plan, appended (any order: the driver
+    // sorts their entries by merge key) for the plan merge
+    if (n_new != nullptr) {
+        const unsigned m = __ballot_sync(0xffffffffu, fresh);
+        if (m) {
+            const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(n_new, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            const int pos = base + __popc(m & ((1u << lane) - 1u));
+            if (fresh && pos < new_cap) new_list[pos] = (int)i;
+        }
+    }
 }
 
 // Engaged set and weights after a full-CCD site (stepper.py:483-487, 564-565).
@@ -892,12 +915,15 @@ __global__ void k_engage_init(const double* __restrict__ toi, const double* __re
 // Per engaged pair: 4 positional targets (stepper.py:238-285).  Entries for
 // immovable or zero-weight endpoints get key 0x7fffffff (sorted to the end).
 // frozen_k >= 0 selects residual forwarding's frozen weights (stepper.py:635-642).
+// key == nullptr: payload only, for every entry of the driver's cached stamp plan, at
+// its plan position plan_dst[o] (-1: not a plan entry; pairs no longer engaged get w = 0).
 __global__ void __launch_bounds__(256, 4) k_collision_terms(const int* __restrict__ sel, int64_t A, const int8_t* __restrict__ kind,
                                   const int4* __restrict__ idx, const double* __restrict__ xw,
                                   const double* __restrict__ bary, const double* __restrict__ normal,
                                   const double* __restrict__ weight, double d_hat, int n_cloth,
                                   const int* __restrict__ free_index, int cloth_only,
-                                  int* __restrict__ key, double4* __restrict__ stamp_out) {
+                                  int* __restrict__ key, double4* __restrict__ stamp_out,
+                                  const int* __restrict__ plan_dst) {
     int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (a >= A) return;
     const int i = sel[a];
@@ -948,8 +974,15 @@ __global__ void __launch_bounds__(256, 4) k_collision_terms(const int* __restric
         bool keep = mov[k] && (w > 0.0);
         if (cloth_only && ids[k] >= n_cloth) keep = false;
         int64_t o = 4 * a + k;
-        key[o] = keep ? free_index[ids[k]] : 0x7fffffff;
-        if (keep) stamp_out[o] = make_double4(tg.x, tg.y, tg.z, w);  // others are never read
+        if (key != nullptr) {
+            key[o] = keep ? free_index[ids[k]] : 0x7fffffff;
+            if (keep) stamp_out[o] = make_double4(tg.x, tg.y, tg.z, w);  // others are never read
+        } else {
+            // plan entry (its pair may have left the engaged set: w = 0, skipped by the rhs),
+            // written at its row-sorted plan position so the rhs streams the stamps
+            const int j = plan_dst[o];
+            if (j >= 0) stamp_out[j] = make_double4(tg.x, tg.y, tg.z, w);
+        }
     }
 }
 

@@ -100,6 +100,97 @@ __global__ void k_mark_segments(const int* __restrict__ skey, int m, int nrows, 
     if (j == m - 1 || skey[j + 1] != k) seg_end[k] = j + 1;
 }
 
+// ---- stamp plan (driver-cached row order of the collision stamps, reused across the
+// LG iterations of one pair set).  Plan entries are ordered by the merge key
+// row << 34 | pair << 2 | slot, i.e. by free row and, within a row, in pair order
+// (np.add.at order over the engaged pairs: entries of pairs that are not engaged carry
+// w = 0 and are skipped by every consumer).
+constexpr int kPlanRowShift = 34;
+
+// merge keys of the row-sorted entries of a freshly built plan
+// (+ the plan position of every entry slot: dst[src] = j, -1 elsewhere by a memset)
+__global__ void k_plan_keys(const int* __restrict__ skey_s, const int* __restrict__ ssrc_s,
+                            const int* __restrict__ sel, int m, unsigned long long* __restrict__ pkey,
+                            int* __restrict__ dst) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const int src = ssrc_s[j];
+    pkey[j] = ((unsigned long long)skey_s[j] << kPlanRowShift) | ((unsigned long long)sel[src >> 2] << 2) |
+              (unsigned long long)(src & 3);
+    dst[src] = j;
+}
+
+__global__ void k_plan_flag_new(const uint8_t* __restrict__ engaged, const uint8_t* __restrict__ inplan, int64_t P,
+                                uint8_t* __restrict__ flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < P) flag[i] = engaged[i] && !inplan[i];
+}
+
+// pairs newly engaged during the plan's lifetime: appended to the plan's pair list
+// (sel[U0 + j]); their four entries get merge keys (or the sentinel when the slot can
+// never stamp: immovable endpoint or clipped barycentric weight 0, as k_collision_terms)
+__global__ void k_plan_new(const int* __restrict__ newsel, int N, int U0, const int8_t* __restrict__ kind,
+                           const int4* __restrict__ idx, const double* __restrict__ bary, int n_cloth,
+                           const int* __restrict__ free_index, unsigned long long sentinel, int* __restrict__ sel,
+                           uint8_t* __restrict__ inplan, unsigned long long* __restrict__ nkey,
+                           int* __restrict__ nsrc) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    const int i = newsel[j];
+    sel[U0 + j] = i;
+    inplan[i] = 1;
+    const int kd = kind[i];
+    const int4 id = idx[i];
+    const double l1 = bary[2 * i], l2 = bary[2 * i + 1];
+    double gam[4];
+    if (kd == CS_VT) {
+        gam[0] = 1.0;
+        gam[1] = (1.0 - l1) - l2;
+        gam[2] = l1;
+        gam[3] = l2;
+    } else {
+        gam[0] = 1.0 - l1;
+        gam[1] = l1;
+        gam[2] = 1.0 - l2;
+        gam[3] = l2;
+    }
+    const int ids[4] = {id.x, id.y, id.z, id.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int v = ids[k];
+        const int row = v < n_cloth ? free_index[v] : -1;
+        const bool ok = row >= 0 && clip01(gam[k]) > 0.0;
+        nkey[4 * j + k] = ok ? (((unsigned long long)row << kPlanRowShift) | ((unsigned long long)i << 2) | k)
+                             : sentinel;
+        nsrc[4 * j + k] = 4 * (U0 + j) + k;
+    }
+}
+
+// row segments + entry positions of a merged plan (sentinel entries trail and are ignored)
+__global__ void k_plan_segments(const unsigned long long* __restrict__ pkey, const int* __restrict__ psrc, int m,
+                                int nrows, int* __restrict__ seg_beg, int* __restrict__ seg_end,
+                                int* __restrict__ dst) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const unsigned long long r = pkey[j] >> kPlanRowShift;
+    if (r >= (unsigned long long)nrows) return;
+    dst[psrc[j]] = j;
+    if (j == 0 || (pkey[j - 1] >> kPlanRowShift) != r) seg_beg[r] = j;
+    if (j == m - 1 || (pkey[j + 1] >> kPlanRowShift) != r) seg_end[r] = j + 1;
+}
+
+// rows whose stamps carry weight (delta_i > 0): the reduced Gram's row list
+__global__ void k_flag_positive(const double* __restrict__ v, int m, uint8_t* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) flag[i] = v[i] > 0.0;
+}
+
+struct U64Less {
+    __host__ __device__ __forceinline__ bool operator()(unsigned long long a, unsigned long long b) const {
+        return a < b;
+    }
+};
+
 // compaction helpers for the per-stage collision-terms entry point
 // stable compaction of the stamp entries that land on a free row: indices from
 // DeviceSelect::If with this predicate, then their keys
@@ -208,7 +299,10 @@ __global__ void k_stamp_delta(int nf, const int* __restrict__ seg_beg, const int
     if (i >= nf) return;
     double d = 0.0;
     if (seg_beg != nullptr)
-        for (int k = seg_beg[i]; k < seg_end[i]; ++k) d = d + stamp[src[k]].w;
+        for (int k = seg_beg[i]; k < seg_end[i]; ++k) {
+            const double w = stamp[src[k]].w;
+            if (w > 0.0) d = d + w;  // plan entries outside the engaged set carry w = 0
+        }
     delta[i] = d;
 }
 

@@ -195,8 +195,10 @@ __global__ void k_assemble_rhs(int nf, const int* __restrict__ free_ids, const d
     double dl = 0.0;
     if (seg_beg != nullptr) {
         for (int k = seg_beg[i]; k < seg_end[i]; ++k) {
-            const double4 st = stamp[stamp_src[k]];  // target xyz + weight, one 32-byte sector
+            // entry order (gather through the row sort) or plan order (stamp_src == null: streamed)
+            const double4 st = stamp[stamp_src != nullptr ? stamp_src[k] : k];
             const double w = st.w;
+            if (!(w > 0.0)) continue;  // plan entry of a pair that left the engaged set
             dl = dl + w;
             bi = bi + w * d3{st.x, st.y, st.z};
         }
@@ -874,6 +876,7 @@ __global__ void k_energy_grad(int n, const double* __restrict__ x, const double*
     if (seg_beg != nullptr) {
         for (int k = seg_beg[fi]; k < seg_end[fi]; ++k) {
             const double4 st = stamp[stamp_src[k]];
+            if (!(st.w > 0.0)) continue;  // plan entry outside the engaged set
             g = g + st.w * (xv - d3{st.x, st.y, st.z});
         }
     }

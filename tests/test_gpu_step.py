@@ -461,3 +461,65 @@ def test_sphere_ground128_contact_vs_reference(cuda):
         assert np.abs(sim.state.x - xs[j + 1]).max() <= 1e-9, k
     assert contact > 0
 
+
+
+_PLAN_SCENES = [
+    ("sphere_drape", dict(resolution=14, size=0.2), 14),
+    ("skirt", dict(around=40, down=14, radius=0.205), 10),
+    ("stacked_twist", dict(resolution=10, size=0.3, sheets=2, gap=0.0015), 8),
+]
+
+
+@pytest.mark.parametrize("kind,kw,steps", _PLAN_SCENES)
+def test_stamp_plan_reuse_is_bitwise(cuda, monkeypatch, kind, kw, steps):
+    """Many LG iterations per outer loop (the paper's iteration-cap regime): the driver
+    reuses the row order of the collision stamps across iterations (pairs leaving the
+    engaged set keep w = 0 entries, joining pairs are merged in).  Positions and
+    counters must equal, bit for bit, a run that rebuilds the order every iteration
+    (CS_NO_STAMP_PLAN)."""
+    import paper_2403_19272_b200 as P
+
+    cfg = P.StepConfig(h=1.0 / 200.0, eps_inner=1e-9, eps_outer=1e-9, iteration_cap=16)
+
+    def run(plan):
+        if plan:
+            monkeypatch.delenv("CS_NO_STAMP_PLAN", raising=False)
+        else:
+            monkeypatch.setenv("CS_NO_STAMP_PLAN", "1")
+        sim = P.build_scene(kind, config=cfg, **kw)
+        out, reuses = [], 0
+        for _ in range(steps):
+            r = sim.step()
+            out.append((r.lg_iterations, r.outer_loops, r.active_pairs, r.rf_triggered, r.toi_exit))
+            reuses += sim.last_report_c.stamp_plan_reuses
+        return out, sim.state.x.copy(), reuses
+
+    a, xa, ra = run(True)
+    b, xb, rb = run(False)
+    assert rb == 0
+    assert ra > 0, "the cached stamp plan was never reused"
+    assert a == b
+    assert np.array_equal(xa, xb)
+
+
+def test_stamp_plan_teacher_forced_vs_oracle(cuda):
+    """Iteration-cap regime with contact, teacher forced against the oracle (which
+    rebuilds its stamps from scratch every iteration, stepper.py:238-285)."""
+    import paper_2403_19272_b200 as P
+
+    cfg = P.StepConfig(h=1.0 / 200.0, eps_inner=1e-9, eps_outer=1e-9, iteration_cap=12)
+    sim = P.build_scene("sphere_drape", resolution=14, size=0.2, config=cfg)
+    for _ in range(8):
+        sim.step()
+    ref = OracleSimulation.from_simulation(sim)
+    reuses = 0
+    for s in range(4):
+        sim.state = ref.state
+        sim.obstacle_x = ref.obstacle_x
+        r = sim.step()
+        rr = ref.step()
+        reuses += sim.last_report_c.stamp_plan_reuses
+        assert r.active_pairs == rr["active_pairs"], s
+        assert r.lg_iterations == rr["lg_iterations"], s
+        assert float(np.abs(sim.state.x - ref.state.x).max()) <= 1e-9, s
+    assert reuses > 0

@@ -10,17 +10,23 @@ sys.path.insert(0, ".")
 import paper_2403_19272_b200 as P  # noqa: E402
 from paper_2403_19272_b200 import scenes as S  # noqa: E402
 
+import dataclasses  # noqa: E402
+
+PAPER = "--paper" in sys.argv   # eps 1e-9, 67 LG iterations (bench.py paper_regime)
+TAG = "_paper" if PAPER else ""
 cfg = P.StepConfig(h=1.0 / 200.0)
 sim = S.skirt_scene(cfg, around=584, down=584, eigensolver="device")
 for _ in range(4):
     sim.step()
+if PAPER:
+    sim.config = dataclasses.replace(cfg, eps_inner=1e-9, eps_outer=1e-9, iteration_cap=67)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-    for _ in range(2):
+    for _ in range(1 if PAPER else 2):
         sim.step()
     torch.cuda.synchronize()
-prof.export_chrome_trace("gpurun_out/timeline.json")
-ev = json.load(open("gpurun_out/timeline.json"))["traceEvents"]
+prof.export_chrome_trace(f"gpurun_out/timeline{TAG}.json")
+ev = json.load(open(f"gpurun_out/timeline{TAG}.json"))["traceEvents"]
 dev = [e for e in ev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
 dev.sort(key=lambda e: e["ts"])
 t0, t1 = dev[0]["ts"], max(e["ts"] + e["dur"] for e in dev)
@@ -32,7 +38,7 @@ for e in dev:
     by.setdefault(k, [0, 0.0])
     by[k][0] += 1
     by[k][1] += e["dur"]
-for k, (c, d) in sorted(by.items(), key=lambda x: -x[1][1])[:25]:
+for k, (c, d) in sorted(by.items(), key=lambda x: -x[1][1])[:40]:
     print(f"{d / 1e3:8.3f} ms {c:5d}  {k}")
 gaps = []
 end = dev[0]["ts"] + dev[0]["dur"]
