@@ -303,24 +303,32 @@ struct cs_scene {
     int sm_count = 148;
     bool stamps_valid = false;   // seg_beg/seg_end hold stamps for the current rhs
     int n_stamp_rows = 0;
-    // stamp plan (engaged-pair list `sel`, row-sorted entry permutation, row segments,
-    // active rows) of pair set plan_pr: valid while that set's engaged mask is unchanged
-    // (k_partial_ndb raises I_FLIP on any change; every site engagement drops it)
-    // The plan is a superset: pairs that leave the engaged set keep their entries (w = 0,
-    // skipped); pairs that join (counted into I_NEW by k_partial_ndb) are merged in.
+    // Stamp plan: the row order of the collision stamps of pair set plan_pr, cached across
+    // its LG iterations.  A superset of the engaged set: pairs that leave it keep their
+    // entries (w = 0, skipped by the rhs); pairs that join are appended by k_partial_ndb
+    // (newsel) and merged in by key (row, pair, slot) = np.add.at order within a row.
+    // Entries live in a main list (pkey / ssrc_s / seg_beg / seg_end / stamp_p) and a
+    // small side list of recently joined pairs (skey_sd / ssrc_sd / sseg_* / stamp_sd)
+    // that the rhs interleaves by key; the side list is folded into the main list when it
+    // outgrows 1/8 of it.  pdst[4u + k] = plan position of entry k of plan pair u
+    // (plan_store encoding); k_partial_ndb writes the next iteration's stamps there.
     bool plan_valid = false;
     const PairBuf* plan_pr = nullptr;
     long long plan_U = 0;        // pairs in the plan (sel[0, plan_U))
-    long long plan_M = 0;        // plan entries (row-sorted, incl. trailing sentinels)
+    long long plan_Umain = 0;    // sel[0, plan_Umain) have their entries in the main list
+    long long plan_M = 0;        // main-list entries (row-sorted, incl. trailing sentinels)
+    long long side_M = 0;        // side-list entries
     long long plan_new = 0;      // engaged pairs outside the plan at the last partial CCD
     long long plan_reuses = 0;
+    bool fused_ok = false;       // k_partial_ndb wrote this plan's stamps at the candidate
+    int last_loop_lg = 0;        // LG iterations of the last outer loop (plan worth building?)
     bool rows_from_delta = false;  // rows_act must be rebuilt from delta after the rhs
     bool plan_enabled = std::getenv("CS_NO_STAMP_PLAN") == nullptr;  // read at scene creation
-    DBuf<unsigned long long> pkey, pkey2, nkey, nkey_s;
-    DBuf<int> psrc2, nsrc, nsrc_s, newsel, pdst;
-    DBuf<double4> stamp_p;          // stamps in plan (row-sorted) order, written by reuse iterations
-    bool stamps_plan_order = false;  // the current rhs streams stamp_p instead of gathering stamp
-    DBuf<uint8_t> inplan, rowpos;
+    DBuf<unsigned long long> pkey, pkey2, nkey, nkey_s, skey_sd, skey_sd2;
+    DBuf<int> psrc2, nsrc, nsrc_s, newsel, pdst, pair_u, ssrc_sd, ssrc_sd2, sseg_beg, sseg_end;
+    DBuf<double4> stamp_p, stamp_sd;  // stamps in plan order (main / side list)
+    bool stamps_plan_order = false;   // the current rhs streams stamp_p instead of gathering stamp
+    DBuf<uint8_t> rowpos;
 
     // ------------------------------------------------------------ utilities
     cudaEvent_t ev() {
@@ -379,7 +387,10 @@ struct cs_scene {
         k_assemble_rhs<<<grid(nf), 256, 0, s>>>(nf, free_ids.p, xcl, zc, mh2.p, edges(), rinc_ptr.p, rinc.p,
                                                 has_fp ? hfp_ptr.p : nullptr, hfp_col.p, hfp_val.p, xcl, sb,
                                                 seg_end.p, stamps_plan_order ? nullptr : ssrc_s.p,
-                                                stamps_plan_order ? stamp_p.p : stamp.p, b.p, delta.p);
+                                                stamps_plan_order ? stamp_p.p : stamp.p, b.p, delta.p,
+                                                with_stamps && stamps_plan_order && side_M > 0
+                                                    ? StampSide{sseg_beg.p, sseg_end.p, skey_sd.p, stamp_sd.p, pkey.p}
+                                                    : StampSide{});
         ++launches;
         CS_CHECK_LAUNCH();
         return 0;
@@ -549,7 +560,9 @@ struct cs_scene {
         launches += 2;
         const double* gram = nullptr;
         if (refactor && n_rows_act_known > 0) {
-            const int gg = std::min(cs_div_up(n_rows_act_known, 8), sm_count);
+            // grid from nf only: the row partition (hence the rounding) depends on the device
+            // row count alone, whatever bound the host holds
+            const int gg = std::min(cs_div_up(nf, 64), 2 * sm_count);
             CS_RET(part2.ensure((size_t)gg * r * r));
             k_gram_partial<<<gg, kGramThreads, 0, s>>>(rows_act.p, d_iscal.p + I_ROWS, dl, V.p, r, part2.p);
             k_reduce_partials<<<cs_div_up(r * r, 32), 256, 0, s>>>(part2.p, gg, r * r, gram_red.p);
@@ -558,7 +571,8 @@ struct cs_scene {
         }
         ReducedState rs{Xred.p, beta_red.p, fallback.p};
         k_reduced_solve<<<1, 256, 0, s>>>(rhs_red.p, gram, lam.p, r, 0, refactor ? 1 : 0, rs, q.p);
-        k_prolong<<<cs_div_up((long long)nf * 32, 256), 256, 0, s>>>(V.p, r, q.p, nf, xx);
+        k_prolong<<<cs_div_up(nf, prolong_rows(r)), 128, prolong_rows(r) * (r | 1) * sizeof(double), s>>>(
+            V.p, r, q.p, nf, xx);
         launches += 2;
         CS_CHECK_LAUNCH();
         return 0;
@@ -572,7 +586,8 @@ struct cs_scene {
         k_reduce_partials<<<cs_div_up(3 * rb, 32), 256, 0, s>>>(part.p, g, 3 * rb, rhs_red.p);
         ReducedState rs{Xred.p, beta_red.p, fallback.p};
         k_reduced_solve<<<1, 256, 0, s>>>(rhs_red.p, nullptr, lam.p, rb, 1, 0, rs, q.p);
-        k_prolong<<<cs_div_up((long long)nf * 32, 256), 256, 0, s>>>(U.p, rb, q.p, nf, xx);
+        k_prolong<<<cs_div_up(nf, prolong_rows(rb)), 128, prolong_rows(rb) * (rb | 1) * sizeof(double), s>>>(
+            U.p, rb, q.p, nf, xx);
         launches += 4;
         CS_CHECK_LAUNCH();
         return 0;
@@ -1226,26 +1241,31 @@ struct cs_scene {
     // A = number of engaged pairs (known on host).  Fills seg_beg/seg_end, rows_act.
     int stamps(PairBuf& pr, long long A, const double* xw) {
         if (plan_valid && plan_pr == &pr && A > 0 && stamps_valid) {
+            long long from = fused_ok ? plan_U : 0;  // plan pairs whose stamps must be computed here
             if (plan_new > 0) {
                 // a union drifting far from the engaged set costs more per iteration than a
                 // rebuild; an overflowing append list means the list is incomplete
-                if (plan_new <= (long long)newsel.n && plan_U + plan_new <= A + A / 2 + (1 << 16))
-                    CS_RET(plan_extend(pr, plan_new));
-                else
+                if (plan_new <= (long long)newsel.n && plan_U + plan_new <= A + A / 2 + (1 << 16)) {
+                    long long r0 = 0;
+                    CS_RET(plan_extend(pr, plan_new, r0));
+                    from = std::min(from, r0);
+                } else {
                     plan_valid = false;
+                }
                 plan_new = 0;
             }
+            fused_ok = false;
             if (plan_valid) {
-                // same row order: only the stamp payload (targets at xw, weights) changes
-                CS_RET(stamp_p.ensure(plan_M));
-                k_collision_terms<<<grid(plan_U), 256, 0, s>>>(sel.p, plan_U, pr.kind.p, pr.idx.p, xw, pr.bary.p,
-                                                               pr.normal.p, pr.weight.p, cfg.d_hat, n,
-                                                               free_index.p, 0, nullptr, stamp_p.p, pdst.p);
+                if (from < plan_U) {
+                    k_collision_terms<<<grid(plan_U - from), 256, 0, s>>>(
+                        sel.p + from, plan_U - from, pr.kind.p, pr.idx.p, xw, pr.bary.p, pr.normal.p, pr.weight.p,
+                        cfg.d_hat, n, free_index.p, 0, nullptr, stamp_p.p, pdst.p + 4 * from, stamp_sd.p);
+                    ++launches;
+                    CS_CHECK_LAUNCH();
+                }
                 stamps_plan_order = true;
-                ++launches;
                 ++plan_reuses;
                 rows_from_delta = true;
-                CS_CHECK_LAUNCH();
                 return 0;
             }
         }
@@ -1274,7 +1294,7 @@ struct cs_scene {
         CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, pr.engaged.p, sel.p, d_iscal.p + I_BAD, (int)pr.P, s));
         k_collision_terms<<<grid(A), 256, 0, s>>>(sel.p, A, pr.kind.p, pr.idx.p, xw, pr.bary.p, pr.normal.p,
                                                   pr.weight.p, cfg.d_hat, n, free_index.p, 0, skey.p, stamp.p,
-                                                  nullptr);
+                                                  nullptr, nullptr);
         ++launches;
         // entries on a free row (a third of them are not: obstacle / pinned endpoints,
         // zero weight), compacted in order: indices, then their keys
@@ -1316,68 +1336,123 @@ struct cs_scene {
         stamps_valid = true;
         n_stamp_rows = (int)std::min<long long>(m, nf);  // upper bound; exact count read on device
         rows_from_delta = false;
-        if (plan_enabled && cfg.barrier_mode != CS_BARRIER_DBB && &pr == cur) {
+        // (only when the last outer loop ran more than one LG iteration: with one
+        // iteration per pair set the plan would never be reused)
+        if (plan_enabled && last_loop_lg > 1 && cfg.barrier_mode != CS_BARRIER_DBB && &pr == cur) {
             // cache the plan for the next LG iterations on this pair set
             CS_RET(pkey.ensure(mc));
             CS_RET(pdst.ensure(m));
+            CS_RET(pair_u.ensure(pr.P));
+            CS_RET(stamp_p.ensure(mc));
             CS_TRY(cudaMemsetAsync(pdst.p, 0xff, sizeof(int) * m, s));
+            CS_TRY(cudaMemsetAsync(pair_u.p, 0xff, sizeof(int) * pr.P, s));
             k_plan_keys<<<grid(mc), 256, 0, s>>>(skey_s.p, ssrc_s.p, sel.p, (int)mc, pkey.p, pdst.p);
-            CS_RET(inplan.ensure(pr.P));
-            CS_TRY(cudaMemcpyAsync(inplan.p, pr.engaged.p, pr.P, cudaMemcpyDeviceToDevice, s));
+            k_plan_pair_u<<<grid(A), 256, 0, s>>>(sel.p, (int)A, pair_u.p);
             CS_RET(newsel.ensure(std::max<long long>(pr.P / 8, 1 << 16)));
-            ++launches;
+            launches += 2;
             CS_CHECK_LAUNCH();
             plan_valid = true;
             plan_pr = &pr;
-            plan_U = A;
+            plan_U = plan_Umain = A;
             plan_M = mc;
+            side_M = 0;
             plan_new = 0;
+            fused_ok = false;
         }
         return 0;
     }
 
     // merge the N pairs that joined the engaged set into the cached plan: append them to
-    // the plan's pair list, sort their entries by merge key, merge with the plan's
-    // entries, rebuild the row segments (sentinels trail)
-    int plan_extend(PairBuf& pr, long long N) {
+    // the plan's pair list, sort their entries by merge key and merge them into the side
+    // list (or, once the side list outgrows 1/8 of the main list, fold both into the main
+    // list); rebuild the affected row segments and plan positions.  r0 = first plan pair
+    // whose stamps the positions change (their fused stamps are stale).
+    int plan_extend(PairBuf& pr, long long N, long long& r0) {
         int rb = 1;
         while ((1LL << rb) <= (long long)nf) ++rb;
         const int end_bit = kPlanRowShift + rb;
         const unsigned long long sentinel = (1ull << end_bit) - 1;
-        const long long m4 = 4 * N;
-        CS_RET(sel.grow_keep(plan_U + N, plan_U));
+        const long long m4 = 4 * N, U2 = plan_U + N;
+        CS_RET(sel.grow_keep(U2, plan_U));
+        CS_RET(pdst.grow_keep(4 * U2, 4 * plan_U));
         CS_RET(nkey.ensure(m4));
         CS_RET(nsrc.ensure(m4));
         CS_RET(nkey_s.ensure(m4));
         CS_RET(nsrc_s.ensure(m4));
         // the append order of newsel is arbitrary; the plan order is the merge key's
         k_plan_new<<<grid(N), 256, 0, s>>>(newsel.p, (int)N, (int)plan_U, pr.kind.p, pr.idx.p, pr.bary.p, n,
-                                           free_index.p, sentinel, sel.p, inplan.p, nkey.p, nsrc.p);
+                                           free_index.p, sentinel, sel.p, pair_u.p, nkey.p, nsrc.p);
         size_t bytes = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, bytes, nkey.p, nkey_s.p, nsrc.p, nsrc_s.p, (int)m4, 0, end_bit, s);
         CS_RET(cub_tmp.ensure(bytes));
         CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, nkey.p, nkey_s.p, nsrc.p, nsrc_s.p, (int)m4, 0,
                                                end_bit, s));
-        const long long M2 = plan_M + m4;
-        CS_RET(pkey2.ensure(M2));
-        CS_RET(psrc2.ensure(M2));
-        bytes = 0;
-        cub::DeviceMerge::MergePairs(nullptr, bytes, pkey.p, ssrc_s.p, (int)plan_M, nkey_s.p, nsrc_s.p, (int)m4,
-                                     pkey2.p, psrc2.p, U64Less{}, s);
-        CS_RET(cub_tmp.ensure(bytes));
-        CS_TRY(cub::DeviceMerge::MergePairs(cub_tmp.p, bytes, pkey.p, ssrc_s.p, (int)plan_M, nkey_s.p, nsrc_s.p,
-                                            (int)m4, pkey2.p, psrc2.p, U64Less{}, s));
-        std::swap(pkey, pkey2);
-        std::swap(ssrc_s, psrc2);
-        CS_TRY(cudaMemsetAsync(seg_beg.p, 0, sizeof(int) * nf, s));
-        CS_TRY(cudaMemsetAsync(seg_end.p, 0, sizeof(int) * nf, s));
-        CS_RET(pdst.ensure(4 * (plan_U + N)));
-        CS_TRY(cudaMemsetAsync(pdst.p, 0xff, sizeof(int) * 4 * (plan_U + N), s));
-        k_plan_segments<<<grid(M2), 256, 0, s>>>(pkey.p, ssrc_s.p, (int)M2, nf, seg_beg.p, seg_end.p, pdst.p);
-        launches += 4;
+        launches += 2;
+        // side list + new entries
+        const unsigned long long* k2 = nkey_s.p;
+        const int* v2 = nsrc_s.p;
+        long long n2 = m4;
+        if (side_M > 0) {
+            CS_RET(skey_sd2.ensure(side_M + m4));
+            CS_RET(ssrc_sd2.ensure(side_M + m4));
+            CS_RET(merge_keys(skey_sd.p, ssrc_sd.p, side_M, nkey_s.p, nsrc_s.p, m4, skey_sd2.p, ssrc_sd2.p));
+            std::swap(skey_sd, skey_sd2);
+            std::swap(ssrc_sd, ssrc_sd2);
+            k2 = skey_sd.p;
+            v2 = ssrc_sd.p;
+            n2 = side_M + m4;
+        }
+        if (n2 <= std::max<long long>(plan_M / 8, 1 << 16)) {
+            if (side_M == 0) {  // the sorted new entries become the side list
+                CS_RET(skey_sd.ensure(m4));
+                CS_RET(ssrc_sd.ensure(m4));
+                CS_TRY(cudaMemcpyAsync(skey_sd.p, nkey_s.p, sizeof(unsigned long long) * m4, cudaMemcpyDeviceToDevice,
+                                       s));
+                CS_TRY(cudaMemcpyAsync(ssrc_sd.p, nsrc_s.p, sizeof(int) * m4, cudaMemcpyDeviceToDevice, s));
+            }
+            side_M = n2;
+            CS_RET(sseg_beg.ensure(nf));
+            CS_RET(sseg_end.ensure(nf));
+            CS_RET(stamp_sd.ensure(side_M));
+            CS_TRY(cudaMemsetAsync(sseg_beg.p, 0, sizeof(int) * nf, s));
+            CS_TRY(cudaMemsetAsync(sseg_end.p, 0, sizeof(int) * nf, s));
+            CS_TRY(cudaMemsetAsync(pdst.p + 4 * plan_Umain, 0xff, sizeof(int) * 4 * (U2 - plan_Umain), s));
+            k_plan_segments<<<grid(side_M), 256, 0, s>>>(skey_sd.p, ssrc_sd.p, (int)side_M, nf, sseg_beg.p,
+                                                         sseg_end.p, pdst.p, 1);
+            r0 = plan_Umain;
+        } else {
+            // fold the side list (+ new entries) into the main list
+            const long long M2 = plan_M + n2;
+            CS_RET(pkey2.ensure(M2));
+            CS_RET(psrc2.ensure(M2));
+            CS_RET(merge_keys(pkey.p, ssrc_s.p, plan_M, k2, v2, n2, pkey2.p, psrc2.p));
+            std::swap(pkey, pkey2);
+            std::swap(ssrc_s, psrc2);
+            plan_M = M2;
+            side_M = 0;
+            plan_Umain = U2;
+            CS_RET(stamp_p.ensure(plan_M));
+            CS_TRY(cudaMemsetAsync(seg_beg.p, 0, sizeof(int) * nf, s));
+            CS_TRY(cudaMemsetAsync(seg_end.p, 0, sizeof(int) * nf, s));
+            CS_TRY(cudaMemsetAsync(pdst.p, 0xff, sizeof(int) * 4 * U2, s));
+            k_plan_segments<<<grid(plan_M), 256, 0, s>>>(pkey.p, ssrc_s.p, (int)plan_M, nf, seg_beg.p, seg_end.p,
+                                                         pdst.p, 0);
+            r0 = 0;
+        }
+        ++launches;
         CS_CHECK_LAUNCH();
-        plan_U += N;
-        plan_M = M2;
+        plan_U = U2;
+        return 0;
+    }
+
+    int merge_keys(const unsigned long long* k1, const int* v1, long long n1, const unsigned long long* k2,
+                   const int* v2, long long n2, unsigned long long* ko, int* vo) {
+        size_t bytes = 0;
+        cub::DeviceMerge::MergePairs(nullptr, bytes, k1, v1, (int)n1, k2, v2, (int)n2, ko, vo, U64Less{}, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceMerge::MergePairs(cub_tmp.p, bytes, k1, v1, (int)n1, k2, v2, (int)n2, ko, vo, U64Less{},
+                                            s));
+        ++launches;
         return 0;
     }
 
@@ -1757,7 +1832,10 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     int lg = 0, outer_loops = 0, partial_calls = 0;
     int n_deltas = 0;
     for (int outer = 0; outer < cfg.outer_cap; ++outer) {
+        int lg_loop = 0;
         for (int inner = 0; inner < cfg.inner_cap; ++inner) {
+            ++lg_loop;
+            last_loop_lg = std::max(last_loop_lg, lg_loop);
             CS_RET(inner_solve(A));
             // dx = rms(x_new[free] - x_cand[free]); write back (stepper.py:506-509)
             CS_RET(sqnorm(xf.p, xf0.p, nf, nullptr, S_SQ));
@@ -1806,15 +1884,19 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             stage(T_PARTIAL);
             CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
             CS_TRY(cudaMemsetAsync(d_iscal.p + I_NEW, 0, sizeof(int), s));
-            const bool track = plan_valid && plan_pr == cur;  // collect pairs joining the stamp plan
+            // collect pairs joining the stamp plan; write the plan's next stamps (fused terms)
+            const bool track = plan_valid && plan_pr == cur;
+            PlanView plan{};
+            if (track)
+                plan = PlanView{pair_u.p, d_iscal.p + I_NEW, newsel.p, (int)newsel.n, pdst.p, stamp_p.p,
+                                side_M > 0 ? stamp_sd.p : nullptr, n, free_index.p};
+            fused_ok = track;
             if (cur->P) {
                 k_partial_ndb<<<grid(cur->P, 128), 128, 0, s>>>(cur->kind.p, cur->idx.p, anchor_w.p, xc_w.p, cur->P,
                                                                 pat, cur->bary.p, cur->normal.p, cfg.d_hat, cfg.ndb_k,
                                                                 cfg.ndb_base, cur->life.p, cur->weight.p,
                                                                 cur->engaged.p, 0, nullptr, d_iscal.p + I_ENG,
-                                                                track ? inplan.p : nullptr,
-                                                                track ? d_iscal.p + I_NEW : nullptr, newsel.p,
-                                                                (int)newsel.n, 1);
+                                                                plan, 1);
                 ++launches;
                 CS_CHECK_LAUNCH();
             }
@@ -1830,6 +1912,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             if (dx_last <= cfg.eps_inner) break;
         }
         ++outer_loops;
+        last_loop_lg = lg_loop;
         // fresh pair set + line-search filter at the end of every outer loop (stepper.py:547-570)
         double tout = 1.0;
         CS_RET(ccd_site(anchor_w.p, xc_w.p, *nxt, rep, tout, nullptr, 1));
@@ -2234,7 +2317,7 @@ int cs_partial_ccd(const int8_t* kind, const int* idx4, const double* x_start, c
     CS_TRY(cudaMemsetAsync(life.p, 0, sizeof(int) * P, s));
     k_partial_ndb<<<(int)((P + 127) / 128), 128, 0, s>>>(kind, (const int4*)idx4, x_start, x_end, P, tmp.pat, bary.p,
                                                          normal.p, -1.0, 1.0, 2.0, life.p, weight.p, eng.p, 1, active,
-                                                         nullptr, nullptr, nullptr, nullptr, 0, 0);
+                                                         nullptr, PlanView{}, 0);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(s));
     bary.release();
@@ -2380,7 +2463,7 @@ int cs_assemble_rhs(cs_scene* sc, const double* z, const double* x, const double
                                                     sc->rinc_ptr.p, sc->rinc.p, sc->has_fp ? sc->hfp_ptr.p : nullptr,
                                                     sc->hfp_col.p, sc->hfp_val.p, pins ? pins : x,
                                                     with ? sc->seg_beg.p : nullptr, sc->seg_end.p, sc->ssrc_s.p,
-                                                    sc->stamp.p, b, delta);
+                                                    sc->stamp.p, b, delta, StampSide{});
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(s));
     return 0;
@@ -2419,7 +2502,7 @@ int cs_collision_terms(cs_scene* sc, const int8_t* kind, const int* idx4, const 
     CS_RET(sc->rows_act.ensure(m));
     k_collision_terms<<<sc->grid(A), 256, 0, s>>>(sc->sel.p, A, kind, (const int4*)idx4, x_world, bary, normal, weight,
                                                   sc->cfg.d_hat, sc->n, sc->free_index.p, 0, sc->skey.p,
-                                                  sc->stamp.p, nullptr);
+                                                  sc->stamp.p, nullptr, nullptr);
     CS_RET(sc->keep_flag.ensure(m));
     k_key_kept<<<sc->grid(m), 256, 0, s>>>(sc->skey.p, (int)m, sc->nf, sc->keep_flag.p);
     bytes = 0;
@@ -2518,7 +2601,7 @@ int cs_reduced_update(cs_scene* sc, const int* rows, const double* weights, int 
         return 0;
     }
     CS_TRY(cudaMemcpyAsync(sc->d_iscal.p + I_FLAG, &m, sizeof(int), cudaMemcpyHostToDevice, sc->s));
-    const int gg = std::min(cs_div_up(m, 8), sc->sm_count);
+    const int gg = std::min(cs_div_up(m, 64), 2 * sc->sm_count);
     CS_RET(sc->part2.ensure((size_t)gg * r * r));
     k_gram_partial<<<gg, kGramThreads, 0, sc->s>>>(rows, sc->d_iscal.p + I_FLAG, nullptr, sc->V.p, r, sc->part2.p,
                                                    weights);

@@ -799,6 +799,71 @@ __device__ __forceinline__ void witness_sides(int kd, const Corners& q, double l
     }
 }
 
+// The 4 positional targets of a pair (stepper.py:238-285) from the frozen witness
+// (l1, l2, nrm), the gap along nrm at positions q, and the pair weight wp: target
+// tg[k], weight w[k] = wp * clip(gamma_k); mov[k] = endpoint k is a free cloth vertex.
+__device__ __forceinline__ void pair_stamps(int kd, const Corners& q, int4 id, double l1, double l2, d3 nrm,
+                                            double gap, double wp, double d_hat, int n_cloth,
+                                            const int* __restrict__ free_index, d3 tg[4], double w[4],
+                                            bool mov[4], double g[4]) {
+    double deficit = d_hat - gap;
+    deficit = (deficit != deficit) ? deficit : (deficit > 0.0 ? deficit : 0.0);
+    double gam[4];
+    if (kd == CS_VT) {
+        gam[0] = 1.0;
+        gam[1] = (1.0 - l1) - l2;
+        gam[2] = l1;
+        gam[3] = l2;
+    } else {
+        gam[0] = 1.0 - l1;
+        gam[1] = l1;
+        gam[2] = 1.0 - l2;
+        gam[3] = l2;
+    }
+    const int ids[4] = {id.x, id.y, id.z, id.w};
+    bool m1 = false, m2 = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int v = ids[k];
+        mov[k] = (v < n_cloth) && (free_index[v < n_cloth ? v : n_cloth - 1] >= 0);
+        bool first = (kd == CS_VT) ? (k == 0) : (k < 2);
+        if (first) m1 = m1 || mov[k];
+        else m2 = m2 || mov[k];
+    }
+    const bool both = m1 && m2;
+    const double sh1 = (both ? 0.5 : (m1 ? 1.0 : 0.0)) * deficit;
+    const double sh2 = (both ? 0.5 : (m2 ? 1.0 : 0.0)) * deficit;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        bool first = (kd == CS_VT) ? (k == 0) : (k < 2);
+        double mvs = first ? sh1 : -sh2;
+        tg[k] = q.p[k] + mvs * nrm;
+        g[k] = clip01(gam[k]);
+        w[k] = wp * g[k];
+    }
+}
+
+// a stamp at its cached plan position: dst >= 0 main list, dst <= -2 side list
+// (-2 - position), -1 not a plan entry
+__device__ __forceinline__ void plan_store(int dst, d3 tg, double w, double4* __restrict__ main_out,
+                                           double4* __restrict__ side_out) {
+    if (dst >= 0) main_out[dst] = make_double4(tg.x, tg.y, tg.z, w);
+    else if (dst <= -2) side_out[-2 - dst] = make_double4(tg.x, tg.y, tg.z, w);
+}
+
+// The driver's cached stamp plan as seen by k_partial_ndb (all null: no plan).
+struct PlanView {
+    const int* pair_u;   // pair -> position in the plan's pair list, -1 outside the plan
+    int* n_new;          // count of engaged pairs outside the plan (appended to new_list)
+    int* new_list;
+    int new_cap;
+    const int* dst;      // plan position of entry 4u + k (plan_store encoding)
+    double4* main_out;   // fused stamps (null: counting only)
+    double4* side_out;
+    int n_cloth;
+    const int* free_index;
+};
+
 struct SamplePattern {
     double vt[6][2];
     double ee[6][2];
@@ -806,15 +871,13 @@ struct SamplePattern {
 };
 
 // Partial CCD classifier + NDB update, one pass per inner LG iteration.
-__global__ void __launch_bounds__(128, 6) k_partial_ndb(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+__global__ void __launch_bounds__(128, 5) k_partial_ndb(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                               const double* __restrict__ xa, const double* __restrict__ xc, int64_t P,
                               SamplePattern pat, const double* __restrict__ bary,
                               const double* __restrict__ normal, double d_hat, double k_ndb, double base,
                               int* __restrict__ life, double* __restrict__ weight,
                               uint8_t* __restrict__ engaged, int write_active, uint8_t* __restrict__ active_out,
-                              int* __restrict__ eng_count, const uint8_t* __restrict__ inplan,
-                              int* __restrict__ n_new, int* __restrict__ new_list, int new_cap,
-                              int proj_is_witness) {
+                              int* __restrict__ eng_count, const PlanView plan, int proj_is_witness) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     bool eng = false, fresh = false;
     if (i < P) {
@@ -875,24 +938,42 @@ __global__ void __launch_bounds__(128, 6) k_partial_ndb(const int8_t* __restrict
     act = act || (gap < d_hat);
     int lf = act ? min(life[i] + 1, 64) : 0;
     eng = act || (gap < 2.0 * d_hat);
-    fresh = eng && inplan != nullptr && !inplan[i];
     life[i] = lf;
     engaged[i] = eng;
-    weight[i] = eng ? ndb_weight(lf, k_ndb, base) : 0.0;
+    const double wnew = eng ? ndb_weight(lf, k_ndb, base) : 0.0;
+    weight[i] = wnew;
     if (write_active) active_out[i] = act;
+    if (plan.pair_u != nullptr) {
+        const int u = plan.pair_u[i];
+        fresh = eng && u < 0;
+        if (u >= 0 && plan.main_out != nullptr) {
+            // fused collision terms of the next LG iteration: same candidate positions,
+            // the weight just computed, the driver's cached plan positions
+            d3 tg[4];
+            double w[4], gg[4];
+            bool mov[4];
+            pair_stamps(kd, e, id, w1, w2, ld3(normal, i), gap, wnew, d_hat, plan.n_cloth, plan.free_index, tg, w,
+                        mov, gg);
+            const int4 d = reinterpret_cast<const int4*>(plan.dst)[u];
+            plan_store(d.x, tg[0], w[0], plan.main_out, plan.side_out);
+            plan_store(d.y, tg[1], w[1], plan.main_out, plan.side_out);
+            plan_store(d.z, tg[2], w[2], plan.main_out, plan.side_out);
+            plan_store(d.w, tg[3], w[3], plan.main_out, plan.side_out);
+        }
+    }
     }
     if (eng_count != nullptr) block_count(eng, eng_count);
     // engaged pairs outside the driver's stamp plan, appended (any order: the driver
     // sorts their entries by merge key) for the plan merge
-    if (n_new != nullptr) {
+    if (plan.n_new != nullptr) {
         const unsigned m = __ballot_sync(0xffffffffu, fresh);
         if (m) {
             const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
             int base = 0;
-            if (lane == leader) base = atomicAdd(n_new, __popc(m));
+            if (lane == leader) base = atomicAdd(plan.n_new, __popc(m));
             base = __shfl_sync(0xffffffffu, base, leader);
             const int pos = base + __popc(m & ((1u << lane) - 1u));
-            if (fresh && pos < new_cap) new_list[pos] = (int)i;
+            if (fresh && pos < plan.new_cap) plan.new_list[pos] = (int)i;
         }
     }
 }
@@ -914,16 +995,15 @@ __global__ void k_engage_init(const double* __restrict__ toi, const double* __re
 
 // Per engaged pair: 4 positional targets (stepper.py:238-285).  Entries for
 // immovable or zero-weight endpoints get key 0x7fffffff (sorted to the end).
-// frozen_k >= 0 selects residual forwarding's frozen weights (stepper.py:635-642).
 // key == nullptr: payload only, for every entry of the driver's cached stamp plan, at
-// its plan position plan_dst[o] (-1: not a plan entry; pairs no longer engaged get w = 0).
+// its plan position plan_dst[4a + k] (pairs no longer engaged get w = 0).
 __global__ void __launch_bounds__(256, 4) k_collision_terms(const int* __restrict__ sel, int64_t A, const int8_t* __restrict__ kind,
                                   const int4* __restrict__ idx, const double* __restrict__ xw,
                                   const double* __restrict__ bary, const double* __restrict__ normal,
                                   const double* __restrict__ weight, double d_hat, int n_cloth,
                                   const int* __restrict__ free_index, int cloth_only,
                                   int* __restrict__ key, double4* __restrict__ stamp_out,
-                                  const int* __restrict__ plan_dst) {
+                                  const int* __restrict__ plan_dst, double4* __restrict__ side_out) {
     int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (a >= A) return;
     const int i = sel[a];
@@ -935,54 +1015,26 @@ __global__ void __launch_bounds__(256, 4) k_collision_terms(const int* __restric
     witness_sides(kd, q, l1, l2, s1, s2);
     const d3 nrm = ld3(normal, i);
     const double gap = dot3(s1 - s2, nrm);
-    double deficit = d_hat - gap;
-    deficit = (deficit != deficit) ? deficit : (deficit > 0.0 ? deficit : 0.0);
-    double gam[4];
-    if (kd == CS_VT) {
-        gam[0] = 1.0;
-        gam[1] = (1.0 - l1) - l2;
-        gam[2] = l1;
-        gam[3] = l2;
-    } else {
-        gam[0] = 1.0 - l1;
-        gam[1] = l1;
-        gam[2] = 1.0 - l2;
-        gam[3] = l2;
-    }
-    const int ids[4] = {id.x, id.y, id.z, id.w};
+    d3 tg[4];
+    double w[4], g[4];
     bool mov[4];
-    bool m1 = false, m2 = false;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        int v = ids[k];
-        mov[k] = (v < n_cloth) && (free_index[v < n_cloth ? v : n_cloth - 1] >= 0);
-        bool first = (kd == CS_VT) ? (k == 0) : (k < 2);
-        if (first) m1 = m1 || mov[k];
-        else m2 = m2 || mov[k];
+    pair_stamps(kd, q, id, l1, l2, nrm, gap, weight[i], d_hat, n_cloth, free_index, tg, w, mov, g);
+    const int ids[4] = {id.x, id.y, id.z, id.w};
+    if (key == nullptr) {
+        const int4 d = reinterpret_cast<const int4*>(plan_dst)[a];
+        plan_store(d.x, tg[0], w[0], stamp_out, side_out);
+        plan_store(d.y, tg[1], w[1], stamp_out, side_out);
+        plan_store(d.z, tg[2], w[2], stamp_out, side_out);
+        plan_store(d.w, tg[3], w[3], stamp_out, side_out);
+        return;
     }
-    const bool both = m1 && m2;
-    const double sh1 = (both ? 0.5 : (m1 ? 1.0 : 0.0)) * deficit;
-    const double sh2 = (both ? 0.5 : (m2 ? 1.0 : 0.0)) * deficit;
-    const double wp = weight[i];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        bool first = (kd == CS_VT) ? (k == 0) : (k < 2);
-        double mvs = first ? sh1 : -sh2;
-        d3 tg = q.p[k] + mvs * nrm;
-        double g = clip01(gam[k]);
-        double w = wp * g;
-        bool keep = mov[k] && (w > 0.0);
+        bool keep = mov[k] && (w[k] > 0.0);
         if (cloth_only && ids[k] >= n_cloth) keep = false;
         int64_t o = 4 * a + k;
-        if (key != nullptr) {
-            key[o] = keep ? free_index[ids[k]] : 0x7fffffff;
-            if (keep) stamp_out[o] = make_double4(tg.x, tg.y, tg.z, w);  // others are never read
-        } else {
-            // plan entry (its pair may have left the engaged set: w = 0, skipped by the rhs),
-            // written at its row-sorted plan position so the rhs streams the stamps
-            const int j = plan_dst[o];
-            if (j >= 0) stamp_out[j] = make_double4(tg.x, tg.y, tg.z, w);
-        }
+        key[o] = keep ? free_index[ids[k]] : 0x7fffffff;
+        if (keep) stamp_out[o] = make_double4(tg[k].x, tg[k].y, tg[k].z, w[k]);  // others are never read
     }
 }
 

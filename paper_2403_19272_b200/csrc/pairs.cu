@@ -120,10 +120,10 @@ __global__ void k_plan_keys(const int* __restrict__ skey_s, const int* __restric
     dst[src] = j;
 }
 
-__global__ void k_plan_flag_new(const uint8_t* __restrict__ engaged, const uint8_t* __restrict__ inplan, int64_t P,
-                                uint8_t* __restrict__ flag) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < P) flag[i] = engaged[i] && !inplan[i];
+// pair -> position in the plan's pair list (the rest stays -1 from a memset)
+__global__ void k_plan_pair_u(const int* __restrict__ sel, int A, int* __restrict__ pair_u) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a < A) pair_u[sel[a]] = a;
 }
 
 // pairs newly engaged during the plan's lifetime: appended to the plan's pair list
@@ -132,13 +132,13 @@ __global__ void k_plan_flag_new(const uint8_t* __restrict__ engaged, const uint8
 __global__ void k_plan_new(const int* __restrict__ newsel, int N, int U0, const int8_t* __restrict__ kind,
                            const int4* __restrict__ idx, const double* __restrict__ bary, int n_cloth,
                            const int* __restrict__ free_index, unsigned long long sentinel, int* __restrict__ sel,
-                           uint8_t* __restrict__ inplan, unsigned long long* __restrict__ nkey,
+                           int* __restrict__ pair_u, unsigned long long* __restrict__ nkey,
                            int* __restrict__ nsrc) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= N) return;
     const int i = newsel[j];
     sel[U0 + j] = i;
-    inplan[i] = 1;
+    pair_u[i] = U0 + j;
     const int kd = kind[i];
     const int4 id = idx[i];
     const double l1 = bary[2 * i], l2 = bary[2 * i + 1];
@@ -169,12 +169,12 @@ __global__ void k_plan_new(const int* __restrict__ newsel, int N, int U0, const 
 // row segments + entry positions of a merged plan (sentinel entries trail and are ignored)
 __global__ void k_plan_segments(const unsigned long long* __restrict__ pkey, const int* __restrict__ psrc, int m,
                                 int nrows, int* __restrict__ seg_beg, int* __restrict__ seg_end,
-                                int* __restrict__ dst) {
+                                int* __restrict__ dst, int side) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     const unsigned long long r = pkey[j] >> kPlanRowShift;
     if (r >= (unsigned long long)nrows) return;
-    dst[psrc[j]] = j;
+    dst[psrc[j]] = side ? -2 - j : j;  // plan_store encoding
     if (j == 0 || (pkey[j - 1] >> kPlanRowShift) != r) seg_beg[r] = j;
     if (j == m - 1 || (pkey[j + 1] >> kPlanRowShift) != r) seg_end[r] = j + 1;
 }

@@ -141,6 +141,16 @@ __global__ void k_inertia_target(const double* __restrict__ x, const double* __r
 // then collision stamps delta_i += w, b_i += w t in pair order.
 // inc_ptr/inc_edge/inc_sign: vertex->edge incidence, edges where the vertex is
 // endpoint 0 first (edge order) then endpoint 1 (edge order) = np.add.at order.
+// the stamp plan's side list (recently joined pairs, row-sorted by merge key) and the
+// main list's merge keys; seg_beg == null: no side list
+struct StampSide {
+    const int* __restrict__ seg_beg;
+    const int* __restrict__ seg_end;
+    const unsigned long long* __restrict__ key;
+    const double4* __restrict__ stamp;
+    const unsigned long long* __restrict__ main_key;
+};
+
 struct EdgeSet {
     const int* __restrict__ e0;
     const int* __restrict__ e1;
@@ -166,7 +176,7 @@ __global__ void k_assemble_rhs(int nf, const int* __restrict__ free_ids, const d
                                const int* __restrict__ seg_beg, const int* __restrict__ seg_end,
                                const int* __restrict__ stamp_src, const double4* __restrict__ stamp,
                                double* __restrict__ b,
-                               double* __restrict__ delta) {
+                               double* __restrict__ delta, StampSide side) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nf) return;
     const int v = free_ids[i];
@@ -194,9 +204,35 @@ __global__ void k_assemble_rhs(int nf, const int* __restrict__ free_ids, const d
     }
     double dl = 0.0;
     if (seg_beg != nullptr) {
-        for (int k = seg_beg[i]; k < seg_end[i]; ++k) {
-            // entry order (gather through the row sort) or plan order (stamp_src == null: streamed)
-            const double4 st = stamp[stamp_src != nullptr ? stamp_src[k] : k];
+        int k = seg_beg[i];
+        const int ke = seg_end[i];
+        int q = 0, qe = 0;
+        if (side.seg_beg != nullptr) {
+            q = side.seg_beg[i];
+            qe = side.seg_end[i];
+        }
+        if (q == qe) {
+            // main list only, 4 stamps in flight per step (the sums stay sequential)
+            for (; k + 4 <= ke; k += 4) {
+                double4 st[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) st[u] = stamp[stamp_src != nullptr ? stamp_src[k + u] : k + u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double w = st[u].w;
+                    if (!(w > 0.0)) continue;
+                    dl = dl + w;
+                    bi = bi + w * d3{st[u].x, st[u].y, st[u].z};
+                }
+            }
+        }
+        while (k < ke || q < qe) {
+            // entry order (gather through the row sort) or plan order (stamp_src == null:
+            // streamed); a row with side-list entries interleaves both lists by merge key
+            const bool from_main = q >= qe || (k < ke && side.main_key[k] < side.key[q]);
+            const double4 st = from_main ? stamp[stamp_src != nullptr ? stamp_src[k] : k] : side.stamp[q];
+            k += from_main ? 1 : 0;
+            q += from_main ? 0 : 1;
             const double w = st.w;
             if (!(w > 0.0)) continue;  // plan entry of a pair that left the engaged set
             dl = dl + w;
@@ -415,11 +451,11 @@ __global__ void __launch_bounds__(256) k_project_partial(Sell H, const double* _
 
 // G partials over the ascending list of collided rows (count read on device):
 // block b owns a contiguous chunk of the list.  Rows are staged 64 at a time in
-// shared memory (V_i and delta_i V_i, padded to 32 columns); each of the 64 threads
-// owns a 4x4 register tile of the 32x32 output and accumulates every row of the
-// chunk in order, s = fma(V_ia, delta_i V_ib, s) - four operand loads per 16 FMAs,
-// the same per-entry operation sequence as a thread-per-entry loop.  All 256
-// threads stage (8 independent loads each); the first 64 accumulate.
+// shared memory (V_i and delta_i V_i, padded to 32 columns; the next tile's loads are
+// in flight while the current one is consumed).  The 256 threads form 4 groups; each
+// thread of a group owns a 4x4 register tile of the 32x32 output and accumulates the
+// group's rows (every 4th row of a tile) in order, s = fma(V_ia, delta_i V_ib, s); the
+// block partial is ((g0 + g1) + g2) + g3 - a fixed order, so run-to-run deterministic.
 constexpr int kGramThreads = 256;
 __global__ void __launch_bounds__(kGramThreads) k_gram_partial(const int* __restrict__ rows,
                                                                const int* __restrict__ nrows_ptr,
@@ -430,23 +466,24 @@ __global__ void __launch_bounds__(kGramThreads) k_gram_partial(const int* __rest
     // weight of list entry j: delta[rows[j]] (the step), or wlist[j] (reduced_update's
     // explicit (active_vertices, weights), subspace.py:97-106)
     constexpr int kT = 64;
-    __shared__ __align__(16) double sv[kT][32];
-    __shared__ __align__(16) double sw[kT][32];
+    constexpr int kPer = kT * 32 / kGramThreads;
+    __shared__ __align__(16) double sbuf[2][kT][32];
+    double(&sv)[kT][32] = sbuf[0];
+    double(&sw)[kT][32] = sbuf[1];
     const int cnt = *nrows_ptr;
     const int per = (cnt + gridDim.x - 1) / gridDim.x;
     const int beg = min(cnt, (int)blockIdx.x * per);
     const int end = min(cnt, beg + per);
-    const int t = threadIdx.x;
+    const int t = threadIdx.x, grp = t >> 6;
     const int ta = ((t & 63) >> 3) * 4, tb = (t & 7) * 4;
     double acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    for (int t0 = beg; t0 < end; t0 += kT) {
+    double v[kPer], d[kPer];
+    auto load = [&](int t0) {
         const int nt = min(kT, end - t0);
-        constexpr int kPer = kT * 32 / kGramThreads;
-        double v[kPer], d[kPer];
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
             const int e = t + u * kGramThreads, k = e >> 5, c = e & 31;
@@ -458,6 +495,11 @@ __global__ void __launch_bounds__(kGramThreads) k_gram_partial(const int* __rest
                 d[u] = wlist != nullptr ? wlist[t0 + k] : delta[row];
             }
         }
+    };
+    if (beg < end) load(beg);
+    for (int t0 = beg; t0 < end; t0 += kT) {
+        const int nt = min(kT, end - t0);
+        __syncthreads();
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
             const int e = t + u * kGramThreads, k = e >> 5, c = e & 31;
@@ -465,8 +507,8 @@ __global__ void __launch_bounds__(kGramThreads) k_gram_partial(const int* __rest
             sw[k][c] = d[u] * v[u];
         }
         __syncthreads();
-        if (t < 64)
-        for (int k = 0; k < nt; ++k) {
+        if (t0 + kT < end) load(t0 + kT);
+        for (int k = grp; k < nt; k += 4) {
             const double2 a01 = *reinterpret_cast<const double2*>(&sv[k][ta]);
             const double2 a23 = *reinterpret_cast<const double2*>(&sv[k][ta + 2]);
             const double2 b01 = *reinterpret_cast<const double2*>(&sw[k][tb]);
@@ -477,16 +519,19 @@ __global__ void __launch_bounds__(kGramThreads) k_gram_partial(const int* __rest
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
         }
-        __syncthreads();
     }
-    if (t >= 64) return;
+    // group partials -> shared (sv and sw hold 4 x 32 x 32 doubles), summed in group order
+    __syncthreads();
+    double* red = &sbuf[0][0][0];  // [grp][a * 32 + b]
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int a = ta + i, b = tb + j;
-            if (a < r && b < r) part[(int64_t)blockIdx.x * r * r + a * r + b] = acc[i][j];
-        }
+        for (int j = 0; j < 4; ++j) red[grp * 1024 + (ta + i) * 32 + tb + j] = acc[i][j];
+    __syncthreads();
+    for (int o = t; o < r * r; o += kGramThreads) {
+        const int a = o / r, b2 = o - a * r, q = a * 32 + b2;
+        part[(int64_t)blockIdx.x * r * r + o] = ((red[q] + red[1024 + q]) + red[2048 + q]) + red[3072 + q];
+    }
 }
 
 // ---------------------------------------------------------------- reduced solve (one CTA)
@@ -743,29 +788,34 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restric
 }
 
 // x_i += sum_j B[i, j] q[j]
-__global__ void k_prolong(const double* __restrict__ B, int rb, const double* __restrict__ q, int n,
-                          double* __restrict__ x) {
+// One thread per row: the block's rows of B (one contiguous span) are staged in
+// shared memory by coalesced loads (row stride rb | 1: odd, conflict-free), then each
+// thread forms its row's B_i q in column order.  prolong_rows(rb) rows per block.
+__host__ __device__ constexpr int prolong_rows(int rb) { return rb <= 32 ? 128 : 32; }
+__global__ void __launch_bounds__(128) k_prolong(const double* __restrict__ B, int rb, const double* __restrict__ q,
+                                                 int n, double* __restrict__ x) {
     __shared__ double qs[3 * 128];
+    extern __shared__ double sB[];
     for (int o = threadIdx.x; o < 3 * rb; o += blockDim.x) qs[o] = q[o];
+    const int rpb = prolong_rows(rb), rbp = rb | 1;
+    const int r0 = blockIdx.x * rpb;
+    const int nr = min(rpb, n - r0);
+    const double* src = B + (int64_t)r0 * rb;
+    for (int e = threadIdx.x; e < nr * rb; e += blockDim.x) {
+        const int rr = e / rb;
+        sB[rr * rbp + (e - rr * rb)] = __ldg(src + e);
+    }
     __syncthreads();
-    // one warp per row, lanes over basis columns
-    const int lane = threadIdx.x & 31;
-    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (row >= n) return;
-    const double* br = B + (int64_t)row * rb;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int j = lane; j < rb; j += 32) {
-        const double v = __ldg(br + j);
-        a0 = fma(v, qs[3 * j], a0);
-        a1 = fma(v, qs[3 * j + 1], a1);
-        a2 = fma(v, qs[3 * j + 2], a2);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        a0 += __shfl_down_sync(0xffffffffu, a0, o);
-        a1 += __shfl_down_sync(0xffffffffu, a1, o);
-        a2 += __shfl_down_sync(0xffffffffu, a2, o);
-    }
-    if (lane == 0) {
+    for (int t = threadIdx.x; t < nr; t += blockDim.x) {
+        const double* br = sB + t * rbp;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int j = 0; j < rb; ++j) {
+            const double v = br[j];
+            a0 = fma(v, qs[3 * j], a0);
+            a1 = fma(v, qs[3 * j + 1], a1);
+            a2 = fma(v, qs[3 * j + 2], a2);
+        }
+        const int row = r0 + t;
         x[3 * row] += a0;
         x[3 * row + 1] += a1;
         x[3 * row + 2] += a2;
