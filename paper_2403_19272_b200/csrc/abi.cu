@@ -553,9 +553,11 @@ struct cs_scene {
 
     // reduced correction in the reuse basis (subspace.py:165-186); x (nf,3) in place
     int reduced(const double* bb, double* xx, const double* dl, bool refactor, int n_rows_act_known) {
-        const int g = std::min(cs_div_up(nf, PROJ_TILE), 2 * sm_count);
+        const int g = std::min(cs_div_up(nf, proj_rows(r)), 3 * sm_count);
         CS_RET(part.ensure((size_t)g * 3 * r));
-        k_project_partial<<<g, 256, 0, s>>>(sell(), bb, xx, dl, V.p, r, part.p);
+        CS_TRY(cudaFuncSetAttribute(k_project_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)proj_smem(r)));
+        k_project_partial<<<g, 256, proj_smem(r), s>>>(sell(), bb, xx, dl, V.p, r, part.p);
         k_reduce_partials<<<cs_div_up(3 * r, 32), 256, 0, s>>>(part.p, g, 3 * r, rhs_red.p);
         launches += 2;
         const double* gram = nullptr;
@@ -580,9 +582,11 @@ struct cs_scene {
 
     // warm-start correction in the wide basis (subspace.py:189-192)
     int warm_correction(const double* bb, double* xx) {
-        const int g = std::min(cs_div_up(nf, PROJ_TILE), 2 * sm_count);
+        const int g = std::min(cs_div_up(nf, proj_rows(rb)), 3 * sm_count);
         CS_RET(part.ensure((size_t)g * 3 * rb));
-        k_project_partial<<<g, 256, 0, s>>>(sell(), bb, xx, nullptr, U.p, rb, part.p);
+        CS_TRY(cudaFuncSetAttribute(k_project_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)proj_smem(rb)));
+        k_project_partial<<<g, 256, proj_smem(rb), s>>>(sell(), bb, xx, nullptr, U.p, rb, part.p);
         k_reduce_partials<<<cs_div_up(3 * rb, 32), 256, 0, s>>>(part.p, g, 3 * rb, rhs_red.p);
         ReducedState rs{Xred.p, beta_red.p, fallback.p};
         k_reduced_solve<<<1, 256, 0, s>>>(rhs_red.p, nullptr, lam.p, rb, 1, 0, rs, q.p);

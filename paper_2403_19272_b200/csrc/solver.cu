@@ -367,86 +367,92 @@ __global__ void k_norm_final(const double* __restrict__ part, int nparts, double
 }
 
 // ---------------------------------------------------------------- basis projection
-// part[blk][j][c] = sum_{rows in tile} B[row, j] * res[row][c], where
-// res = b - H x - delta x  (mode 0/1: delta may be null) or res = given vector (mode 2).
-#define PROJ_TILE 128
-// Persistent: block b accumulates tiles b, b+grid, ... then writes one partial.
+// part[blk][3 j + c] = sum over the block's rows of B[row, j] * res[row][c], where
+// res = b - H x - delta x (delta may be null) or res = b (x null).
+// Persistent: block b takes row tiles b, b + grid, ...  Per tile, every thread computes
+// one row's residual (SELL row, scipy order) into shared memory while the tile's B rows
+// are staged there by 16-byte loads (row stride rb | 1); then output (j, c) of group g
+// accumulates the tile rows i = g (mod G) in order.  Block partial = groups summed in
+// order; the partials are summed in order by k_reduce_partials.
+__host__ __device__ constexpr int proj_rows(int rb) { return rb <= 32 ? 256 : 64; }
+__host__ constexpr size_t proj_smem(int rb) {
+    return sizeof(double) * ((size_t)proj_rows(rb) * (rb | 1) + 3 * (size_t)proj_rows(rb) + 2 * 3 * 128);
+}
 __global__ void __launch_bounds__(256) k_project_partial(Sell H, const double* __restrict__ b,
                                                          const double* __restrict__ x,
                                                          const double* __restrict__ delta,
                                                          const double* __restrict__ B, int rb,
                                                          double* __restrict__ part) {
-    __shared__ double res[PROJ_TILE][3];
-    __shared__ double acc_sm[8][3 * 128];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double acc[4][3];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = 0.0;
-    const int ntiles = (H.nrows + PROJ_TILE - 1) / PROJ_TILE;
+    extern __shared__ double psm[];
+    const int TR = proj_rows(rb), rbp = rb | 1, O = 3 * rb;
+    double* sB = psm;                         // [TR][rbp]
+    double* res = psm + (size_t)TR * rbp;     // [TR][3]
+    double* red = res + 3 * TR;               // [2][3 * 128] group partials
+    const int G = O <= 128 ? 2 : 1;           // row groups (rb = 30: 2 x 90 outputs)
+    const int t = threadIdx.x;
+    const int grp = G == 2 ? (t >= 128 ? 1 : 0) : 0;
+    const int o0 = G == 2 ? (t & 127) : t;    // first output of this thread
+    double acc0 = 0.0, acc1 = 0.0;            // outputs o0 and o0 + 256 (rb = 120)
+    const int ntiles = (H.nrows + TR - 1) / TR;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int tile0 = tile * PROJ_TILE;
+        const int tile0 = tile * TR;
+        const int nr = min(TR, H.nrows - tile0);
         __syncthreads();
-        for (int r = threadIdx.x; r < PROJ_TILE; r += blockDim.x) {
-            const int i = tile0 + r;
-            d3 rr{0.0, 0.0, 0.0};
-            if (i < H.nrows) {
-                if (x != nullptr) {
-                    const d3 hx = sell_row(H, i, x);
-                    rr = ld3(b, i) - hx;
-                    if (delta != nullptr) rr = rr - delta[i] * ld3(x, i);
-                } else {
-                    rr = ld3(b, i);
-                }
-            }
-            res[r][0] = rr.x;
-            res[r][1] = rr.y;
-            res[r][2] = rr.z;
-        }
-        __syncthreads();
-        // four rows per step with all basis loads issued first (same row order per lane)
-        for (int r = warp; r < PROJ_TILE; r += 4 * nw) {
-            double bv[4][4];
+        // stage B rows (16-byte loads; tile0 * rb is even)
+        const int tot = nr * rb, tot2 = tot >> 1;
+        const double2* src2 = reinterpret_cast<const double2*>(B + (int64_t)tile0 * rb);
+        for (int e0 = t; e0 < tot2; e0 += 4 * 256) {
+            double2 v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int i = tile0 + r + u * nw;
-                const double* row = B + (int64_t)i * rb;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int j = lane + 32 * q;
-                    bv[u][q] = (i < H.nrows && r + u * nw < PROJ_TILE && j < rb) ? __ldg(row + j) : 0.0;
-                }
+                const int e2 = e0 + u * 256;
+                v[u] = e2 < tot2 ? __ldg(src2 + e2) : make_double2(0.0, 0.0);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int rr = r + u * nw;
-                if (rr >= PROJ_TILE || tile0 + rr >= H.nrows) break;
-                const double r0 = res[rr][0], r1 = res[rr][1], r2 = res[rr][2];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (lane + 32 * q < rb) {
-                        acc[q][0] = fma(bv[u][q], r0, acc[q][0]);
-                        acc[q][1] = fma(bv[u][q], r1, acc[q][1]);
-                        acc[q][2] = fma(bv[u][q], r2, acc[q][2]);
-                    }
+                const int e2 = e0 + u * 256;
+                if (e2 < tot2) {
+                    const int e = 2 * e2, ra = e / rb, rb1 = (e + 1) / rb;
+                    sB[ra * rbp + (e - ra * rb)] = v[u].x;
+                    sB[rb1 * rbp + (e + 1 - rb1 * rb)] = v[u].y;
                 }
             }
         }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int j = lane + 32 * q;
-        if (j < rb) {
-            acc_sm[warp][3 * j] = acc[q][0];
-            acc_sm[warp][3 * j + 1] = acc[q][1];
-            acc_sm[warp][3 * j + 2] = acc[q][2];
+        if ((tot & 1) && t == 0) {
+            const int e = tot - 1, ra = e / rb;
+            sB[ra * rbp + (e - ra * rb)] = __ldg(B + (int64_t)tile0 * rb + e);
+        }
+        // residual rows
+        for (int rr = t; rr < nr; rr += 256) {
+            const int i = tile0 + rr;
+            d3 v;
+            if (x != nullptr) {
+                const d3 hx = sell_row(H, i, x);
+                v = ld3(b, i) - hx;
+                if (delta != nullptr) v = v - delta[i] * ld3(x, i);
+            } else {
+                v = ld3(b, i);
+            }
+            res[3 * rr] = v.x;
+            res[3 * rr + 1] = v.y;
+            res[3 * rr + 2] = v.z;
+        }
+        __syncthreads();
+        if (o0 < O) {
+            const int j = o0 / 3, c = o0 - 3 * j;
+            for (int rr = grp; rr < nr; rr += G) acc0 = fma(sB[rr * rbp + j], res[3 * rr + c], acc0);
+        }
+        if (o0 + 256 < O) {
+            const int o1 = o0 + 256, j = o1 / 3, c = o1 - 3 * j;
+            for (int rr = 0; rr < nr; ++rr) acc1 = fma(sB[rr * rbp + j], res[3 * rr + c], acc1);
         }
     }
     __syncthreads();
-    for (int o = threadIdx.x; o < 3 * rb; o += blockDim.x) {
-        double s = 0.0;
-        for (int w = 0; w < nw; ++w) s += acc_sm[w][o];
-        part[(int64_t)blockIdx.x * 3 * rb + o] = s;
-    }
+    if (o0 < O) red[grp * 384 + o0] = acc0;
+    if (o0 + 256 < O) red[o0 + 256] = acc1;
+    __syncthreads();
+    for (int o = t; o < O; o += 256)
+        part[(int64_t)blockIdx.x * O + o] = G == 2 ? red[o] + red[384 + o] : red[o];
 }
 
 // G partials over the ascending list of collided rows (count read on device):
@@ -660,58 +666,81 @@ __global__ void __launch_bounds__(256) k_reduced_solve(const double* __restrict_
         }
         for (int o = tid; o < r * r; o += blockDim.x) LU[o] = A[o];
         __syncthreads();
-        // LU with partial pivoting (LAPACK getrf semantics)
+        // LU with partial pivoting (LAPACK getrf semantics: the first row of largest |a_ik|,
+        // scanning down from the diagonal with strict >; a NaN diagonal keeps row k)
+        const int lane = tid & 31;
         for (int k = 0; k < r; ++k) {
-            if (tid == 0) {
-                int p = k;
-                double best = fabs(LU[k * r + k]);
-                for (int i2 = k + 1; i2 < r; ++i2)
-                    if (fabs(LU[i2 * r + k]) > best) {
-                        best = fabs(LU[i2 * r + k]);
-                        p = i2;
+            if (tid < 32) {
+                const int i2 = k + lane;
+                double v = (i2 < r) ? fabs(LU[i2 * r + k]) : -1.0;
+                const double vk = __shfl_sync(0xffffffffu, v, 0);
+                if (!(v == v)) v = -1.0;  // NaN below the diagonal never wins the strict > scan
+                int p = i2;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double v2 = __shfl_down_sync(0xffffffffu, v, o);
+                    const int p2 = __shfl_down_sync(0xffffffffu, p, o);
+                    if (v2 > v || (v2 == v && p2 < p)) {
+                        v = v2;
+                        p = p2;
                     }
-                piv[k] = p;
-                if (best == 0.0) singular = 1;
-                if (p != k)
-                    for (int c = 0; c < r; ++c) {
-                        double tmp = LU[k * r + c];
-                        LU[k * r + c] = LU[p * r + c];
-                        LU[p * r + c] = tmp;
-                    }
+                }
+                if (lane == 0) {
+                    if (!(vk == vk)) p = k;
+                    piv[k] = p;
+                    if ((vk == vk ? v : vk) == 0.0) singular = 1;
+                }
+            }
+            __syncthreads();
+            const int p = piv[k];
+            if (p != k && tid < r) {
+                const double tmp = LU[k * r + tid];
+                LU[k * r + tid] = LU[p * r + tid];
+                LU[p * r + tid] = tmp;
             }
             __syncthreads();
             const double pv = LU[k * r + k];
             for (int i2 = k + 1 + tid; i2 < r; i2 += blockDim.x) LU[i2 * r + k] = pv != 0.0 ? LU[i2 * r + k] / pv : 0.0;
             __syncthreads();
-            const int m = r - k - 1;
-            for (int o = tid; o < m * m; o += blockDim.x) {
-                const int i2 = k + 1 + o / m, c = k + 1 + o % m;
-                LU[i2 * r + c] = LU[i2 * r + c] - LU[i2 * r + k] * LU[k * r + c];
+            // rank-1 update: lane = column, warps stride the rows (r <= 32)
+            {
+                const int c = k + 1 + lane;
+                if (c < r)
+                    for (int i2 = k + 1 + (tid >> 5); i2 < r; i2 += (int)(blockDim.x >> 5))
+                        LU[i2 * r + c] = LU[i2 * r + c] - LU[i2 * r + k] * LU[k * r + c];
             }
             __syncthreads();
         }
         const double bt = beta_sm;
-        // X = A^-1 (I / beta): one thread per right-hand side column
+        // X = A^-1 (I / beta): permuted identity / beta, then forward substitution
+        // (unit L) and back substitution (U), right-looking and element-parallel
+        for (int o = tid; o < r * r; o += blockDim.x) X[o] = 0.0;
+        __syncthreads();
         if (tid < r) {
-            double col[32];
-            for (int i2 = 0; i2 < r; ++i2) col[i2] = (i2 == tid ? 1.0 : 0.0) / bt;
+            // column tid of P (I / beta): apply the row interchanges in order
+            int row = tid;
             for (int k = 0; k < r; ++k) {
                 const int p = piv[k];
-                double tmp = col[k];
-                col[k] = col[p];
-                col[p] = tmp;
+                if (row == k) row = p;
+                else if (row == p) row = k;
             }
-            for (int i2 = 0; i2 < r; ++i2) {
-                double s = col[i2];
-                for (int k = 0; k < i2; ++k) s -= LU[i2 * r + k] * col[k];
-                col[i2] = s;
-            }
-            for (int i2 = r - 1; i2 >= 0; --i2) {
-                double s = col[i2];
-                for (int k = i2 + 1; k < r; ++k) s -= LU[i2 * r + k] * col[k];
-                col[i2] = s / LU[i2 * r + i2];
-            }
-            for (int i2 = 0; i2 < r; ++i2) X[i2 * r + tid] = col[i2];
+            X[row * r + tid] = 1.0 / bt;
+        }
+        __syncthreads();
+        const int wstride = (int)(blockDim.x >> 5);
+        for (int k = 0; k < r; ++k) {  // rows i2 > k: x_i2 -= L_i2k x_k (lane = column)
+            if (lane < r)
+                for (int i2 = k + 1 + (tid >> 5); i2 < r; i2 += wstride)
+                    X[i2 * r + lane] = X[i2 * r + lane] - LU[i2 * r + k] * X[k * r + lane];
+            __syncthreads();
+        }
+        // back substitution, right-looking: x_k /= U_kk, then rows i2 < k: x_i2 -= U_i2k x_k
+        for (int k = r - 1; k >= 0; --k) {
+            if (tid < r) X[k * r + tid] = X[k * r + tid] / LU[k * r + k];
+            __syncthreads();
+            if (lane < r)
+                for (int i2 = tid >> 5; i2 < k; i2 += wstride)
+                    X[i2 * r + lane] = X[i2 * r + lane] - LU[i2 * r + k] * X[k * r + lane];
+            __syncthreads();
         }
         __syncthreads();
         // residual |A (beta X) - I|_max  (subspace.py:136-139)
@@ -720,8 +749,9 @@ __global__ void __launch_bounds__(256) k_reduced_solve(const double* __restrict_
         __syncthreads();
         double wl = 0.0;
         bool nonfinite = false;
-        for (int o = tid; o < r * r; o += blockDim.x) {
-            const int a = o / r, c = o % r;
+        for (int a = tid >> 5; a < r; a += (int)(blockDim.x >> 5)) {
+            const int c = lane;
+            if (c >= r) break;
             double s = 0.0;
             for (int k = 0; k < r; ++k) s += A[a * r + k] * (bt * X[k * r + c]);
             const double e = fabs(s - (a == c ? 1.0 : 0.0));
@@ -801,9 +831,29 @@ __global__ void __launch_bounds__(128) k_prolong(const double* __restrict__ B, i
     const int r0 = blockIdx.x * rpb;
     const int nr = min(rpb, n - r0);
     const double* src = B + (int64_t)r0 * rb;
-    for (int e = threadIdx.x; e < nr * rb; e += blockDim.x) {
-        const int rr = e / rb;
-        sB[rr * rbp + (e - rr * rb)] = __ldg(src + e);
+    // 16-byte loads, 8 in flight per thread (r0 * rb is even: the span is 16-byte aligned)
+    const int tot = nr * rb, tot2 = tot >> 1;
+    const double2* src2 = reinterpret_cast<const double2*>(src);
+    for (int e0 = threadIdx.x; e0 < tot2; e0 += 8 * blockDim.x) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e2 = e0 + u * blockDim.x;
+            v[u] = e2 < tot2 ? __ldg(src2 + e2) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e2 = e0 + u * blockDim.x;
+            if (e2 < tot2) {
+                const int e = 2 * e2, ra = e / rb, rb1 = (e + 1) / rb;
+                sB[ra * rbp + (e - ra * rb)] = v[u].x;
+                sB[rb1 * rbp + (e + 1 - rb1 * rb)] = v[u].y;
+            }
+        }
+    }
+    if ((tot & 1) && threadIdx.x == 0) {
+        const int e = tot - 1, ra = e / rb;
+        sB[ra * rbp + (e - ra * rb)] = __ldg(src + e);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < nr; t += blockDim.x) {

@@ -20,5 +20,7 @@ sim.step()
 torch.cuda.synchronize()
 for _ in range(steps):
     r = sim.step()
-    print("lg", r.lg_iterations, "outer", r.outer_loops, "reuses", sim.last_report_c.stamp_plan_reuses, flush=True)
+    c = sim.last_report_c
+    print("lg", r.lg_iterations, "outer", r.outer_loops, "reuses", c.stamp_plan_reuses, "reduced_fallbacks",
+          c.reduced_fallbacks, "host_syncs", c.host_syncs, flush=True)
 torch.cuda.synchronize()
