@@ -250,6 +250,25 @@ int cs_intersections(cs_scene *scene, const double *x_world, long long *count, i
 int cs_scene_set_verify(cs_scene *scene, int on);
 int cs_last_intersections(cs_scene *scene, long long *count, int *pairs, int cap, double *x_final);
 
+/* ---- device eigensolver (setup; subspace.py:49-84 for paper-scale meshes) --- */
+/* Opaque context: H (CSR, HOST arrays copied at creation, n x n) and nblocks row-major
+ * n x p device blocks.  The block operations of a Chebyshev-filtered subspace iteration;
+ * the p x p algebra stays with the caller (eigen.py).  HOST pointers throughout. */
+typedef struct cs_eig cs_eig;
+cs_eig *cs_eig_create(int n, const int *indptr, const int *indices, const double *data, int p, int nblocks,
+                      int *status);
+int cs_eig_destroy(cs_eig *eig);
+int cs_eig_set(cs_eig *eig, int block, const double *host, void *stream);            /* block <- host (n,p) */
+int cs_eig_get(cs_eig *eig, int block, int cols, double *host, void *stream);        /* host (n,cols) <- block */
+int cs_eig_spmm(cs_eig *eig, int src, int dst, void *stream);                        /* dst = H src */
+int cs_eig_filter(cs_eig *eig, int x, int w1, int w2, int degree, double a, double lam_max, double a0,
+                  void *stream);                                                      /* Chebyshev filter of x */
+int cs_eig_gram(cs_eig *eig, int a, int b, double *out, void *stream);               /* out (p,p) = A^T B */
+int cs_eig_mul(cs_eig *eig, int src, const double *S, int dst, void *stream);        /* dst = src S, S (p,p) */
+int cs_eig_swap(cs_eig *eig, int a, int b);                                          /* exchange block slots */
+int cs_eig_residuals(cs_eig *eig, int hx, int x, const double *w, int cols, double *out,
+                     void *stream);                                                  /* |HX_j - w_j X_j|^2 */
+
 const char *cs_version(void);
 
 /* Host helper for frame output: the OBJ vertex block "v %.9f %.9f %.9f\n" of n

@@ -77,6 +77,8 @@ EXPORTED = (
     "cs_frame_async", "cs_frame_wait", "cs_format_obj_vertices", "cs_scene_create_parts", "cs_tri_tri_intersect",
     "cs_coplanarity_coefficients", "cs_query_q", "cs_swept_boxes", "cs_dbb_weight", "cs_jacobi_step",
     "cs_reduced_update", "cs_build_reduced", "cs_reduced_get",
+    "cs_eig_create", "cs_eig_destroy", "cs_eig_set", "cs_eig_get", "cs_eig_spmm", "cs_eig_filter", "cs_eig_gram",
+    "cs_eig_mul", "cs_eig_residuals", "cs_eig_swap",
 )
 
 _lib = None
@@ -135,6 +137,17 @@ def load(path: str = LIB_PATH):
         "cs_build_reduced": (ctypes.c_int, [vp, vp, ctypes.c_double, vp, ctypes.POINTER(ctypes.c_double), c_int_p,
                                             vp]),
         "cs_reduced_get": (ctypes.c_int, [vp, vp, ctypes.POINTER(ctypes.c_double), c_int_p, vp]),
+        "cs_eig_create": (vp, [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, c_int_p]),
+        "cs_eig_destroy": (ctypes.c_int, [vp]),
+        "cs_eig_set": (ctypes.c_int, [vp, ctypes.c_int, vp, vp]),
+        "cs_eig_get": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp]),
+        "cs_eig_spmm": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp]),
+        "cs_eig_filter": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_double, vp]),
+        "cs_eig_gram": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp]),
+        "cs_eig_mul": (ctypes.c_int, [vp, ctypes.c_int, vp, ctypes.c_int, vp]),
+        "cs_eig_residuals": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, vp, vp]),
+        "cs_eig_swap": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -45,6 +45,7 @@ using namespace cs;
     } while (0)
 
 #include "stages.cu"  // scene-free stage kernels + their C entry points
+#include "eigen.cu"   // device eigensolver block kernels (setup)
 
 namespace {
 
@@ -2692,6 +2693,205 @@ int cs_energy_gradient(cs_scene* sc, const double* x, const double* z, const int
                                                   sc->seg_end.p, sc->ssrc_s.p, sc->stamp.p, grad);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(s));
+    return 0;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ device eigensolver (setup)
+// Block kernels of the Chebyshev-filtered subspace iteration (eigen.cu) on an opaque
+// context holding H (CSR) and nb row-major n x pp blocks; eigen.py drives it.
+struct cs_eig {
+    int n = 0, p = 0, pp = 0;
+    DBuf<int> indptr, indices;
+    DBuf<double> data, part, red, S, w;
+    std::vector<DBuf<double>> blk;
+    cudaStream_t s = nullptr;
+    int grid_rows(int rows_per_block) const { return std::max(1, (n + rows_per_block - 1) / rows_per_block); }
+    int spmm(int src, int dst, int prev, int mode, double c, double s1, double s2) {
+        const int g = std::max(1, (int)(((long long)n * 32 + 255) / 256));
+        const double* X = blk[src].p;
+        const double* Xp = prev >= 0 ? blk[prev].p : nullptr;
+        double* Y = blk[dst].p;
+#define CS_EIG_SPMM(NQ)                                                                                           \
+    if (pp == 32 * NQ) {                                                                                          \
+        if (mode == 0) k_blk_spmm<NQ, 0><<<g, 256, 0, s>>>(n, indptr.p, indices.p, data.p, X, Xp, pp, c, s1, s2, Y); \
+        else if (mode == 1) k_blk_spmm<NQ, 1><<<g, 256, 0, s>>>(n, indptr.p, indices.p, data.p, X, Xp, pp, c, s1, s2, Y); \
+        else k_blk_spmm<NQ, 2><<<g, 256, 0, s>>>(n, indptr.p, indices.p, data.p, X, Xp, pp, c, s1, s2, Y);     \
+        return 0;                                                                                                 \
+    }
+        CS_EIG_SPMM(1) CS_EIG_SPMM(2) CS_EIG_SPMM(3) CS_EIG_SPMM(4) CS_EIG_SPMM(5) CS_EIG_SPMM(6) CS_EIG_SPMM(7)
+        CS_EIG_SPMM(8)
+#undef CS_EIG_SPMM
+        return CS_BAD_ARGUMENT;
+    }
+};
+
+extern "C" {
+
+cs_eig* cs_eig_create(int n, const int* indptr, const int* indices, const double* data, int p, int nblocks,
+                      int* status) {
+    auto fail = [&](int st, cs_eig* e) -> cs_eig* {
+        if (status) *status = st;
+        delete e;
+        return nullptr;
+    };
+    if (n <= 0 || p <= 0 || p > 256 || nblocks <= 0 || !indptr || !indices || !data) return fail(CS_BAD_ARGUMENT, nullptr);
+    cs_eig* e = new cs_eig();
+    e->n = n;
+    e->p = p;
+    e->pp = (p + 31) / 32 * 32;
+    t_alloc_stream = nullptr;
+    const long long nnz = indptr[n];
+    int st = 0;
+    if ((st = e->indptr.upload(indptr, (size_t)n + 1)) || (st = e->indices.upload(indices, (size_t)nnz)) ||
+        (st = e->data.upload(data, (size_t)nnz)))
+        return fail(st, e);
+    e->blk.resize(nblocks);
+    for (auto& b : e->blk) {
+        if ((st = b.ensure((size_t)n * e->pp, true))) return fail(st, e);
+        if (cudaMemset(b.p, 0, sizeof(double) * (size_t)n * e->pp) != cudaSuccess) return fail(CS_INTERNAL, e);
+    }
+    if ((st = e->S.ensure((size_t)e->pp * e->pp, true)) || (st = e->w.ensure(e->pp, true))) return fail(st, e);
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(CS_INTERNAL, e);
+    if (status) *status = 0;
+    return e;
+}
+
+int cs_eig_destroy(cs_eig* e) {
+    if (!e) return 0;
+    cudaDeviceSynchronize();
+    for (auto& b : e->blk) b.release();
+    e->indptr.release();
+    e->indices.release();
+    e->data.release();
+    e->part.release();
+    e->red.release();
+    e->S.release();
+    e->w.release();
+    delete e;
+    return 0;
+}
+
+static bool eig_ok(cs_eig* e, int b) { return e && b >= 0 && b < (int)e->blk.size(); }
+
+// block <- host (n x p row-major); padding columns zero
+int cs_eig_set(cs_eig* e, int b, const double* host, void* stream) {
+    if (!eig_ok(e, b) || !host) return CS_BAD_ARGUMENT;
+    e->s = (cudaStream_t)stream;
+    CS_TRY(cudaMemsetAsync(e->blk[b].p, 0, sizeof(double) * (size_t)e->n * e->pp, e->s));
+    CS_TRY(cudaMemcpy2DAsync(e->blk[b].p, sizeof(double) * e->pp, host, sizeof(double) * e->p, sizeof(double) * e->p,
+                             e->n, cudaMemcpyHostToDevice, e->s));
+    CS_TRY(cudaStreamSynchronize(e->s));
+    return 0;
+}
+
+// host (n x cols row-major) <- first cols columns of block b
+int cs_eig_get(cs_eig* e, int b, int cols, double* host, void* stream) {
+    if (!eig_ok(e, b) || !host || cols <= 0 || cols > e->p) return CS_BAD_ARGUMENT;
+    e->s = (cudaStream_t)stream;
+    CS_TRY(cudaMemcpy2DAsync(host, sizeof(double) * cols, e->blk[b].p, sizeof(double) * e->pp, sizeof(double) * cols,
+                             e->n, cudaMemcpyDeviceToHost, e->s));
+    CS_TRY(cudaStreamSynchronize(e->s));
+    return 0;
+}
+
+// dst = H src
+int cs_eig_spmm(cs_eig* e, int src, int dst, void* stream) {
+    if (!eig_ok(e, src) || !eig_ok(e, dst) || src == dst) return CS_BAD_ARGUMENT;
+    e->s = (cudaStream_t)stream;
+    CS_RET(e->spmm(src, dst, -1, 0, 0.0, 1.0, 0.0));
+    CS_CHECK_LAUNCH();
+    return 0;
+}
+
+// Chebyshev filter of degree `degree` damping [a, lam_max] (scaled at a0) applied to
+// block x in place; w1, w2: scratch blocks (eigen.py: Y1 = (H X - c X) sigma / e,
+// Y_{d+1} = (H Y_d - c Y_d) 2 s / e - sigma s Y_{d-1})
+int cs_eig_filter(cs_eig* e, int x, int w1, int w2, int degree, double a, double lam_max, double a0, void* stream) {
+    if (!eig_ok(e, x) || !eig_ok(e, w1) || !eig_ok(e, w2) || x == w1 || x == w2 || w1 == w2 || degree < 1)
+        return CS_BAD_ARGUMENT;
+    e->s = (cudaStream_t)stream;
+    const double ee = (lam_max - a) / 2.0, c = (lam_max + a) / 2.0;
+    double sigma = ee / (a0 - c);
+    const double tau = 2.0 / sigma;
+    int bufs[3] = {x, w1, w2};
+    int prev = 0, cur = 1;
+    CS_RET(e->spmm(bufs[prev], bufs[cur], -1, 1, c, sigma / ee, 0.0));
+    for (int d = 2; d <= degree; ++d) {
+        const double s_new = 1.0 / (tau - sigma);
+        const int nxt = 3 - prev - cur;
+        CS_RET(e->spmm(bufs[cur], bufs[nxt], bufs[prev], 2, c, 2.0 * s_new / ee, sigma * s_new));
+        prev = cur;
+        cur = nxt;
+        sigma = s_new;
+    }
+    if (bufs[cur] != x)
+        CS_TRY(cudaMemcpyAsync(e->blk[x].p, e->blk[bufs[cur]].p, sizeof(double) * (size_t)e->n * e->pp,
+                               cudaMemcpyDeviceToDevice, e->s));
+    CS_CHECK_LAUNCH();
+    return 0;
+}
+
+// exchange two block slots (no data movement)
+int cs_eig_swap(cs_eig* e, int a, int b) {
+    if (!eig_ok(e, a) || !eig_ok(e, b)) return CS_BAD_ARGUMENT;
+    std::swap(e->blk[a], e->blk[b]);
+    return 0;
+}
+
+// out (HOST p x p) = A^T B
+int cs_eig_gram(cs_eig* e, int a, int b, double* out, void* stream) {
+    if (!eig_ok(e, a) || !eig_ok(e, b) || !out) return CS_BAD_ARGUMENT;
+    e->s = (cudaStream_t)stream;
+    t_alloc_stream = e->s;
+    const int pp = e->pp, nt = pp / 32;
+    const int chunks = std::max(1, std::min(64, (e->n + 4095) / 4096));
+    const int rpc = (e->n + chunks - 1) / chunks;
+    CS_RET(e->part.ensure((size_t)chunks * pp * pp));
+    CS_RET(e->red.ensure((size_t)pp * pp));
+    k_blk_gram_partial<<<dim3(chunks, nt * nt), 256, 0, e->s>>>(e->n, pp, e->blk[a].p, e->blk[b].p, rpc, e->part.p);
+    k_reduce_partials<<<cs_div_up(pp * pp, 32), 256, 0, e->s>>>(e->part.p, chunks, pp * pp, e->red.p);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaMemcpy2DAsync(out, sizeof(double) * e->p, e->red.p, sizeof(double) * pp, sizeof(double) * e->p, e->p,
+                             cudaMemcpyDeviceToHost, e->s));
+    CS_TRY(cudaStreamSynchronize(e->s));
+    return 0;
+}
+
+// dst = src S (S HOST p x p row-major)
+int cs_eig_mul(cs_eig* e, int src, const double* S, int dst, void* stream) {
+    if (!eig_ok(e, src) || !eig_ok(e, dst) || src == dst || !S) return CS_BAD_ARGUMENT;
+    e->s = (cudaStream_t)stream;
+    const int pp = e->pp;
+    CS_TRY(cudaMemsetAsync(e->S.p, 0, sizeof(double) * pp * pp, e->s));
+    CS_TRY(cudaMemcpy2DAsync(e->S.p, sizeof(double) * pp, S, sizeof(double) * e->p, sizeof(double) * e->p, e->p,
+                             cudaMemcpyHostToDevice, e->s));
+    const size_t smem = sizeof(double) * pp * 33;
+    CS_TRY(cudaFuncSetAttribute(k_blk_mul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int gx = std::min(e->grid_rows(8), 4 * 148);
+    k_blk_mul<<<dim3(gx, pp / 32), 256, smem, e->s>>>(e->n, pp, e->blk[src].p, e->S.p, e->blk[dst].p);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaStreamSynchronize(e->s));
+    return 0;
+}
+
+// out (HOST, cols) = |HX_j - w_j X_j|^2 per column j < cols (w HOST, p)
+int cs_eig_residuals(cs_eig* e, int hx, int x, const double* w, int cols, double* out, void* stream) {
+    if (!eig_ok(e, hx) || !eig_ok(e, x) || !w || !out || cols <= 0 || cols > e->p) return CS_BAD_ARGUMENT;
+    e->s = (cudaStream_t)stream;
+    t_alloc_stream = e->s;
+    const int pp = e->pp;
+    CS_TRY(cudaMemsetAsync(e->w.p, 0, sizeof(double) * pp, e->s));
+    CS_TRY(cudaMemcpyAsync(e->w.p, w, sizeof(double) * e->p, cudaMemcpyHostToDevice, e->s));
+    const int g = std::min(e->grid_rows(8), 2 * 148);
+    CS_RET(e->part.ensure((size_t)g * pp));
+    CS_RET(e->red.ensure((size_t)pp * pp));
+    k_blk_resid<<<g, 256, 0, e->s>>>(e->n, pp, e->blk[hx].p, e->blk[x].p, e->w.p, e->part.p);
+    k_reduce_partials<<<cs_div_up(pp, 32), 256, 0, e->s>>>(e->part.p, g, pp, e->red.p);
+    CS_CHECK_LAUNCH();
+    CS_TRY(cudaMemcpyAsync(out, e->red.p, sizeof(double) * cols, cudaMemcpyDeviceToHost, e->s));
+    CS_TRY(cudaStreamSynchronize(e->s));
     return 0;
 }
 

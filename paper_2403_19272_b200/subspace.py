@@ -10,7 +10,8 @@ r x r reduced solve, U q prolongation) are device kernels in
 ``csrc/solver.cu``.
 
 For paper-scale garments the host ``eigsh`` is minutes long; ``method="device"``
-selects the GPU Chebyshev-filtered subspace iteration (``eigen.py``).
+selects the GPU Chebyshev-filtered subspace iteration (``eigen.py`` driving the
+``csrc/eigen.cu`` block kernels through the C ABI).
 """
 
 from __future__ import annotations
@@ -58,8 +59,9 @@ def build_subspace(system: GlobalSystem, rest: np.ndarray, r_bar: int, r: int, m
     """Smallest-r_bar eigenpairs of H (reference subspace.py:49-84).
 
     method="host": scipy shift-invert Lanczos, identical to the reference.
-    method="device": GPU LOBPCG-style block solver for large meshes (basis
-    spans the same invariant subspace to solver tolerance; not bit-identical).
+    method="device": GPU Chebyshev-filtered subspace iteration for large meshes
+    (eigen.py over the csrc/eigen.cu block kernels; the basis spans the same
+    invariant subspace to solver tolerance; not bit-identical).
     """
     H = system.H
     n = H.shape[0]
