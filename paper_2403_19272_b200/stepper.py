@@ -438,25 +438,27 @@ class Simulation:
         x = np.array(z, dtype=np.float64)
         if mesh.pinned.size:
             x[mesh.pinned] = pin_next
+        # device buffers are plumbing; the arithmetic is cs_assemble_rhs /
+        # cs_warmstart_correction, the gathers and the exit norm are host glue
         zd = self._dbuf(z)
-        xd = self._dbuf(x)
         b = torch.empty((mesh.free.size, 3), dtype=torch.float64, device="cuda")
         delta = torch.empty(mesh.free.size, dtype=torch.float64, device="cuda")
-        free = torch.as_tensor(mesh.free, device="cuda")
         its = 0
         for _ in range(cfg.warm_start_cap):
+            xd = self._dbuf(x)
             _lib.check(self._lib.cs_assemble_rhs(self._scene, zd.data_ptr(), xd.data_ptr(), None, None, None, None, 0,
                                                  b.data_ptr(), delta.data_ptr(), self._stream()), "cs_assemble_rhs")
-            xf = xd[free].contiguous()
-            x0 = xf.clone()
+            x0 = np.ascontiguousarray(x[mesh.free])
+            xf = self._dbuf(x0)
             _lib.check(self._lib.cs_warmstart_correction(self._scene, b.data_ptr(), xf.data_ptr(), self._stream()),
                        "cs_warmstart_correction")
-            dx = float(torch.linalg.vector_norm(xf - x0)) / max(np.sqrt(xf.numel()), 1.0)
-            xd[free] = xf
+            xn = xf.cpu().numpy()
+            dx = float(np.linalg.norm(xn - x0)) / max(np.sqrt(xn.size), 1.0)
+            x[mesh.free] = xn
             its += 1
             if dx < cfg.eps_initial:
                 break
-        return xd.cpu().numpy(), its
+        return x, its
 
     def energy(self, x: np.ndarray, z: np.ndarray, collision=None):
         """Energy and gradient (stepper.py:309-380, 'quad' form).
@@ -638,7 +640,7 @@ class Simulation:
                                                  delta.data_ptr(), self._stream()), "cs_assemble_rhs")
         dx = torch.zeros((nf, 3), dtype=torch.float64, device="cuda")
         r = torch.empty_like(dx)
-        fnorm = float(torch.linalg.vector_norm(f_r))
+        fnorm = float(np.linalg.norm(grad[mesh.free]))
         for it in range(cfg.rf_iterations):
             _lib.check(self._lib.cs_reduced_correction(self._scene, f_r.data_ptr(), dx.data_ptr(), delta.data_ptr(),
                                                        int(it > 0), self._stream()), "cs_reduced_correction")
@@ -647,7 +649,7 @@ class Simulation:
                                                    self._stream()), "cs_ajacobi_smooth")
             _lib.check(self._lib.cs_residual(self._scene, f_r.data_ptr(), dx.data_ptr(), delta.data_ptr(),
                                              r.data_ptr(), self._stream()), "cs_residual")
-            if float(torch.linalg.vector_norm(r)) <= cfg.rf_tolerance * max(fnorm, 1e-30):
+            if float(np.linalg.norm(r.cpu().numpy())) <= cfg.rf_tolerance * max(fnorm, 1e-30):
                 break
         delta_f = np.zeros_like(np.asarray(x, dtype=np.float64))
         delta_f[mesh.free] = 2.0 * mesh.vertex_mass[mesh.free, None] * dx.cpu().numpy() / (cfg.h * cfg.h)
