@@ -112,7 +112,9 @@ typedef struct {
     int verified_sites;         /* subset / motion-free sites re-checked against a full broad phase (CS_VERIFY_STATIC_SITE) */
     int host_syncs;             /* host<->device synchronisations inside this cs_step */
     int stamp_plan_reuses;      /* LG iterations whose collision stamps reused the cached row order
-                                   (engaged set unchanged since the previous rhs) */
+                                   (stamp plan of the pair set, abi.cu) */
+    int lazy_exit_sites;        /* motion-free exit sites settled from the last site's witness
+                                   distances without materialising their pair set */
 } cs_step_report;
 
 /* ---- scene lifetime ---------------------------------------------------- */

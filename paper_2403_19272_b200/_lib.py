@@ -62,7 +62,7 @@ class StepReportC(ctypes.Structure):
         ("pairs_last_site", ctypes.c_longlong), ("pairs_max_site", ctypes.c_longlong),
         ("reduced_fallbacks", ctypes.c_int), ("gpu_launches", ctypes.c_longlong), ("static_sites", ctypes.c_int),
         ("subset_sites", ctypes.c_int), ("verified_sites", ctypes.c_int), ("host_syncs", ctypes.c_int),
-        ("stamp_plan_reuses", ctypes.c_int)]
+        ("stamp_plan_reuses", ctypes.c_int), ("lazy_exit_sites", ctypes.c_int)]
 
 
 CS_OK, CS_PENETRATION, CS_NONFINITE, CS_DIVERGENCE, CS_BAD_DIAGONAL, CS_BAD_ARGUMENT, CS_INTERNAL = range(7)

@@ -323,6 +323,7 @@ struct cs_scene {
     long long plan_reuses = 0;
     bool fused_ok = false;       // k_partial_ndb wrote this plan's stamps at the candidate
     int last_loop_lg = 0;        // LG iterations of the last outer loop (plan worth building?)
+    bool lazy_exit = std::getenv("CS_NO_LAZY_EXIT") == nullptr;  // read at scene creation
     bool rows_from_delta = false;  // rows_act must be rebuilt from delta after the rhs
     bool plan_enabled = std::getenv("CS_NO_STAMP_PLAN") == nullptr;  // read at scene creation
     DBuf<unsigned long long> pkey, pkey2, nkey, nkey_s, skey_sd, skey_sd2;
@@ -1178,6 +1179,7 @@ struct cs_scene {
             }
             CS_CHECK_LAUNCH();
             CS_RET(sync_scalars());
+            if (trace_sites) std::fprintf(stderr, "[cs site] min march toi %.6g\n", h_scal[S_CLAMP_MIN]);
             if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;
             clamp = h_scal[S_CLAMP];
         } else {
@@ -1947,8 +1949,33 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     const long long active_pairs = cur->P ? A : 0;
     double tfin = 1.0;
     // anchor_w == xc_w here (the last outer site set the anchor to the clamped
-    // candidate): a motion-free site whose pairs are a subset of that site's (*cur)
-    CS_RET(ccd_site(anchor_w.p, anchor_w.p, *nxt, rep, tfin, cur));
+    // candidate): a motion-free site whose pairs are a subset of that site's (*cur).
+    // With zero motion its distance march returns 0 for a pair at distance 0 and NaN
+    // for every other pair (L = 0, ccd.py:246-266), and its full-CCD results are never
+    // read (stepper.py:587-592): the site reduces to "is some pair at distance 0", and
+    // every such pair is in *cur, whose witness distances were computed at this very
+    // anchor (same closest-point routines as the march's d0).  The pair set itself is
+    // only needed by residual forwarding (stepper.py:604-610), whose trigger does not
+    // depend on this site unless it reports penetration; so it is materialised only
+    // then (or when sites are being verified, CS_VERIFY_STATIC_SITE).
+    const bool rf_pre = toi_exit < cfg.eps_toi || (cap_hit && dx_last > cfg.eps_outer);
+    if (!rf_pre && lazy_exit && std::getenv("CS_VERIFY_STATIC_SITE") == nullptr) {
+        stage(T_FULL);
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_FLAG, 0, sizeof(int), s));
+        if (cur->P) {
+            k_any_nonpositive<<<grid(cur->P), 256, 0, s>>>(cur->dist.p, cur->P, d_iscal.p + I_FLAG);
+            ++launches;
+            CS_CHECK_LAUNCH();
+        }
+        CS_RET(sync_scalars());
+        if (h_iscal[I_FLAG]) return CS_PENETRATION;
+        if (rep) {
+            rep->full_ccd_calls += 1;
+            rep->lazy_exit_sites += 1;
+        }
+    } else {
+        CS_RET(ccd_site(anchor_w.p, anchor_w.p, *nxt, rep, tfin, cur));
+    }
     CS_RET(set_clamp_value(tfin));
     CS_RET(lerp_world(anchor_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));  // tmp_w = x_final_w
     toi_exit = std::min(toi_exit, tfin);

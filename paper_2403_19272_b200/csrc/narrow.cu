@@ -978,6 +978,14 @@ __global__ void __launch_bounds__(128, 5) k_partial_ndb(const int8_t* __restrict
     }
 }
 
+// any pair at distance <= 0 (the motion-free exit site's march reports t = 0 exactly
+// for those, ccd.py:246-249)
+__global__ void k_any_nonpositive(const double* __restrict__ d, int64_t P, int* __restrict__ flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool hit = i < P && d[i] <= 0.0;
+    if (__any_sync(0xffffffffu, hit) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 // Engaged set and weights after a full-CCD site (stepper.py:483-487, 564-565).
 __global__ void k_engage_init(const double* __restrict__ toi, const double* __restrict__ dist, const int* __restrict__ life,
                               int64_t P, double d_hat, double k_ndb, double base, uint8_t* __restrict__ engaged,

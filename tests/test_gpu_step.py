@@ -531,3 +531,34 @@ def test_stamp_plan_teacher_forced_vs_oracle(cuda):
         assert r.lg_iterations == rr["lg_iterations"], s
         assert float(np.abs(sim.state.x - ref.state.x).max()) <= 1e-9, s
     assert reuses > 0
+
+
+@pytest.mark.parametrize("kind,kw,steps", [
+    ("sphere_drape", dict(resolution=14, size=0.2), 20),        # contact + residual forwarding steps
+    ("skirt", dict(around=40, down=14, radius=0.205), 10),
+])
+def test_lazy_exit_site_is_bitwise(cuda, monkeypatch, kind, kw, steps):
+    """The motion-free exit site settled from the last site's witness distances (no pair
+    set materialised unless residual forwarding needs it) gives the same trajectory,
+    counters and TOIs, bit for bit, as the materialised site (CS_NO_LAZY_EXIT)."""
+    import paper_2403_19272_b200 as P
+
+    def run(lazy):
+        if lazy:
+            monkeypatch.delenv("CS_NO_LAZY_EXIT", raising=False)
+        else:
+            monkeypatch.setenv("CS_NO_LAZY_EXIT", "1")
+        sim = P.build_scene(kind, config=P.StepConfig(h=1.0 / 200.0), **kw)
+        out, lazy_sites = [], 0
+        for _ in range(steps):
+            r = sim.step()
+            out.append((r.lg_iterations, r.outer_loops, r.full_ccd_calls, r.active_pairs, r.rf_triggered,
+                        r.toi_exit))
+            lazy_sites += sim.last_report_c.lazy_exit_sites
+        return out, sim.state.x.copy(), sim.state.delta_f.copy(), lazy_sites
+
+    a, xa, fa, la = run(True)
+    b, xb, fb, lb = run(False)
+    assert lb == 0 and la > 0
+    assert a == b
+    assert np.array_equal(xa, xb) and np.array_equal(fa, fb)

@@ -39,7 +39,7 @@ for e in dev:
     by.setdefault(k, [0, 0.0])
     by[k][0] += 1
     by[k][1] += e["dur"]
-for k, (c, d) in sorted(by.items(), key=lambda x: -x[1][1])[:40]:
+for k, (c, d) in sorted(by.items(), key=lambda x: -x[1][1])[:70]:
     print(f"{d / 1e3:8.3f} ms {c:5d}  {k}")
 gaps = []
 end = dev[0]["ts"] + dev[0]["dur"]
