@@ -197,6 +197,10 @@ struct PairBuf {
     DBuf<double> toi, filt, bary, dist, normal, weight;
     DBuf<int> life;
     DBuf<uint8_t> engaged;
+    // near / far split for the partial CCD passes on this set (engage, k_near_split)
+    DBuf<int> near_l;        // near pairs (pair order), then the far pairs (reversed)
+    long long n_near = 0;    // read at the sync after engage (I_NEAR)
+    bool split_valid = false;
     int reserve(long long m) {
         // first real sizing (from the 1024-row placeholder) takes 3x headroom: pair
         // counts drift upward while cloth settles and a regrowth stalls the stream
@@ -217,14 +221,18 @@ struct PairBuf {
     void release() {
         kind.release(); idx.release(); keys.release(); toi.release(); filt.release(); bary.release();
         dist.release(); normal.release(); weight.release(); life.release(); engaged.release();
+        near_l.release();
+        split_valid = false;
     }
 };
 
 // scalar slots (doubles) read back in one D2H copy
 enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_NORM1 = 5, S_NORM_F = 6,
        S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_MINBITS = 10, S_COUNT = 16 };
+// partial CCD near / far split margin, in units of d_hat (k_near_split)
+constexpr double kFarDelta = 0.05;
 enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_FLAG = 7, I_WLF = 8,
-       I_NEW = 9, I_COUNT = 10 };
+       I_NEW = 9, I_NEAR = 10, I_COUNT = 12 };
 
 const int kStages = 8;
 enum { T_WARM = 0, T_LOCAL, T_GLOBAL, T_SMOOTH, T_BROAD, T_PARTIAL, T_FULL, T_RF };
@@ -324,6 +332,8 @@ struct cs_scene {
     bool fused_ok = false;       // k_partial_ndb wrote this plan's stamps at the candidate
     int last_loop_lg = 0;        // LG iterations of the last outer loop (plan worth building?)
     bool lazy_exit = std::getenv("CS_NO_LAZY_EXIT") == nullptr;  // read at scene creation
+    bool far_pairs = std::getenv("CS_NO_FAR_PAIRS") == nullptr;  // partial CCD near / far split
+    DBuf<double> vdn;  // per world vertex |candidate - anchor|
     bool rows_from_delta = false;  // rows_act must be rebuilt from delta after the rhs
     bool plan_enabled = std::getenv("CS_NO_STAMP_PLAN") == nullptr;  // read at scene creation
     DBuf<unsigned long long> pkey, pkey2, nkey, nkey_s, skey_sd, skey_sd2;
@@ -350,11 +360,13 @@ struct cs_scene {
         stage_start = e;
     }
     int n_syncs = 0;  // host<->device synchronisations in the current cs_step
-    cudaError_t hsync() {
+    cudaError_t hsync(int line = 0) {
         ++n_syncs;
+        static const bool trace_sync = std::getenv("CS_TRACE_SYNC") != nullptr;
+        if (trace_sync) std::fprintf(stderr, "[cs sync] abi.cu:%d\n", line);
         return cudaStreamSynchronize(s);
     }
-    int sync_scalars() {
+    int sync_scalars(int line = 0) {
         // doubles [0, S_COUNT) and ints [0, I_COUNT) in one copy (the 4-double scratch
         // between them rides along; its host copy is only read right after its own
         // sync), plus the smoother's pending residual norms
@@ -362,7 +374,7 @@ struct cs_scene {
                                cudaMemcpyDeviceToHost, s));
         const int nchk = pending_checks >= 2 ? std::min(pending_checks, kMaxNormChecks) : 0;
         if (nchk) CS_TRY(cudaMemcpyAsync(h_norms, norms.p, sizeof(double) * nchk, cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(line));
         return check_divergence(nchk);
     }
     int grid(long long m, int bs = 256) { return (int)std::max<long long>(1, (m + bs - 1) / bs); }
@@ -470,7 +482,7 @@ struct cs_scene {
         CS_CHECK_LAUNCH();
         std::vector<double> hp(g);
         CS_TRY(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * g, cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         double rho = 0.0;
         for (double v : hp) rho = std::max(rho, v);
         cheb_rho = rho;
@@ -720,7 +732,7 @@ struct cs_scene {
             CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + k], tabs[k]->offset.p + tabs[k]->np, sizeof(int), cudaMemcpyDeviceToHost, s));
             CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 4 + k], tabs[k]->n_over.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         }
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         for (int k = 0; k < 3; ++k) {
             tabs[k]->m = h_iscal[I_COUNT + k];
             tabs[k]->n_over_h = h_iscal[I_COUNT + 4 + k];
@@ -749,7 +761,7 @@ struct cs_scene {
         long long* hits_h = reinterpret_cast<long long*>(h_scal + S_COUNT);
         CS_TRY(cudaMemcpyAsync(&hits_h[0], vtab.iter_off.p + vtab.m, sizeof(long long), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&hits_h[1], etab.iter_off.p + etab.m, sizeof(long long), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         CS_RET(vtab.masks.ensure(std::max<long long>(hits_h[0], 1)));
         CS_RET(etab.masks.ensure(std::max<long long>(hits_h[1], 1)));
         // pair counts: [VT runs][VT oversize][EE runs][EE oversize]
@@ -800,7 +812,7 @@ struct cs_scene {
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], oo_vt + n_ovt, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 2], etab.poffset.p + etab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 3], oo_ee + n_oee, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         const long long c0 = h_iscal[I_COUNT + 0], c1 = h_iscal[I_COUNT + 1], c2 = h_iscal[I_COUNT + 2], c3 = h_iscal[I_COUNT + 3];
         const long long P = c0 + c1 + c2 + c3;
         CS_RET(pr.reserve(std::max<long long>(P, 1)));
@@ -873,7 +885,7 @@ struct cs_scene {
         k_box_contained<<<grid(3LL * nw), 256, 0, s>>>(x, 3 * nw, margin, vlo.p, vhi.p, d_iscal.p + I_FLAG);
         ++launches;
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_FLAG], d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         if (h_iscal[I_FLAG]) return 0;
         // boxes of this site (static), then the surviving subset of prev
         k_vertex_boxes<<<grid(3LL * nw), 256, 0, s>>>(x, x, nw, margin, vlo.p, vhi.p, fvbox.p);
@@ -887,7 +899,7 @@ struct cs_scene {
         k_prim_motion<2><<<ge, 256, 0, s>>>(wedges.p, new_, x, x, febox.p);
         launches += 4;
         CS_RET(keep_tiles(prev, nullptr, nullptr, nullptr, I_FLAG));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         const long long P = h_iscal[I_FLAG];
         CS_RET(pr.reserve(std::max<long long>(P, 1)));
         if (P) CS_RET(compact_tiles(prev, pr));
@@ -963,7 +975,7 @@ struct cs_scene {
         // violator counts decide first (nothing else is queued yet, so a refusal wastes
         // only the box and violator passes)
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], d_iscal.p + I_COUNT, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         const int nv = h_iscal[I_COUNT], nt = h_iscal[I_COUNT + 1], ne = h_iscal[I_COUNT + 2];
         const long long nq = (long long)nv + nt + ne;
         // violator x violator tests: one warp walks a whole violator list, so the
@@ -996,7 +1008,7 @@ struct cs_scene {
         CS_RET(scan(qcount.p, qoff.p, (int)nq + 1));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], qoff.p + nq, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], qoff.p + nv + nt, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         const long long Q = h_iscal[I_COUNT], Qvt = h_iscal[I_COUNT + 1];
         const long long Pa = h_iscal[I_COUNT + 3];
         if (trace_sites) {
@@ -1066,7 +1078,7 @@ struct cs_scene {
             std::vector<unsigned long long> ha(full.P), hb(full.P);
             CS_TRY(cudaMemcpyAsync(ha.data(), a.p, sizeof(unsigned long long) * full.P, cudaMemcpyDeviceToHost, s));
             CS_TRY(cudaMemcpyAsync(hb.data(), b.p, sizeof(unsigned long long) * full.P, cudaMemcpyDeviceToHost, s));
-            CS_TRY(hsync());
+            CS_TRY(hsync(__LINE__));
             if (ha != hb) rc = CS_INTERNAL;
             a.release();
             b.release();
@@ -1097,7 +1109,7 @@ struct cs_scene {
         CS_RET(table_count(ttab, ts, ttab.inv.p));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT], ttab.offset.p + ttab.np, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], ttab.n_over.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         ttab.m = h_iscal[I_COUNT];
         ttab.n_over_h = h_iscal[I_COUNT + 1];
         ttab.set_buckets(ttab.m);
@@ -1114,7 +1126,7 @@ struct cs_scene {
         launches += 2;
         CS_CHECK_LAUNCH();
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_FLAG], d_iscal.p + I_FLAG, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         count = h_iscal[I_FLAG];
         return 0;
     }
@@ -1178,7 +1190,7 @@ struct cs_scene {
                 std::fprintf(stderr, "[cs site] pairs %lld full-ccd worklist %d march worklist %d\n", P, wl[0], wl[1]);
             }
             CS_CHECK_LAUNCH();
-            CS_RET(sync_scalars());
+            CS_RET(sync_scalars(__LINE__));
             if (trace_sites) std::fprintf(stderr, "[cs site] min march toi %.6g\n", h_scal[S_CLAMP_MIN]);
             if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;
             clamp = h_scal[S_CLAMP];
@@ -1214,6 +1226,22 @@ struct cs_scene {
             k_engage_init<<<grid(pr.P), 256, 0, s>>>(pr.toi.p, pr.dist.p, pr.life.p, pr.P, cfg.d_hat, cfg.ndb_k,
                                                      cfg.ndb_base, pr.engaged.p, pr.weight.p, d_iscal.p + I_ENG);
         ++launches;
+        pr.split_valid = false;
+        // (with a cached stamp plan the partial pass is bound by the plan pairs' fused
+        // stamp writes, and the split only adds its own passes: single-iteration outer
+        // loops only)
+        if (cfg.barrier_mode != CS_BARRIER_DBB && far_pairs && !(plan_enabled && last_loop_lg > 1)) {
+            CS_RET(pr.near_l.ensure(pr.P));
+            cub::CountingInputIterator<int> it(0);
+            const NearPair pred{pr.toi.p, pr.dist.p, (2.0 * cfg.d_hat + kFarDelta * cfg.d_hat) * (1.0 + 1e-6) + 1e-12};
+            size_t bytes = 0;
+            cub::DevicePartition::If(nullptr, bytes, it, pr.near_l.p, d_iscal.p + I_NEAR, (int)pr.P, pred, s);
+            CS_RET(cub_tmp.ensure(bytes));
+            CS_TRY(cub::DevicePartition::If(cub_tmp.p, bytes, it, pr.near_l.p, d_iscal.p + I_NEAR, (int)pr.P, pred,
+                                            s));
+            ++launches;
+            pr.split_valid = true;  // counts read at the caller's sync (I_NEAR)
+        }
         CS_CHECK_LAUNCH();
         return 0;
     }
@@ -1229,7 +1257,7 @@ struct cs_scene {
         k_count_nonzero<<<grid(old.P), 256, 0, s>>>(old.life.p, old.P, d_iscal.p + I_LIVE);
         ++launches;
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_LIVE], d_iscal.p + I_LIVE, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         const long long live = h_iscal[I_LIVE];
         if (live == 0) return 0;
         unsigned long long cap = 1024;
@@ -1312,7 +1340,7 @@ struct cs_scene {
                                      RowKept{skey.p, nf}, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 7], d_iscal.p + I_COUNT + 7, sizeof(int), cudaMemcpyDeviceToHost,
                                s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         const long long mc = h_iscal[I_COUNT + 7];
         static const bool trace_stamps = std::getenv("CS_TRACE_SITES") != nullptr;
         if (trace_stamps)
@@ -1770,7 +1798,12 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     if (npin) {
         if (pin_next_h) {
             std::memcpy(h_stage, pin_next_h, sizeof(double) * 3 * npin);
+            static const bool trace_h = std::getenv("CS_TRACE_HOST") != nullptr;
+            const auto tq0 = std::chrono::steady_clock::now();
             CS_TRY(cudaMemcpyAsync(pins_next_d.p, h_stage, sizeof(double) * 3 * npin, cudaMemcpyHostToDevice, s));
+            if (trace_h)
+                std::fprintf(stderr, "[cs host] pins H2D call %.1f us\n",
+                             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tq0).count());
         } else {
             k_gather_rows<<<grid(npin), 256, 0, s>>>(x.p, pin_ids.p, npin, pins_next_d.p);
             ++launches;
@@ -1793,7 +1826,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     // ---- warm start (stepper.py:384-400): x = z (pins already at pin_next)
     double* xcl = xc_w.p;  // cloth rows of the candidate world array
     CS_TRY(cudaMemcpyAsync(xcl, z.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
-    CS_RET(sync_scalars());
+    CS_RET(sync_scalars(__LINE__));
     if (h_iscal[I_BAD]) return CS_NONFINITE;
     int ws_iters = 0;
     for (int it = 0; it < cfg.warm_start_cap; ++it) {
@@ -1805,7 +1838,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         CS_RET(sqnorm(xf.p, xf0.p, nf, nullptr, S_SQ));
         k_scatter_rows<<<grid(nf), 256, 0, s>>>(xf.p, free_ids.p, nf, xcl);
         ++launches;
-        CS_RET(sync_scalars());
+        CS_RET(sync_scalars(__LINE__));
         ++ws_iters;
         const double dx = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
         if (dx < cfg.eps_initial) break;
@@ -1830,8 +1863,9 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     if (cur->P) CS_TRY(cudaMemsetAsync(cur->life.p, 0, sizeof(int) * cur->P, s));
     CS_RET(engage(*cur));
     CS_TRY(cudaMemcpyAsync(prev_outer.p, xcl, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
-    CS_RET(sync_scalars());
+    CS_RET(sync_scalars(__LINE__));
     long long A = h_iscal[I_ENG];
+    if (cur->split_valid) cur->n_near = h_iscal[I_NEAR];
 
     double dx_last = INFINITY;
     bool cap_hit = false;
@@ -1866,7 +1900,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
                     launches += 3;
                     CS_CHECK_LAUNCH();
                 }
-                CS_RET(sync_scalars());
+                CS_RET(sync_scalars(__LINE__));
                 dx_last = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
                 if (cur->P) {
                     if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;
@@ -1878,7 +1912,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
                 }
                 CS_RET(witness(*cur, xc_w.p));
                 CS_RET(engage(*cur));
-                CS_RET(sync_scalars());
+                CS_RET(sync_scalars(__LINE__));
                 A = h_iscal[I_ENG];
                 if (cfg.iteration_cap && lg >= cfg.iteration_cap) {
                     cap_hit = true;
@@ -1899,19 +1933,33 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
                                 side_M > 0 ? stamp_sd.p : nullptr, n, free_index.p};
             fused_ok = track;
             if (cur->P) {
-                k_partial_ndb<<<grid(cur->P, 128), 128, 0, s>>>(cur->kind.p, cur->idx.p, anchor_w.p, xc_w.p, cur->P,
-                                                                pat, cur->bary.p, cur->normal.p, cfg.d_hat, cfg.ndb_k,
-                                                                cfg.ndb_base, cur->life.p, cur->weight.p,
-                                                                cur->engaged.p, 0, nullptr, d_iscal.p + I_ENG,
-                                                                plan, 1);
-                ++launches;
+                const NdbArgs na{cur->kind.p, cur->idx.p, anchor_w.p, xc_w.p, pat, cur->bary.p, cur->normal.p,
+                                 cfg.d_hat, cfg.ndb_k, cfg.ndb_base, cur->life.p, cur->weight.p, cur->engaged.p,
+                                 0, nullptr, 1};
+                if (cur->split_valid) {
+                    // near list: the full classifier; far list (after it, reversed): gated on the
+                    // largest vertex displacement anchor -> candidate (k_partial_far)
+                    const long long nn = cur->n_near, nfar = cur->P - cur->n_near;
+                    CS_RET(vdn.ensure(nw));
+                    k_vertex_disp_norm<<<grid(nw), 256, 0, s>>>(anchor_w.p, xc_w.p, nw, vdn.p);
+                    if (nn > 0)
+                        k_partial_ndb<<<grid(nn, 128), 128, 0, s>>>(na, nn, d_iscal.p + I_ENG, plan, cur->near_l.p);
+                    if (nfar > 0)
+                        k_partial_far<<<std::max(1, std::min(grid(nfar, 128), 5 * sm_count)), 128, 0, s>>>(
+                            na, nfar, d_iscal.p + I_ENG, plan, cur->near_l.p + nn, cur->dist.p, vdn.p);
+                    launches += 3;
+                } else {
+                    k_partial_ndb<<<grid(cur->P, 128), 128, 0, s>>>(na, cur->P, d_iscal.p + I_ENG, plan, nullptr);
+                    ++launches;
+                }
                 CS_CHECK_LAUNCH();
             }
             ++partial_calls;
-            CS_RET(sync_scalars());
+            CS_RET(sync_scalars(__LINE__));
             dx_last = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
             A = h_iscal[I_ENG];
             plan_new = h_iscal[I_NEW];
+
             if (cfg.iteration_cap && lg >= cfg.iteration_cap) {
                 cap_hit = true;
                 break;
@@ -1939,8 +1987,9 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         CS_RET(sqnorm(xcl, prev_outer.p, nf, free_ids.p, S_SQ));
         // prev_outer holds cloth rows; compare over free rows only
         CS_TRY(cudaMemcpyAsync(prev_outer.p, xcl, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
-        CS_RET(sync_scalars());
+        CS_RET(sync_scalars(__LINE__));
         A = h_iscal[I_ENG];
+        if (cur->split_valid) cur->n_near = h_iscal[I_NEAR];
         const double d_out = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
         if (rep && n_deltas < 64) rep->outer_deltas[n_deltas++] = d_out;
         if (cap_hit || d_out <= cfg.eps_outer) break;
@@ -1967,7 +2016,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             ++launches;
             CS_CHECK_LAUNCH();
         }
-        CS_RET(sync_scalars());
+        CS_RET(sync_scalars(__LINE__));
         if (h_iscal[I_FLAG]) return CS_PENETRATION;
         if (rep) {
             rep->full_ccd_calls += 1;
@@ -2025,7 +2074,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         rep->active_pairs = (int)active_pairs;
         rep->n_outer_deltas = n_deltas;
         rep->gpu_launches = launches;
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         rep->host_syncs = n_syncs;
         rep->stamp_plan_reuses = (int)(plan_reuses - plan_reuses0);
         double acc[kStages] = {0};
@@ -2056,7 +2105,7 @@ int cs_scene::residual_forward(const double* xfw, cs_step_report* rep) {
         k_rf_weights<<<grid(ex.P), 256, 0, s>>>(ex.dist.p, ex.P, cfg.d_hat, cfg.ndb_k, ex.engaged.p, ex.weight.p);
         k_count_true<<<grid(ex.P), 256, 0, s>>>(ex.engaged.p, ex.P, d_iscal.p + I_ENG);
         launches += 2;
-        CS_RET(sync_scalars());
+        CS_RET(sync_scalars(__LINE__));
         A = h_iscal[I_ENG];
     }
     CS_RET(stamps(ex, A, xfw));
@@ -2080,14 +2129,14 @@ int cs_scene::residual_forward(const double* xfw, cs_step_report* rep) {
         k_residual<<<grid(nf), 256, 0, s>>>(sell(), fr.p, xf.p, delta.p, t.p);
         ++launches;
         CS_RET(sqnorm(t.p, nullptr, nf, nullptr, S_RES));
-        CS_RET(sync_scalars());
+        CS_RET(sync_scalars(__LINE__));
         if (h_scal[S_RES] <= cfg.rf_tolerance * std::max(h_scal[S_NORM_F], 1e-30)) break;
     }
     CS_TRY(cudaMemsetAsync(dfn.p, 0, sizeof(double) * 3 * n, s));
     k_forward_force<<<grid(nf), 256, 0, s>>>(xf.p, free_ids.p, nf, mass.p, cfg.h, dfn.p);
     ++launches;
     CS_RET(sqnorm(dfn.p, nullptr, n, nullptr, S_DFNORM));
-    CS_RET(sync_scalars());
+    CS_RET(sync_scalars(__LINE__));
     const double nrm = h_scal[S_DFNORM];
     if (nrm > cfg.delta_f_cap) {
         h_scal[S_DFSCALE] = cfg.delta_f_cap / nrm;
@@ -2098,7 +2147,7 @@ int cs_scene::residual_forward(const double* xfw, cs_step_report* rep) {
     CS_CHECK_LAUNCH();
     if (rep) {
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_FALLBACK], fallback.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync());
+        CS_TRY(hsync(__LINE__));
         rep->reduced_fallbacks += h_iscal[I_FALLBACK];
     }
     return 0;
@@ -2144,9 +2193,11 @@ long long cs_format_obj_vertices(const double* v, long long n, char* out, long l
 cs_scene* cs_scene_create(const cs_scene_desc* desc, const cs_step_config* cfg, int* status) {
     if (desc) {
         // map a slab into the library pool once per process and device, so pair-buffer
-        // regrowth under contact is served without mapping fresh memory: ~4 KB per world
-        // primitive (pair sets, grid tables, stamps at the bench's contact density),
-        // at most a quarter of the free memory; CS_POOL_RESERVE_GB overrides (0 = none)
+        // regrowth under contact is served without mapping fresh memory (a mapping of a few
+        // GB stalls the stream for hundreds of ms): ~32 KB per world primitive (pair sets
+        // of up to ~50 M pairs, grid tables, stamps and the stamp plan at the bench's
+        // contact density), at most a third of the free memory; CS_POOL_RESERVE_GB
+        // overrides (0 = none)
         static bool reserved[64] = {};
         int dev = 0;
         cudaGetDevice(&dev);
@@ -2157,7 +2208,7 @@ cs_scene* cs_scene_create(const cs_scene_desc* desc, const cs_step_config* cfg, 
             cudaMemGetInfo(&free_b, &total_b);
             const char* env = std::getenv("CS_POOL_RESERVE_GB");
             const size_t prims = (size_t)std::max(desc->n_world_tris, 0) + (size_t)std::max(desc->n_world_edges, 0);
-            size_t want = env ? (size_t)(std::atof(env) * (1ull << 30)) : std::min<size_t>(4096 * prims, free_b / 4);
+            size_t want = env ? (size_t)(std::atof(env) * (1ull << 30)) : std::min<size_t>(32768 * prims, free_b / 3);
             void* slab = nullptr;
             if (want && cudaMallocFromPoolAsync(&slab, want, pool, nullptr) == cudaSuccess) {
                 cudaFreeAsync(slab, nullptr);
@@ -2347,9 +2398,9 @@ int cs_partial_ccd(const int8_t* kind, const int* idx4, const double* x_start, c
     CS_TRY(cudaMemsetAsync(bary.p, 0, sizeof(double) * 2 * P, s));
     CS_TRY(cudaMemsetAsync(normal.p, 0, sizeof(double) * 3 * P, s));
     CS_TRY(cudaMemsetAsync(life.p, 0, sizeof(int) * P, s));
-    k_partial_ndb<<<(int)((P + 127) / 128), 128, 0, s>>>(kind, (const int4*)idx4, x_start, x_end, P, tmp.pat, bary.p,
-                                                         normal.p, -1.0, 1.0, 2.0, life.p, weight.p, eng.p, 1, active,
-                                                         nullptr, PlanView{}, 0);
+    const NdbArgs na{kind, (const int4*)idx4, x_start, x_end, tmp.pat, bary.p, normal.p, -1.0, 1.0, 2.0,
+                     life.p, weight.p, eng.p, 1, active, 0};
+    k_partial_ndb<<<(int)((P + 127) / 128), 128, 0, s>>>(na, P, nullptr, PlanView{}, nullptr);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(s));
     bary.release();

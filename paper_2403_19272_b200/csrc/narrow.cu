@@ -870,17 +870,38 @@ struct SamplePattern {
     int width;  // max(kv, ke); shorter pattern already padded by repetition
 };
 
-// Partial CCD classifier + NDB update, one pass per inner LG iteration.
-__global__ void __launch_bounds__(128, 5) k_partial_ndb(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
-                              const double* __restrict__ xa, const double* __restrict__ xc, int64_t P,
-                              SamplePattern pat, const double* __restrict__ bary,
-                              const double* __restrict__ normal, double d_hat, double k_ndb, double base,
-                              int* __restrict__ life, double* __restrict__ weight,
-                              uint8_t* __restrict__ engaged, int write_active, uint8_t* __restrict__ active_out,
-                              int* __restrict__ eng_count, const PlanView plan, int proj_is_witness) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    bool eng = false, fresh = false;
-    if (i < P) {
+// Partial CCD classifier + NDB update of pair i (partial.py:149-204, stepper.py:511-523).
+struct NdbArgs {
+    const int8_t* __restrict__ kind;
+    const int4* __restrict__ idx;
+    const double* __restrict__ xa;
+    const double* __restrict__ xc;
+    SamplePattern pat;
+    const double* __restrict__ bary;
+    const double* __restrict__ normal;
+    double d_hat, k_ndb, base;
+    int* __restrict__ life;
+    double* __restrict__ weight;
+    uint8_t* __restrict__ engaged;
+    int write_active;
+    uint8_t* __restrict__ active_out;
+    int proj_is_witness;
+};
+
+__device__ __forceinline__ void ndb_pair(const NdbArgs& A, const PlanView& plan, int64_t i, bool& eng, bool& fresh) {
+    const int8_t* __restrict__ kind = A.kind;
+    const int4* __restrict__ idx = A.idx;
+    const double* __restrict__ xa = A.xa;
+    const double* __restrict__ xc = A.xc;
+    const SamplePattern& pat = A.pat;
+    const double* __restrict__ bary = A.bary;
+    const double* __restrict__ normal = A.normal;
+    const double d_hat = A.d_hat, k_ndb = A.k_ndb, base = A.base;
+    int* __restrict__ life = A.life;
+    double* __restrict__ weight = A.weight;
+    uint8_t* __restrict__ engaged = A.engaged;
+    const int write_active = A.write_active, proj_is_witness = A.proj_is_witness;
+    uint8_t* __restrict__ active_out = A.active_out;
     const int kd = kind[i];
     const int4 id = idx[i];
     Corners s = gather4(xa, id), e = gather4(xc, id);
@@ -961,7 +982,10 @@ __global__ void __launch_bounds__(128, 5) k_partial_ndb(const int8_t* __restrict
             plan_store(d.w, tg[3], w[3], plan.main_out, plan.side_out);
         }
     }
-    }
+}
+
+__device__ __forceinline__ void ndb_counts(const PlanView& plan, int* __restrict__ eng_count, int64_t i, bool eng,
+                                           bool fresh) {
     if (eng_count != nullptr) block_count(eng, eng_count);
     // engaged pairs outside the driver's stamp plan, appended (any order: the driver
     // sorts their entries by merge key) for the plan merge
@@ -969,12 +993,86 @@ __global__ void __launch_bounds__(128, 5) k_partial_ndb(const int8_t* __restrict
         const unsigned m = __ballot_sync(0xffffffffu, fresh);
         if (m) {
             const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-            int base = 0;
-            if (lane == leader) base = atomicAdd(plan.n_new, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            const int pos = base + __popc(m & ((1u << lane) - 1u));
+            int bpos = 0;
+            if (lane == leader) bpos = atomicAdd(plan.n_new, __popc(m));
+            bpos = __shfl_sync(0xffffffffu, bpos, leader);
+            const int pos = bpos + __popc(m & ((1u << lane) - 1u));
             if (fresh && pos < plan.new_cap) plan.new_list[pos] = (int)i;
         }
+    }
+}
+
+// One pass per inner LG iteration over all P pairs (wl == null) or over the n pair
+// indices of a worklist (the near list of the step's near / far split).
+__global__ void __launch_bounds__(128, 5) k_partial_ndb(NdbArgs A, int64_t n, int* __restrict__ eng_count,
+                                                        const PlanView plan, const int* __restrict__ wl) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool valid = k < n;
+    const int64_t i = !valid ? 0 : (wl != nullptr ? (int64_t)wl[k] : k);
+    bool eng = false, fresh = false;
+    if (valid) ndb_pair(A, plan, i, eng, fresh);
+    ndb_counts(plan, eng_count, i, eng, fresh);
+}
+
+// The far list of the split (NearPair): a far pair whose witness distance d exceeds
+// (2 d_hat + D1 + D2)(1 + 1e-6) + 1e-12, with D1, D2 the largest anchor -> candidate
+// displacements of its two sides' vertices (vdisp), is provably inactive and disengaged
+// (NearPair's argument): life 0, engaged 0, weight 0 without the classifier; the others
+// (and any far pair that has joined the stamp plan) run it.  Uniform grid-stride loop
+// (block_count inside).
+__global__ void __launch_bounds__(128, 5) k_partial_far(NdbArgs A, int64_t n, int* __restrict__ eng_count,
+                                                        const PlanView plan, const int* __restrict__ wl,
+                                                        const double* __restrict__ dist,
+                                                        const double* __restrict__ vdisp) {
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = b0 + threadIdx.x;
+        const bool valid = k < n;
+        const int64_t i = valid ? (int64_t)wl[k] : 0;
+        bool eng = false, fresh = false;
+        if (valid) {
+            const int4 id = A.idx[i];
+            const bool vt = A.kind[i] == CS_VT;
+            const double v0 = vdisp[id.x], v1 = vdisp[id.y], v2 = vdisp[id.z], v3 = vdisp[id.w];
+            const double D1 = vt ? v0 : fmax(v0, v1), D2 = vt ? fmax(fmax(v1, v2), v3) : fmax(v2, v3);
+            // a pair in the stamp plan (it joined through an earlier full pass) keeps the full
+            // path: its fused stamps must be rewritten
+            const bool in_plan = plan.pair_u != nullptr && plan.pair_u[i] >= 0;
+            if (!in_plan && dist[i] > (2.0 * A.d_hat + D1 + D2) * (1.0 + 1e-6) + 1e-12) {
+                A.life[i] = 0;
+                A.engaged[i] = 0;
+                A.weight[i] = 0.0;
+            } else {
+                ndb_pair(A, plan, i, eng, fresh);
+            }
+        }
+        ndb_counts(plan, eng_count, i, eng, fresh);
+    }
+}
+
+// Near / far split of a step's pair set at its engagement (anchor = the interval start
+// of every partial CCD on this set).  Far: not hit by the full CCD and witness distance
+// d > (2 d_hat + delta)(1 + 1e-6) + 1e-12.  While both sides' anchor -> candidate
+// displacements D1 + D2 stay below delta, every sampled offset of a far pair keeps
+// |o_start| >= d > D1 + D2 >= |o_end - o_start| (so Q > 0) and its frozen-witness gap
+// at the candidate is >= d - D1 - D2 > 2 d_hat: the classifier finds it inactive and
+// disengaged (life 0, weight 0), as k_partial_far assumes.  Predicate for
+// cub::DevicePartition (near first in pair order, far after it in reverse order).
+struct NearPair {
+    const double* __restrict__ toi;
+    const double* __restrict__ dist;
+    double thresh;  // (2 d_hat + delta)(1 + 1e-6) + 1e-12
+    __host__ __device__ __forceinline__ bool operator()(int i) const {
+        return toi[i] == toi[i] || !(dist[i] > thresh);
+    }
+};
+
+// |x1 - x0| per world vertex (k_partial_far's displacement bounds)
+__global__ void k_vertex_disp_norm(const double* __restrict__ x0, const double* __restrict__ x1, int n,
+                                   double* __restrict__ out) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) {
+        const double d = norm3(ld3(x1, v) - ld3(x0, v));
+        out[v] = d == d ? d : INFINITY;  // NaN: never far
     }
 }
 

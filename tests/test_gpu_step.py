@@ -562,3 +562,35 @@ def test_lazy_exit_site_is_bitwise(cuda, monkeypatch, kind, kw, steps):
     assert lb == 0 and la > 0
     assert a == b
     assert np.array_equal(xa, xb) and np.array_equal(fa, fb)
+
+
+@pytest.mark.parametrize("kind,kw,steps,cap", [
+    ("sphere_drape", dict(resolution=14, size=0.2), 14, 0),
+    ("skirt", dict(around=40, down=14, radius=0.205), 8, 12),
+    ("stacked_twist", dict(resolution=10, size=0.3, sheets=2, gap=0.0015), 8, 12),
+])
+def test_far_pair_shortcut_is_bitwise(cuda, monkeypatch, kind, kw, steps, cap):
+    """Partial CCD's far-pair shortcut (witness distance beyond 2 d_hat plus both sides'
+    candidate displacements: provably inactive and disengaged) leaves trajectories and
+    counters bit for bit unchanged (CS_NO_FAR_PAIRS runs the full classifier everywhere)."""
+    import paper_2403_19272_b200 as P
+
+    extra = dict(eps_inner=1e-9, eps_outer=1e-9, iteration_cap=cap) if cap else {}
+    cfg = P.StepConfig(h=1.0 / 200.0, **extra)
+
+    def run(fast):
+        if fast:
+            monkeypatch.delenv("CS_NO_FAR_PAIRS", raising=False)
+        else:
+            monkeypatch.setenv("CS_NO_FAR_PAIRS", "1")
+        sim = P.build_scene(kind, config=cfg, **kw)
+        out = []
+        for _ in range(steps):
+            r = sim.step()
+            out.append((r.lg_iterations, r.outer_loops, r.active_pairs, r.rf_triggered, r.toi_exit))
+        return out, sim.state.x.copy()
+
+    a, xa = run(True)
+    b, xb = run(False)
+    assert a == b
+    assert np.array_equal(xa, xb)

@@ -63,3 +63,17 @@ for e in cpu:
 print("host CUDA runtime calls:")
 for k, (c, d) in sorted(byc.items(), key=lambda x: -x[1][1])[:12]:
     print(f"{d / 1e3:8.3f} ms {c:5d}  {k}")
+
+# host runtime calls overlapping the two largest device gaps
+gl = []
+end = dev[0]["ts"] + dev[0]["dur"]
+for e in dev[1:]:
+    if e["ts"] > end:
+        gl.append((e["ts"] - end, end, e["ts"]))
+    end = max(end, e["ts"] + e["dur"])
+gl.sort(reverse=True)
+for g, a, b in gl[:2]:
+    print(f"gap {g:.1f} us [{a:.1f}, {b:.1f}]: host events inside")
+    for e in sorted([e for e in ev if e.get("ph") == "X" and e.get("cat") in ("cuda_runtime", "cpu_op", "python_function")
+                     and e["ts"] + e.get("dur", 0) >= a and e["ts"] <= b], key=lambda e: e["ts"])[:40]:
+        print(f"    {e['ts'] - a:9.1f} +{e.get('dur', 0):8.1f}  {e.get('cat')}: {e['name'][:80]}")
