@@ -79,7 +79,7 @@ def main():
                     break
         except Exception:
             pass
-    launches = load(csv_path)
+    launches = [d for d in load(csv_path) if not d["name"].startswith("k_blk_")]  # setup eigensolver
     agg: "OrderedDict[str, dict]" = OrderedDict()
     for d in launches:
         a = agg.setdefault(d["name"], {"n": 0, "ns": 0.0, "dram": 0.0, "flop": 0.0, "w_pipe": 0.0, "w_issue": 0.0,

@@ -32,6 +32,8 @@ def launches(path):
             continue
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("void ", "").replace("cs::", "")
+        if name.startswith("k_blk_"):  # setup eigensolver kernels
+            continue
         agg[name][0] += 1
         agg[name][1] += v
         tot += v
