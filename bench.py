@@ -674,10 +674,16 @@ def run_ours(args, ws, rank, local):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = bytes_per_launch / t_launch / 1e9 if t_launch > 0 else None
     traffic = None
+    frac_cold = None
     prof = os.path.join(ROOT, "profiles", "jacobi_traffic.json")
     if os.path.exists(prof):
         with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            jt = json.load(fh)
+        traffic = jt.get("dram_bytes_per_launch")
+        if jt.get("cold_launch_us"):
+            # the same pass cold (ncu flushes L2 before the launch): the lower bound of the
+            # two; the timed figure replays the captured smoother graph back to back
+            frac_cold = bytes_per_launch / (jt["cold_launch_us"] * 1e-6) / 1e9 / peak
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         from oracle.stepper import OracleSimulation
@@ -708,6 +714,10 @@ def run_ours(args, ws, rank, local):
         "pairs_per_site_max": pairs,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "frac_cold_l2": frac_cold,
+                     "note": "achieved = CUDA-event mean over the timed steps' 2 x 16 passes per smoothing call "
+                             "(graph replay, L2 warm from the previous pass); frac_cold_l2 = the ncu cold-L2 launch "
+                             "(profiles/r2_full.md)",
                      "kernel": "k_jacobi_a/k_jacobi_b (A-Jacobi SELL-32 SpMV pass)",
                      "bytes_per_launch": bytes_per_launch, "launch_us": t_launch * 1e6},
         "gpu_launches": launches,
