@@ -92,13 +92,15 @@ struct DBuf {
         if (m <= n && p) return 0;
         if (p) cudaFreeAsync(p, t_alloc_stream);
         p = nullptr;
-        // regrowth reserves 2x: per-step sizes (pairs, grid entries) drift and
-        // every cudaFree/cudaMalloc of a large buffer stalls the stream
+        // regrowth reserves 1.5x and a large first sizing 2x: per-step sizes (pairs, grid
+        // entries, stamps) drift upward while the cloth settles; regrowth from the
+        // library pool's slab costs microseconds, the headroom only saves the copies of
+        // many small regrowths (and memory for many scenes per GPU matters more)
         size_t want = std::max<size_t>(m, 1);
-        if (n) want = std::max(2 * want, n + n / 2);
-        // large first sizing: 3x (per-step sizes grow while the cloth settles; a regrowth
-        // mid-run costs a device-synchronising cudaFree + cudaMalloc)
-        else if (!exact && want > (1u << 16)) want *= 3;
+        if (!exact) {
+            if (n) want = std::max(want + want / 2, n + n / 2);
+            else if (want > (1u << 16)) want *= 2;
+        }
         static const bool trace = std::getenv("CS_TRACE_ALLOC") != nullptr;
         if (trace) std::fprintf(stderr, "[cs alloc] %zu -> %zu bytes\n", n * sizeof(T), want * sizeof(T));
         cudaError_t e = pool_alloc(reinterpret_cast<void**>(&p), want * sizeof(T), t_alloc_stream);
@@ -202,20 +204,22 @@ struct PairBuf {
     long long n_near = 0;    // read at the sync after engage (I_NEAR)
     bool split_valid = false;
     int reserve(long long m) {
-        // first real sizing (from the 1024-row placeholder) takes 3x headroom: pair
-        // counts drift upward while cloth settles and a regrowth stalls the stream
-        if (kind.n <= 1024 && m > 1024) m *= 3;
-        CS_RET(kind.ensure(m));
-        CS_RET(idx.ensure(m));
-        CS_RET(keys.ensure(m));
-        CS_RET(toi.ensure(m));
-        CS_RET(filt.ensure(m));
-        CS_RET(bary.ensure(2 * m));
-        CS_RET(dist.ensure(m));
-        CS_RET(normal.ensure(3 * m));
-        CS_RET(weight.ensure(m));
-        CS_RET(life.ensure(m));
-        CS_RET(engaged.ensure(m));
+        // first real sizing (from the 1024-row placeholder) takes 2x headroom, later
+        // regrowth 1.5x: pair counts drift upward while the cloth settles
+        if (m <= (long long)kind.n && kind.p) return 0;
+        const bool first = kind.n <= 1024 && m > 1024;
+        m = first ? 2 * m : m + m / 2;
+        CS_RET(kind.ensure(m, true));
+        CS_RET(idx.ensure(m, true));
+        CS_RET(keys.ensure(m, true));
+        CS_RET(toi.ensure(m, true));
+        CS_RET(filt.ensure(m, true));
+        CS_RET(bary.ensure(2 * m, true));
+        CS_RET(dist.ensure(m, true));
+        CS_RET(normal.ensure(3 * m, true));
+        CS_RET(weight.ensure(m, true));
+        CS_RET(life.ensure(m, true));
+        CS_RET(engaged.ensure(m, true));
         return 0;
     }
     void release() {
@@ -565,12 +569,20 @@ struct cs_scene {
         return 0;
     }
 
+    // one value for every scene and thread (scenes stepped concurrently from host threads
+    // must not race a smaller limit against a larger launch): the largest tile any basis
+    // width up to 128 columns takes
+    static cudaError_t proj_smem_attr() {
+        size_t mx = 0;
+        for (int w = 1; w <= 128; ++w) mx = std::max(mx, proj_smem(w));
+        return cudaFuncSetAttribute(k_project_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    }
+
     // reduced correction in the reuse basis (subspace.py:165-186); x (nf,3) in place
     int reduced(const double* bb, double* xx, const double* dl, bool refactor, int n_rows_act_known) {
         const int g = std::min(cs_div_up(nf, proj_rows(r)), 3 * sm_count);
         CS_RET(part.ensure((size_t)g * 3 * r));
-        CS_TRY(cudaFuncSetAttribute(k_project_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)proj_smem(r)));
+        CS_TRY(proj_smem_attr());
         k_project_partial<<<g, 256, proj_smem(r), s>>>(sell(), bb, xx, dl, V.p, r, part.p);
         k_reduce_partials<<<cs_div_up(3 * r, 32), 256, 0, s>>>(part.p, g, 3 * r, rhs_red.p);
         launches += 2;
@@ -598,8 +610,7 @@ struct cs_scene {
     int warm_correction(const double* bb, double* xx) {
         const int g = std::min(cs_div_up(nf, proj_rows(rb)), 3 * sm_count);
         CS_RET(part.ensure((size_t)g * 3 * rb));
-        CS_TRY(cudaFuncSetAttribute(k_project_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)proj_smem(rb)));
+        CS_TRY(proj_smem_attr());
         k_project_partial<<<g, 256, proj_smem(rb), s>>>(sell(), bb, xx, nullptr, U.p, rb, part.p);
         k_reduce_partials<<<cs_div_up(3 * rb, 32), 256, 0, s>>>(part.p, g, 3 * rb, rhs_red.p);
         ReducedState rs{Xred.p, beta_red.p, fallback.p};
