@@ -232,7 +232,7 @@ struct PairBuf {
 
 // scalar slots (doubles) read back in one D2H copy
 enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_NORM1 = 5, S_NORM_F = 6,
-       S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_MINBITS = 10, S_COUNT = 16 };
+       S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_MINBITS = 10, S_TOIEXIT = 11, S_COUNT = 16 };
 // partial CCD near / far split margin, in units of d_hat (k_near_split)
 constexpr double kFarDelta = 0.05;
 enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_FLAG = 7, I_WLF = 8,
@@ -334,6 +334,7 @@ struct cs_scene {
     long long plan_new = 0;      // engaged pairs outside the plan at the last partial CCD
     long long plan_reuses = 0;
     bool fused_ok = false;       // k_partial_ndb wrote this plan's stamps at the candidate
+    long long live_pairs = -1;   // upper bound of *cur's nonzero life spans after its last partial pass (-1: unknown)
     int last_loop_lg = 0;        // LG iterations of the last outer loop (plan worth building?)
     bool lazy_exit = std::getenv("CS_NO_LAZY_EXIT") == nullptr;  // read at scene creation
     bool far_pairs = std::getenv("CS_NO_FAR_PAIRS") == nullptr;  // partial CCD near / far split
@@ -1145,8 +1146,11 @@ struct cs_scene {
     // base: 0 full broad phase; 1 subset of the current base site if there is one
     // (else / on refusal the full broad phase); 2 this site becomes the base (first
     // moving site of a step)
+    // defer: the clamp stays on the device (d_scal: S_CLAMP_MIN / S_CLAMP / S_CLAMP_BAD, as
+    // k_clamp_from_min writes them) and is read at the caller's next synchronisation
+    // (clamp is then NaN here); the lerp kernel takes t >= 1 as "no clamp" exactly
     int ccd_site(const double* xa, const double* xb, PairBuf& pr, cs_step_report* rep, double& clamp,
-                 PairBuf* prev_site = nullptr, int base = 0) {
+                 PairBuf* prev_site = nullptr, int base = 0, bool defer = false) {
         stage(T_BROAD);
         bool done = false;
         const bool no_subset = std::getenv("CS_NO_SUBSET_SITES") != nullptr;
@@ -1201,12 +1205,24 @@ struct cs_scene {
                 std::fprintf(stderr, "[cs site] pairs %lld full-ccd worklist %d march worklist %d\n", P, wl[0], wl[1]);
             }
             CS_CHECK_LAUNCH();
-            CS_RET(sync_scalars(__LINE__));
-            if (trace_sites) std::fprintf(stderr, "[cs site] min march toi %.6g\n", h_scal[S_CLAMP_MIN]);
-            if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;
-            clamp = h_scal[S_CLAMP];
+            if (defer) {
+                clamp = NAN;
+            } else {
+                CS_RET(sync_scalars(__LINE__));
+                if (trace_sites) std::fprintf(stderr, "[cs site] min march toi %.6g\n", h_scal[S_CLAMP_MIN]);
+                if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;
+                clamp = h_scal[S_CLAMP];
+            }
         } else {
             clamp = 1.0;
+            if (defer) {  // no pairs: clamp 1, no penetration, on the device too
+                unsigned long long* min_slot = reinterpret_cast<unsigned long long*>(d_scal.p + S_MINBITS);
+                k_fill_u64<<<1, 32, 0, s>>>(min_slot, 1, 0x7ff0000000000000ull);
+                k_clamp_from_min<<<1, 1, 0, s>>>(min_slot, cfg.alpha, d_scal.p + S_CLAMP_MIN);
+                launches += 2;
+                CS_CHECK_LAUNCH();
+                clamp = NAN;
+            }
         }
         if (rep) {
             rep->full_ccd_calls += 1;
@@ -1264,12 +1280,15 @@ struct cs_scene {
         if (nw_.P == 0) return 0;
         CS_TRY(cudaMemsetAsync(nw_.life.p, 0, sizeof(int) * nw_.P, s));
         if (old.P == 0) return 0;
-        CS_TRY(cudaMemsetAsync(d_iscal.p + I_LIVE, 0, sizeof(int), s));
-        k_count_nonzero<<<grid(old.P), 256, 0, s>>>(old.life.p, old.P, d_iscal.p + I_LIVE);
-        ++launches;
-        CS_TRY(cudaMemcpyAsync(&h_iscal[I_LIVE], d_iscal.p + I_LIVE, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync(__LINE__));
-        const long long live = h_iscal[I_LIVE];
+        long long live = live_pairs;  // bound from the last partial pass over `old` (engaged count)
+        if (live < 0) {
+            CS_TRY(cudaMemsetAsync(d_iscal.p + I_LIVE, 0, sizeof(int), s));
+            k_count_nonzero<<<grid(old.P), 256, 0, s>>>(old.life.p, old.P, d_iscal.p + I_LIVE);
+            ++launches;
+            CS_TRY(cudaMemcpyAsync(&h_iscal[I_LIVE], d_iscal.p + I_LIVE, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CS_TRY(hsync(__LINE__));
+            live = h_iscal[I_LIVE];
+        }
         if (live == 0) return 0;
         unsigned long long cap = 1024;
         while (cap < 2ull * (unsigned long long)live) cap <<= 1;
@@ -1799,6 +1818,7 @@ void cs_scene::release() {
 int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_report* rep) {
     launches = 0;
     n_syncs = 0;
+    live_pairs = -1;
     const long long plan_reuses0 = plan_reuses;
     ev_used = 0;
     spans.clear();
@@ -1837,8 +1857,12 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     // ---- warm start (stepper.py:384-400): x = z (pins already at pin_next)
     double* xcl = xc_w.p;  // cloth rows of the candidate world array
     CS_TRY(cudaMemcpyAsync(xcl, z.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
-    CS_RET(sync_scalars(__LINE__));
-    if (h_iscal[I_BAD]) return CS_NONFINITE;
+    // the non-finite check of the inertia target is read at the warm start's first
+    // synchronisation (nothing in between writes I_BAD; a failing step commits nothing)
+    bool inertia_unchecked = true;
+    // toi_exit on the device: min over the outer sites' clamps (stepper.py:556-558)
+    k_set_scalar<<<1, 1, 0, s>>>(d_scal.p + S_TOIEXIT, 1.0);
+    ++launches;
     int ws_iters = 0;
     for (int it = 0; it < cfg.warm_start_cap; ++it) {
         CS_RET(assemble_rhs(z.p, xcl, false));
@@ -1850,6 +1874,8 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         k_scatter_rows<<<grid(nf), 256, 0, s>>>(xf.p, free_ids.p, nf, xcl);
         ++launches;
         CS_RET(sync_scalars(__LINE__));
+        if (inertia_unchecked && h_iscal[I_BAD]) return CS_NONFINITE;
+        inertia_unchecked = false;
         ++ws_iters;
         const double dx = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
         if (dx < cfg.eps_initial) break;
@@ -1863,9 +1889,9 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         CS_TRY(cudaMemcpyAsync(xc_w.p + 3LL * n, obs_next, sizeof(double) * 3 * nobs, cudaMemcpyDeviceToDevice, s));
     }
     double tc = 1.0;
-    CS_RET(ccd_site(xs_w.p, xc_w.p, *cur, rep, tc, nullptr, 2));
-    // x_acc = clamp; anchor = x_acc (stepper.py:475-480)
-    CS_RET(set_clamp_value(tc));
+    CS_RET(ccd_site(xs_w.p, xc_w.p, *cur, rep, tc, nullptr, 2, true));
+    // x_acc = clamp; anchor = x_acc (stepper.py:475-480); the clamp factor is read on the
+    // device, its penetration flag at the next synchronisation (below)
     CS_RET(lerp_world(xs_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));
     CS_TRY(cudaMemcpyAsync(xc_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
     CS_TRY(cudaMemcpyAsync(anchor_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
@@ -1875,6 +1901,8 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     CS_RET(engage(*cur));
     CS_TRY(cudaMemcpyAsync(prev_outer.p, xcl, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
     CS_RET(sync_scalars(__LINE__));
+    if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;  // the first site (_clamp, stepper.py:445-452)
+    if (inertia_unchecked && h_iscal[I_BAD]) return CS_NONFINITE;
     long long A = h_iscal[I_ENG];
     if (cur->split_valid) cur->n_near = h_iscal[I_NEAR];
 
@@ -1946,7 +1974,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             if (cur->P) {
                 const NdbArgs na{cur->kind.p, cur->idx.p, anchor_w.p, xc_w.p, pat, cur->bary.p, cur->normal.p,
                                  cfg.d_hat, cfg.ndb_k, cfg.ndb_base, cur->life.p, cur->weight.p, cur->engaged.p,
-                                 0, nullptr, 1};
+                                 0, nullptr, 1, nullptr};
                 if (cur->split_valid) {
                     // near list: the full classifier; far list (after it, reversed): gated on the
                     // largest vertex displacement anchor -> candidate (k_partial_far)
@@ -1970,6 +1998,9 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             dx_last = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
             A = h_iscal[I_ENG];
             plan_new = h_iscal[I_NEW];
+            // (a bound on the live count from the engaged count sizes the carry's table 2-3x
+            // larger than the count pass does; the larger fill / probe cost more than the
+            // count's synchronisation saves, so the carry keeps its count)
 
             if (cfg.iteration_cap && lg >= cfg.iteration_cap) {
                 cap_hit = true;
@@ -1981,24 +2012,27 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         last_loop_lg = lg_loop;
         // fresh pair set + line-search filter at the end of every outer loop (stepper.py:547-570)
         double tout = 1.0;
-        CS_RET(ccd_site(anchor_w.p, xc_w.p, *nxt, rep, tout, nullptr, 1));
-        if (tout < 1.0) {
-            CS_RET(set_clamp_value(tout));
-            CS_RET(lerp_world(anchor_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));
-            CS_TRY(cudaMemcpyAsync(xc_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
-            toi_exit = std::min(toi_exit, tout);
-        }
+        CS_RET(ccd_site(anchor_w.p, xc_w.p, *nxt, rep, tout, nullptr, 1, true));
+        // truncation with the device clamp (k_lerp: t >= 1 keeps the candidate exactly),
+        // toi_exit folded on the device; the penetration flag is read at this loop's sync
+        CS_RET(lerp_world(anchor_w.p, xc_w.p, d_scal.p + S_CLAMP, tmp_w.p));
+        CS_TRY(cudaMemcpyAsync(xc_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
+        k_min_scalar<<<1, 1, 0, s>>>(d_scal.p + S_TOIEXIT, d_scal.p + S_CLAMP);
+        ++launches;
         CS_TRY(cudaMemcpyAsync(anchor_w.p, xc_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
         stage(T_FULL);
         CS_RET(witness(*nxt, anchor_w.p));
         if (cfg.barrier_mode != CS_BARRIER_DBB) CS_RET(carry(*cur, *nxt));
         CS_RET(engage(*nxt));
         std::swap(cur, nxt);
+        live_pairs = -1;
         // outer progress (stepper.py:574-578)
         CS_RET(sqnorm(xcl, prev_outer.p, nf, free_ids.p, S_SQ));
         // prev_outer holds cloth rows; compare over free rows only
         CS_TRY(cudaMemcpyAsync(prev_outer.p, xcl, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
         CS_RET(sync_scalars(__LINE__));
+        if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;  // this loop's site
+        toi_exit = h_scal[S_TOIEXIT];
         A = h_iscal[I_ENG];
         if (cur->split_valid) cur->n_near = h_iscal[I_NEAR];
         const double d_out = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
@@ -2410,7 +2444,7 @@ int cs_partial_ccd(const int8_t* kind, const int* idx4, const double* x_start, c
     CS_TRY(cudaMemsetAsync(normal.p, 0, sizeof(double) * 3 * P, s));
     CS_TRY(cudaMemsetAsync(life.p, 0, sizeof(int) * P, s));
     const NdbArgs na{kind, (const int4*)idx4, x_start, x_end, tmp.pat, bary.p, normal.p, -1.0, 1.0, 2.0,
-                     life.p, weight.p, eng.p, 1, active, 0};
+                     life.p, weight.p, eng.p, 1, active, 0, nullptr};
     k_partial_ndb<<<(int)((P + 127) / 128), 128, 0, s>>>(na, P, nullptr, PlanView{}, nullptr);
     CS_CHECK_LAUNCH();
     CS_TRY(cudaStreamSynchronize(s));

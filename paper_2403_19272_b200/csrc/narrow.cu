@@ -886,9 +886,11 @@ struct NdbArgs {
     int write_active;
     uint8_t* __restrict__ active_out;
     int proj_is_witness;
+    int* __restrict__ live_count;  // nullable: pairs left with a nonzero life span (the carry's table size)
 };
 
-__device__ __forceinline__ void ndb_pair(const NdbArgs& A, const PlanView& plan, int64_t i, bool& eng, bool& fresh) {
+__device__ __forceinline__ void ndb_pair(const NdbArgs& A, const PlanView& plan, int64_t i, bool& eng, bool& fresh,
+                                         bool& alive) {
     const int8_t* __restrict__ kind = A.kind;
     const int4* __restrict__ idx = A.idx;
     const double* __restrict__ xa = A.xa;
@@ -958,6 +960,7 @@ __device__ __forceinline__ void ndb_pair(const NdbArgs& A, const PlanView& plan,
     const double gap = dot3(s1 - s2, ld3(normal, i));
     act = act || (gap < d_hat);
     int lf = act ? min(life[i] + 1, 64) : 0;
+    alive = lf > 0;
     eng = act || (gap < 2.0 * d_hat);
     life[i] = lf;
     engaged[i] = eng;
@@ -984,9 +987,10 @@ __device__ __forceinline__ void ndb_pair(const NdbArgs& A, const PlanView& plan,
     }
 }
 
-__device__ __forceinline__ void ndb_counts(const PlanView& plan, int* __restrict__ eng_count, int64_t i, bool eng,
-                                           bool fresh) {
+__device__ __forceinline__ void ndb_counts(const PlanView& plan, int* __restrict__ eng_count,
+                                           int* __restrict__ live_count, int64_t i, bool eng, bool fresh, bool alive) {
     if (eng_count != nullptr) block_count(eng, eng_count);
+    if (live_count != nullptr) block_count(alive, live_count);
     // engaged pairs outside the driver's stamp plan, appended (any order: the driver
     // sorts their entries by merge key) for the plan merge
     if (plan.n_new != nullptr) {
@@ -1009,9 +1013,9 @@ __global__ void __launch_bounds__(128, 5) k_partial_ndb(NdbArgs A, int64_t n, in
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid = k < n;
     const int64_t i = !valid ? 0 : (wl != nullptr ? (int64_t)wl[k] : k);
-    bool eng = false, fresh = false;
-    if (valid) ndb_pair(A, plan, i, eng, fresh);
-    ndb_counts(plan, eng_count, i, eng, fresh);
+    bool eng = false, fresh = false, alive = false;
+    if (valid) ndb_pair(A, plan, i, eng, fresh, alive);
+    ndb_counts(plan, eng_count, A.live_count, i, eng, fresh, alive);
 }
 
 // The far list of the split (NearPair): a far pair whose witness distance d exceeds
@@ -1028,7 +1032,7 @@ __global__ void __launch_bounds__(128, 5) k_partial_far(NdbArgs A, int64_t n, in
         const int64_t k = b0 + threadIdx.x;
         const bool valid = k < n;
         const int64_t i = valid ? (int64_t)wl[k] : 0;
-        bool eng = false, fresh = false;
+        bool eng = false, fresh = false, alive = false;
         if (valid) {
             const int4 id = A.idx[i];
             const bool vt = A.kind[i] == CS_VT;
@@ -1042,10 +1046,10 @@ __global__ void __launch_bounds__(128, 5) k_partial_far(NdbArgs A, int64_t n, in
                 A.engaged[i] = 0;
                 A.weight[i] = 0.0;
             } else {
-                ndb_pair(A, plan, i, eng, fresh);
+                ndb_pair(A, plan, i, eng, fresh, alive);
             }
         }
-        ndb_counts(plan, eng_count, i, eng, fresh);
+        ndb_counts(plan, eng_count, A.live_count, i, eng, fresh, alive);
     }
 }
 

@@ -918,6 +918,10 @@ __global__ void k_scatter_rows(const double* __restrict__ src, const int* __rest
 }
 
 // out = a + t (b - a)   (line-search clamp, stepper.py:477, 555, 586)
+__global__ void k_set_scalar(double* __restrict__ p, double v) { *p = v; }
+// *acc = min(*acc, *v) (fmin: a NaN operand is ignored)
+__global__ void k_min_scalar(double* __restrict__ acc, const double* __restrict__ v) { *acc = fmin(*acc, *v); }
+
 __global__ void k_lerp(const double* __restrict__ a, const double* __restrict__ b, const double* __restrict__ tptr,
                        int64_t m, double* __restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
