@@ -334,7 +334,6 @@ struct cs_scene {
     long long plan_new = 0;      // engaged pairs outside the plan at the last partial CCD
     long long plan_reuses = 0;
     bool fused_ok = false;       // k_partial_ndb wrote this plan's stamps at the candidate
-    long long live_pairs = -1;   // upper bound of *cur's nonzero life spans after its last partial pass (-1: unknown)
     int last_loop_lg = 0;        // LG iterations of the last outer loop (plan worth building?)
     bool lazy_exit = std::getenv("CS_NO_LAZY_EXIT") == nullptr;  // read at scene creation
     bool far_pairs = std::getenv("CS_NO_FAR_PAIRS") == nullptr;  // partial CCD near / far split
@@ -1235,10 +1234,28 @@ struct cs_scene {
     int witness(PairBuf& pr, const double* xw) {
         if (pr.P == 0) return 0;
         k_witness<<<grid(pr.P, 128), 128, 0, s>>>(pr.kind.p, pr.idx.p, xw, pr.P, pr.bary.p, pr.dist.p,
-                                                  pr.normal.p, nullptr, nullptr);
+                                                  pr.normal.p, nullptr, nullptr, EngageOut{});
         ++launches;
         CS_CHECK_LAUNCH();
         return 0;
+    }
+
+    // witness refresh at the anchor + engaged set and weights of a fresh site (NDB: one
+    // pass; the life spans must be in place: zeroed or carried); count lands in I_ENG
+    int witness_engage(PairBuf& pr, const double* xw) {
+        if (cfg.barrier_mode == CS_BARRIER_DBB) {
+            CS_RET(witness(pr, xw));
+            return engage(pr);
+        }
+        plan_valid = false;
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
+        if (pr.P == 0) return 0;
+        k_witness<<<grid(pr.P, 128), 128, 0, s>>>(pr.kind.p, pr.idx.p, xw, pr.P, pr.bary.p, pr.dist.p,
+                                                  pr.normal.p, nullptr, nullptr,
+                                                  EngageOut{pr.toi.p, pr.life.p, cfg.d_hat, cfg.ndb_k, cfg.ndb_base,
+                                                            pr.engaged.p, pr.weight.p, d_iscal.p + I_ENG});
+        ++launches;
+        return near_split(pr);
     }
 
     // engaged set + weights after a site; count lands in I_ENG
@@ -1253,6 +1270,11 @@ struct cs_scene {
             k_engage_init<<<grid(pr.P), 256, 0, s>>>(pr.toi.p, pr.dist.p, pr.life.p, pr.P, cfg.d_hat, cfg.ndb_k,
                                                      cfg.ndb_base, pr.engaged.p, pr.weight.p, d_iscal.p + I_ENG);
         ++launches;
+        return near_split(pr);
+    }
+
+    // partial CCD near / far split of a freshly engaged set (k_near_split's argument)
+    int near_split(PairBuf& pr) {
         pr.split_valid = false;
         // (with a cached stamp plan the partial pass is bound by the plan pairs' fused
         // stamp writes, and the split only adds its own passes: single-iteration outer
@@ -1280,15 +1302,12 @@ struct cs_scene {
         if (nw_.P == 0) return 0;
         CS_TRY(cudaMemsetAsync(nw_.life.p, 0, sizeof(int) * nw_.P, s));
         if (old.P == 0) return 0;
-        long long live = live_pairs;  // bound from the last partial pass over `old` (engaged count)
-        if (live < 0) {
-            CS_TRY(cudaMemsetAsync(d_iscal.p + I_LIVE, 0, sizeof(int), s));
-            k_count_nonzero<<<grid(old.P), 256, 0, s>>>(old.life.p, old.P, d_iscal.p + I_LIVE);
-            ++launches;
-            CS_TRY(cudaMemcpyAsync(&h_iscal[I_LIVE], d_iscal.p + I_LIVE, sizeof(int), cudaMemcpyDeviceToHost, s));
-            CS_TRY(hsync(__LINE__));
-            live = h_iscal[I_LIVE];
-        }
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_LIVE, 0, sizeof(int), s));
+        k_count_nonzero<<<grid(old.P), 256, 0, s>>>(old.life.p, old.P, d_iscal.p + I_LIVE);
+        ++launches;
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_LIVE], d_iscal.p + I_LIVE, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(hsync(__LINE__));
+        const long long live = h_iscal[I_LIVE];
         if (live == 0) return 0;
         unsigned long long cap = 1024;
         while (cap < 2ull * (unsigned long long)live) cap <<= 1;
@@ -1818,7 +1837,6 @@ void cs_scene::release() {
 int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_report* rep) {
     launches = 0;
     n_syncs = 0;
-    live_pairs = -1;
     const long long plan_reuses0 = plan_reuses;
     ev_used = 0;
     spans.clear();
@@ -1896,9 +1914,8 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
     CS_TRY(cudaMemcpyAsync(xc_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
     CS_TRY(cudaMemcpyAsync(anchor_w.p, tmp_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
     stage(T_FULL);
-    CS_RET(witness(*cur, anchor_w.p));
     if (cur->P) CS_TRY(cudaMemsetAsync(cur->life.p, 0, sizeof(int) * cur->P, s));
-    CS_RET(engage(*cur));
+    CS_RET(witness_engage(*cur, anchor_w.p));
     CS_TRY(cudaMemcpyAsync(prev_outer.p, xcl, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
     CS_RET(sync_scalars(__LINE__));
     if (h_scal[S_CLAMP_BAD] != 0.0) return CS_PENETRATION;  // the first site (_clamp, stepper.py:445-452)
@@ -1998,9 +2015,6 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             dx_last = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
             A = h_iscal[I_ENG];
             plan_new = h_iscal[I_NEW];
-            // (a bound on the live count from the engaged count sizes the carry's table 2-3x
-            // larger than the count pass does; the larger fill / probe cost more than the
-            // count's synchronisation saves, so the carry keeps its count)
 
             if (cfg.iteration_cap && lg >= cfg.iteration_cap) {
                 cap_hit = true;
@@ -2021,11 +2035,10 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
         ++launches;
         CS_TRY(cudaMemcpyAsync(anchor_w.p, xc_w.p, sizeof(double) * 3 * nw, cudaMemcpyDeviceToDevice, s));
         stage(T_FULL);
-        CS_RET(witness(*nxt, anchor_w.p));
+        // life spans carried first (keys only), then witness + engagement in one pass
         if (cfg.barrier_mode != CS_BARRIER_DBB) CS_RET(carry(*cur, *nxt));
-        CS_RET(engage(*nxt));
+        CS_RET(witness_engage(*nxt, anchor_w.p));
         std::swap(cur, nxt);
-        live_pairs = -1;
         // outer progress (stepper.py:574-578)
         CS_RET(sqnorm(xcl, prev_outer.p, nf, free_ids.p, S_SQ));
         // prev_outer holds cloth rows; compare over free rows only
@@ -2461,7 +2474,7 @@ int cs_pair_witness(const int8_t* kind, const int* idx4, const double* x, long l
     if (P < 0) return CS_BAD_ARGUMENT;
     if (P == 0) return 0;
     k_witness<<<(int)((P + 127) / 128), 128, 0, (cudaStream_t)stream>>>(kind, (const int4*)idx4, x, P, bary, dist,
-                                                                        normal, p1, p2);
+                                                                        normal, p1, p2, EngageOut{});
     CS_CHECK_LAUNCH();
     return 0;
 }

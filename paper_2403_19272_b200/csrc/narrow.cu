@@ -747,12 +747,26 @@ __global__ void k_clamp_from_min(const unsigned long long* __restrict__ min_slot
 }
 
 // Witness refresh: bary/params, distance and separating normal (stepper.py:194-216).
+// NDB engagement of a fresh pair set fused into its witness pass (stepper.py:483-487,
+// 564-565): engaged = full-CCD hit or witness distance < 2 d_hat, weight from the life
+// span (k_engage_init's arithmetic); engaged == null: witness only.
+struct EngageOut {
+    const double* __restrict__ toi;
+    const int* __restrict__ life;
+    double d_hat, k_ndb, base;
+    uint8_t* __restrict__ engaged;
+    double* __restrict__ weight;
+    int* __restrict__ count;
+};
+__device__ __forceinline__ double ndb_weight(int life, double k, double base);
+
 __global__ void __launch_bounds__(128, 8) k_witness(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                           const double* __restrict__ x, int64_t P, double* __restrict__ bary,
                           double* __restrict__ dist, double* __restrict__ normal, double* __restrict__ p1_out,
-                          double* __restrict__ p2_out) {
+                          double* __restrict__ p2_out, EngageOut eo) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= P) return;
+    bool eng = false;
+    if (i < P) {
     const int kd = kind[i];
     Corners a = gather4(x, idx[i]);
     d3 p1, p2;
@@ -780,6 +794,14 @@ __global__ void __launch_bounds__(128, 8) k_witness(const int8_t* __restrict__ k
     if (normal) st3(normal, i, n);
     if (p1_out) st3(p1_out, i, p1);
     if (p2_out) st3(p2_out, i, p2);
+    if (eo.engaged != nullptr) {
+        const double t = eo.toi[i];
+        eng = (t == t) || (d < 2.0 * eo.d_hat);
+        eo.engaged[i] = eng;
+        eo.weight[i] = eng ? ndb_weight(eo.life[i], eo.k_ndb, eo.base) : 0.0;
+    }
+    }
+    if (eo.count != nullptr) block_count(eng, eo.count);
 }
 
 __device__ __forceinline__ double ndb_weight(int life, double k, double base) {
