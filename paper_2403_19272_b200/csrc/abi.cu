@@ -153,6 +153,8 @@ struct EntryBuf {
     int n_over_h = 0;
     DBuf<double> box, part, inv;
     DBuf<int> count, offset, prim, perm, perm_s, prim_s, run, n_run, bstart, bend, over, n_over, pcount, poffset;
+    DBuf<int> lrows, lcount, loff, n_lrows;  // rows of long bucket runs (k_long_ee / k_long_vt)
+    long long n_lrows_h = 0;
     DBuf<long long> iters, iter_off;
     DBuf<unsigned> masks;
     DBuf<unsigned> key, key_s;
@@ -182,7 +184,7 @@ struct EntryBuf {
         return EntryTable{key_s.p, prim_s.p, code_s.p, zb_s.p, run.p, n_run.p, bstart.p, bend.p, (int)m};
     }
     void release() {
-        for (DBuf<int>* b : {&count, &offset, &prim, &perm, &perm_s, &prim_s, &run, &n_run, &bstart, &bend, &over,
+        for (DBuf<int>* b : {&lrows, &lcount, &loff, &n_lrows, &count, &offset, &prim, &perm, &perm_s, &prim_s, &run, &n_run, &bstart, &bend, &over,
                              &n_over, &pcount, &poffset})
             b->release();
         iters.release(); iter_off.release(); masks.release();
@@ -709,6 +711,21 @@ struct cs_scene {
         CS_CHECK_LAUNCH();
         return 0;
     }
+    // entries of long bucket runs (LongRow) into G.lrows, count in G.n_lrows (device)
+    int long_rows(EntryBuf& G, const LongRow& pred) {
+        CS_RET(G.n_lrows.ensure(1));
+        CS_TRY(cudaMemsetAsync(G.n_lrows.p, 0, sizeof(int), s));
+        if (!G.m) return 0;
+        CS_RET(G.lrows.ensure(G.m));
+        cub::CountingInputIterator<int> it(0);
+        size_t bytes = 0;
+        cub::DeviceSelect::If(nullptr, bytes, it, G.lrows.p, G.n_lrows.p, (int)G.m, pred, s);
+        CS_RET(cub_tmp.ensure(bytes));
+        CS_TRY(cub::DeviceSelect::If(cub_tmp.p, bytes, it, G.lrows.p, G.n_lrows.p, (int)G.m, pred, s));
+        ++launches;
+        return 0;
+    }
+
     int run_blocks(long long m) {
         return (int)std::max<long long>(1, std::min<long long>((m + kPairWarps - 1) / kPairWarps, 32LL * sm_count));
     }
@@ -764,15 +781,33 @@ struct cs_scene {
             CS_RET(G->iter_off.ensure(G->m + 1));
             CS_TRY(cudaMemsetAsync(G->iters.p, 0, sizeof(long long) * (G->m + 1), s));
         }
-        if (vtab.m) k_run_iters<<<grid(vtab.m), 256, 0, s>>>(VT, TT, 1, vtab.iters.p);
-        if (etab.m) k_run_iters<<<grid(etab.m), 256, 0, s>>>(ET, ET, 0, etab.iters.p);
+        CS_TRY(cudaMemsetAsync(d_iscal.p + I_COUNT + 4, 0, 2 * sizeof(int), s));
+        if (vtab.m) k_run_iters<<<grid(vtab.m), 256, 0, s>>>(VT, TT, 1, vtab.iters.p, d_iscal.p + I_COUNT + 4);
+        if (etab.m) k_run_iters<<<grid(etab.m), 256, 0, s>>>(ET, ET, 0, etab.iters.p, d_iscal.p + I_COUNT + 5);
         launches += 2;
         CS_RET(scan(vtab.iters.p, vtab.iter_off.p, (int)vtab.m + 1));
         CS_RET(scan(etab.iters.p, etab.iter_off.p, (int)etab.m + 1));
         long long* hits_h = reinterpret_cast<long long*>(h_scal + S_COUNT);
         CS_TRY(cudaMemcpyAsync(&hits_h[0], vtab.iter_off.p + vtab.m, sizeof(long long), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&hits_h[1], etab.iter_off.p + etab.m, sizeof(long long), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 4], d_iscal.p + I_COUNT + 4, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                               s));
         CS_TRY(hsync(__LINE__));
+        // rows of runs too long for one warp (dense piles): one thread each; only when
+        // such runs exist (one more synchronisation for their count)
+        const bool long_vt = vtab.m && h_iscal[I_COUNT + 4], long_ee = etab.m && h_iscal[I_COUNT + 5];
+        vtab.n_lrows_h = etab.n_lrows_h = 0;
+        if (long_vt || long_ee) {
+            if (long_vt) CS_RET(long_rows(vtab, LongRow{VT.key, VT.bstart, VT.bend, TT.bstart, TT.bend}));
+            if (long_ee) CS_RET(long_rows(etab, LongRow{ET.key, ET.bstart, ET.bend, nullptr, nullptr}));
+            if (long_vt)
+                CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 4], vtab.n_lrows.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            if (long_ee)
+                CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 5], etab.n_lrows.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CS_TRY(hsync(__LINE__));
+            vtab.n_lrows_h = long_vt ? h_iscal[I_COUNT + 4] : 0;
+            etab.n_lrows_h = long_ee ? h_iscal[I_COUNT + 5] : 0;
+        }
         CS_RET(vtab.masks.ensure(std::max<long long>(hits_h[0], 1)));
         CS_RET(etab.masks.ensure(std::max<long long>(hits_h[1], 1)));
         // pair counts: [VT runs][VT oversize][EE runs][EE oversize]
@@ -814,18 +849,43 @@ struct cs_scene {
             k_over_ee<0><<<grid(n_oee, 64), 64, 0, s>>>(etab.over.p, n_oee, etab.is_over.p, etab.box.p, new_, W, O);
             ++launches;
         }
+        for (EntryBuf* G : {&vtab, &etab}) {
+            CS_RET(G->lcount.ensure(G->n_lrows_h + 1));
+            CS_RET(G->loff.ensure(G->n_lrows_h + 1));
+            CS_TRY(cudaMemsetAsync(G->lcount.p, 0, sizeof(int) * (G->n_lrows_h + 1), s));
+        }
+        if (vtab.n_lrows_h) {
+            O.counts = vtab.lcount.p;
+            k_long_vt<0><<<grid(vtab.n_lrows_h, 128), 128, 0, s>>>(VT, TT, vlo.p, vhi.p, ttab.box.p, ttab.inv.p, W,
+                                                                   vtab.lrows.p, vtab.n_lrows.p, O);
+            ++launches;
+        }
+        if (etab.n_lrows_h) {
+            O.counts = etab.lcount.p;
+            k_long_ee<0><<<grid(etab.n_lrows_h, 128), 128, 0, s>>>(ET, etab.box.p, etab.inv.p, W, etab.lrows.p,
+                                                                   etab.n_lrows.p, O);
+            ++launches;
+        }
         CS_CHECK_LAUNCH();
         CS_RET(scan(vtab.pcount.p, vtab.poffset.p, (int)vtab.m + 1));
         CS_RET(scan(oc_vt, oo_vt, n_ovt + 1));
         CS_RET(scan(etab.pcount.p, etab.poffset.p, (int)etab.m + 1));
         CS_RET(scan(oc_ee, oo_ee, n_oee + 1));
+        CS_RET(scan(vtab.lcount.p, vtab.loff.p, (int)vtab.n_lrows_h + 1));
+        CS_RET(scan(etab.lcount.p, etab.loff.p, (int)etab.n_lrows_h + 1));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 0], vtab.poffset.p + vtab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 1], oo_vt + n_ovt, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 2], etab.poffset.p + etab.m, sizeof(int), cudaMemcpyDeviceToHost, s));
         CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 3], oo_ee + n_oee, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 4], vtab.loff.p + vtab.n_lrows_h, sizeof(int), cudaMemcpyDeviceToHost,
+                               s));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 5], etab.loff.p + etab.n_lrows_h, sizeof(int), cudaMemcpyDeviceToHost,
+                               s));
         CS_TRY(hsync(__LINE__));
+        // rows: [VT runs c0][VT long runs c4][VT oversize c1][EE runs c2][EE long runs c5][EE oversize c3]
         const long long c0 = h_iscal[I_COUNT + 0], c1 = h_iscal[I_COUNT + 1], c2 = h_iscal[I_COUNT + 2], c3 = h_iscal[I_COUNT + 3];
-        const long long P = c0 + c1 + c2 + c3;
+        const long long c4 = h_iscal[I_COUNT + 4], c5 = h_iscal[I_COUNT + 5];
+        const long long P = c0 + c1 + c2 + c3 + c4 + c5;
         CS_RET(pr.reserve(std::max<long long>(P, 1)));
         auto out_at = [&](long long base, const int* offs) {
             return PairOut{nullptr, offs, pr.kind.p + base, pr.idx.p + base, pr.keys.p + base};
@@ -834,20 +894,28 @@ struct cs_scene {
             k_pairs_vt<1><<<run_blocks(vtab.m), 32 * kPairWarps, 0, s>>>(VT, TT, vlo.p, vhi.p, ttab.box.p, ttab.inv.p, W,
                                                                        vtab.iter_off.p, vtab.masks.p,
                                                                        out_at(0, vtab.poffset.p));
+        if (vtab.n_lrows_h && c4)
+            k_long_vt<1><<<grid(vtab.n_lrows_h, 128), 128, 0, s>>>(VT, TT, vlo.p, vhi.p, ttab.box.p, ttab.inv.p, W,
+                                                                   vtab.lrows.p, vtab.n_lrows.p,
+                                                                   out_at(c0, vtab.loff.p));
         if (n_ovt && c1)
             k_over_vt<1><<<grid(n_ovt, 64), 64, 0, s>>>(vtab.over.p, vtab.n_over_h, ttab.over.p, ttab.n_over_h,
                                                          vtab.is_over.p, vlo.p, vhi.p, ttab.box.p, ntw, W,
-                                                         out_at(c0, oo_vt));
+                                                         out_at(c0 + c4, oo_vt));
+        const long long e0 = c0 + c4 + c1;  // first EE row
         if (etab.m && c2)
             k_pairs_ee<1><<<run_blocks(etab.m), 32 * kPairWarps, 0, s>>>(ET, etab.box.p, etab.inv.p, W,
                                                                        etab.iter_off.p, etab.masks.p,
-                                                                       out_at(c0 + c1, etab.poffset.p));
+                                                                       out_at(e0, etab.poffset.p));
+        if (etab.n_lrows_h && c5)
+            k_long_ee<1><<<grid(etab.n_lrows_h, 128), 128, 0, s>>>(ET, etab.box.p, etab.inv.p, W, etab.lrows.p,
+                                                                   etab.n_lrows.p, out_at(e0 + c2, etab.loff.p));
         if (n_oee && c3)
             k_over_ee<1><<<grid(n_oee, 64), 64, 0, s>>>(etab.over.p, n_oee, etab.is_over.p, etab.box.p, new_, W,
-                                                        out_at(c0 + c1 + c2, oo_ee));
-        launches += 4;
-        if (c2 + c3) {
-            k_ee_orient<<<grid(c2 + c3), 256, 0, s>>>(pr.keys.p + c0 + c1, pr.idx.p + c0 + c1, c2 + c3, W);
+                                                        out_at(e0 + c2 + c5, oo_ee));
+        launches += 6;
+        if (c2 + c5 + c3) {
+            k_ee_orient<<<grid(c2 + c5 + c3), 256, 0, s>>>(pr.keys.p + e0, pr.idx.p + e0, c2 + c5 + c3, W);
             ++launches;
         }
         CS_CHECK_LAUNCH();

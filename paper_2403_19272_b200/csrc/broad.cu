@@ -540,29 +540,49 @@ __device__ __forceinline__ void tri_index(int k, int m, int& i, int& j) {
 }
 
 // warp iterations a run takes (must mirror the loops below exactly)
-__device__ __forceinline__ long long iters_ee(int m) {
-    if (m < 2) return 0;
-    if (m <= kRunCap) return ((long long)m * (m - 1) / 2 + 31) / 32;
+// (runs longer than the staging caps are enumerated by k_long_ee / k_long_vt, one thread
+// per row, and take no iterations here)
+// A run beyond the staging caps is enumerated by one warp row by row (lanes over the
+// partners) while that takes at most kLongIters warp iterations; longer runs (dense
+// piles) go to k_long_ee / k_long_vt, one thread per row.
+constexpr long long kLongIters = 256;
+__host__ __device__ __forceinline__ long long serial_iters_ee(int m) {
     const long long n = m - 1, q = n / 32, r = n % 32;  // sum_{L=1..n} ceil(L/32)
     return 32 * q * (q + 1) / 2 + (q + 1) * r;
 }
+__host__ __device__ __forceinline__ bool ee_long(int m) { return m > kRunCap && serial_iters_ee(m) > kLongIters; }
+__host__ __device__ __forceinline__ bool vt_long(int mv, int mt) {
+    return mt > 0 && mv > 0 && !(mv <= kRunCapV && mt <= kRunCap) && (long long)mv * ((mt + 31) / 32) > kLongIters;
+}
+__device__ __forceinline__ long long iters_ee(int m) {
+    if (m < 2 || ee_long(m)) return 0;
+    if (m <= kRunCap) return ((long long)m * (m - 1) / 2 + 31) / 32;
+    return serial_iters_ee(m);
+}
 __device__ __forceinline__ long long iters_vt(int mv, int mt) {
-    if (mt <= 0 || mv <= 0) return 0;
+    if (mt <= 0 || mv <= 0 || vt_long(mv, mt)) return 0;
     if (mv <= kRunCapV && mt <= kRunCap) return ((long long)mv * mt + 31) / 32;
     return (long long)mv * ((mt + 31) / 32);
 }
 
 // per run: warp iterations (for the ballot buffer); entries beyond n_run stay 0
-__global__ void k_run_iters(EntryTable R, EntryTable T, int vt, long long* __restrict__ iters) {
+// (+ *long_flag = 1 when some run goes to the row kernels)
+__global__ void k_run_iters(EntryTable R, EntryTable T, int vt, long long* __restrict__ iters,
+                            int* __restrict__ long_flag) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= R.n_run[0]) return;
     const int b0 = R.run[r], b1 = r + 1 < R.n_run[0] ? R.run[r + 1] : R.m;
+    bool lng;
     if (vt) {
         const unsigned b = R.key[b0];
-        iters[r] = iters_vt(b1 - b0, T.bend[b] - T.bstart[b]);
+        const int mt = T.bend[b] - T.bstart[b];
+        iters[r] = iters_vt(b1 - b0, mt);
+        lng = vt_long(b1 - b0, mt);
     } else {
         iters[r] = iters_ee(b1 - b0);
+        lng = ee_long(b1 - b0);
     }
+    if (lng) atomicOr(long_flag, 1);
 }
 
 // VT per-warp staging, structure of arrays; static flags ride in bit 3 of the
@@ -669,7 +689,7 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
                 cnt += __popc(m);
             }
             if (PASS == 0) __syncwarp();
-        } else if (mt > 0) {
+        } else if (mt > 0 && !vt_long(mv, mt)) {  // moderately long: one warp, rows in turn
             for (int i = vb; i < ve; ++i) {
                 const int v = V.prim[i];
                 const unsigned long long cv = V.code[i];
@@ -694,7 +714,7 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
                     cnt += __popc(m);
                 }
             }
-        }
+        }  // longer runs: k_long_vt
         if (PASS == 0 && lane == 0) O.counts[r] = cnt;
     }
 }
@@ -795,7 +815,7 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_ee(EntryTable E, cons
                 cnt += __popc(msk);
             }
             if (PASS == 0) __syncwarp();
-        } else {
+        } else if (!ee_long(m)) {  // moderately long: one warp, rows in turn
             for (int i = eb; i + 1 < ee; ++i) {
                 const int a = E.prim[i];
                 const unsigned long long ca = E.code[i];
@@ -816,8 +836,89 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_ee(EntryTable E, cons
                     cnt += __popc(msk);
                 }
             }
-        }
+        }  // longer runs: k_long_ee
         if (PASS == 0 && lane == 0) O.counts[r] = cnt;
+    }
+}
+
+// Long bucket runs (dense piles: more entries than the shared-memory staging holds),
+// one thread per row instead of one warp per run (a run of m entries is m rows of up to
+// m tests: the serial tail of a single warp made config 3's late steps 10x slower).
+// Rows are the entries of long runs in table order (LongRow); pass 0 counts a row's
+// hits, pass 1 writes them at the row's scanned offset in (row, partner) order.  Same
+// predicates as the staged path: same cell code, box overlap, the overlap's min corner
+// in this cell (reported once), adjacency / static filters.
+struct LongRow {
+    const unsigned* __restrict__ key;
+    const int* __restrict__ bstart;
+    const int* __restrict__ bend;
+    const int* __restrict__ tstart;  // VT: the triangle table's bucket ranges (null: EE)
+    const int* __restrict__ tend;
+    __host__ __device__ __forceinline__ bool operator()(int e) const {
+        const unsigned b = key[e];
+        const int m = bend[b] - bstart[b];
+        if (tstart == nullptr) return ee_long(m);
+        return vt_long(m, tend[b] - tstart[b]);
+    }
+};
+
+template <int PASS>
+__global__ void k_long_ee(EntryTable E, const double* __restrict__ ebox, const double* __restrict__ inv_cell,
+                          WorldTopo W, const int* __restrict__ rows, const int* __restrict__ n_rows, PairOut O) {
+    const int n = n_rows[0];
+    const double inv = inv_cell[0];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int i = rows[k];
+        const int end = E.bend[E.key[i]];
+        const int a = E.prim[i];
+        const unsigned long long ca = E.code[i];
+        double qlo[3], qhi[3];
+        load_box(ebox, a, qlo, qhi);
+        int row = PASS == 1 ? O.offsets[k] : 0, cnt = 0;
+        for (int j = i + 1; j < end; ++j) {
+            if (E.code[j] != ca) continue;
+            const int f = E.prim[j];
+            double lo[3], hi[3];
+            load_box(ebox, f, lo, hi);
+            if (overlap6(qlo, qhi, lo, hi) && min_corner_in(qlo, lo, inv, ca) && ee_ok(W, a, f)) {
+                if (PASS == 1) write_ee(O, row++, a, f, W);
+                ++cnt;
+            }
+        }
+        if (PASS == 0) O.counts[k] = cnt;
+    }
+}
+
+template <int PASS>
+__global__ void k_long_vt(EntryTable V, EntryTable T, const double* __restrict__ vlo, const double* __restrict__ vhi,
+                          const double* __restrict__ tbox, const double* __restrict__ inv_cell, WorldTopo W,
+                          const int* __restrict__ rows, const int* __restrict__ n_rows, PairOut O) {
+    const int n = n_rows[0];
+    const double inv = inv_cell[0];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int i = rows[k];
+        const unsigned b = V.key[i];
+        const int tb = T.bstart[b], te = T.bend[b];
+        const int v = V.prim[i];
+        const unsigned long long cv = V.code[i];
+        double qlo[3], qhi[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            qlo[c] = vlo[3 * (int64_t)v + c];
+            qhi[c] = vhi[3 * (int64_t)v + c];
+        }
+        int row = PASS == 1 ? O.offsets[k] : 0, cnt = 0;
+        for (int j = tb; j < te; ++j) {
+            if (T.code[j] != cv) continue;
+            const int f = T.prim[j];
+            double lo[3], hi[3];
+            load_box(tbox, f, lo, hi);
+            if (overlap6(qlo, qhi, lo, hi) && min_corner_in(qlo, lo, inv, cv) && vt_ok(W, v, f)) {
+                if (PASS == 1) write_vt(O, row++, v, f, W);
+                ++cnt;
+            }
+        }
+        if (PASS == 0) O.counts[k] = cnt;
     }
 }
 
