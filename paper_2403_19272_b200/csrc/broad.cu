@@ -545,7 +545,7 @@ __device__ __forceinline__ void tri_index(int k, int m, int& i, int& j) {
 // A run beyond the staging caps is enumerated by one warp row by row (lanes over the
 // partners) while that takes at most kLongIters warp iterations; longer runs (dense
 // piles) go to k_long_ee / k_long_vt, one thread per row.
-constexpr long long kLongIters = 256;
+constexpr long long kLongIters = 1024;
 __host__ __device__ __forceinline__ long long serial_iters_ee(int m) {
     const long long n = m - 1, q = n / 32, r = n % 32;  // sum_{L=1..n} ceil(L/32)
     return 32 * q * (q + 1) / 2 + (q + 1) * r;
