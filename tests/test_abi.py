@@ -43,3 +43,28 @@ def test_no_cpu_fallback_without_library(tmp_path):
         _lib._lib = None
         _lib.load(str(tmp_path / "missing.so"))
     _lib._lib = None
+
+
+def _struct_fields(text, tail):
+    end = text.index("} " + tail + ";")
+    start = text.rindex("typedef struct {", 0, end)
+    body = re.sub(r"/\*.*?\*/", "", text[start + len("typedef struct {"):end], flags=re.S)
+    names = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        # "double t_a, t_b" / "double outer_deltas[64]" / "long long a, b"
+        parts = decl.split(",")
+        first = parts[0].split()
+        names.append(re.sub(r"\[.*\]", "", first[-1]).lstrip("*"))
+        names.extend(re.sub(r"\[.*\]", "", p.strip()).lstrip("*") for p in parts[1:])
+    return names
+
+
+def test_report_and_config_layouts_match_header():
+    """cs_step_report / cs_step_config ctypes mirrors: the header's fields in order
+    (a mismatch would silently shift every report field after it)."""
+    text = open(HEADER).read()
+    assert [f[0] for f in _lib.StepReportC._fields_] == _struct_fields(text, "cs_step_report")
+    assert [f[0] for f in _lib.StepConfigC._fields_] == _struct_fields(text, "cs_step_config")
