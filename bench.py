@@ -627,7 +627,7 @@ def run_ours(args, ws, rank, local):
         q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         q0.record(stream)
         creps = []
-        for _ in range(2):
+        for _ in range(4):
             preps.append(s0.step())
             creps.append(s0.last_report_c)
         q1.record(stream)

@@ -39,6 +39,17 @@ __device__ __forceinline__ double norm3(d3 a) {
 __device__ __forceinline__ d3 cross3(d3 a, d3 b) {
     return d3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
+// 32-byte stamp records (x, y, z, w) move as one 256-bit access (LDG/STG .256 on sm_100a)
+// instead of two 128-bit halves of the same sector; the pointers are 32-byte aligned
+// (pool allocations, double4 indexing)
+__device__ __forceinline__ double4 ldg256(const double4* p) {
+    double4 v;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void stg256(double4* p, double x, double y, double z, double w) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w) : "memory");
+}
 __device__ __forceinline__ d3 ld3(const double* __restrict__ p, int64_t i) {
     return d3{p[3 * i], p[3 * i + 1], p[3 * i + 2]};
 }

@@ -869,8 +869,8 @@ __device__ __forceinline__ void pair_stamps(int kd, const Corners& q, int4 id, d
 // (-2 - position), -1 not a plan entry
 __device__ __forceinline__ void plan_store(int dst, d3 tg, double w, double4* __restrict__ main_out,
                                            double4* __restrict__ side_out) {
-    if (dst >= 0) main_out[dst] = make_double4(tg.x, tg.y, tg.z, w);
-    else if (dst <= -2) side_out[-2 - dst] = make_double4(tg.x, tg.y, tg.z, w);
+    if (dst >= 0) stg256(main_out + dst, tg.x, tg.y, tg.z, w);
+    else if (dst <= -2) stg256(side_out + (-2 - dst), tg.x, tg.y, tg.z, w);
 }
 
 // The driver's cached stamp plan as seen by k_partial_ndb (all null: no plan).
@@ -1030,7 +1030,7 @@ __device__ __forceinline__ void ndb_counts(const PlanView& plan, int* __restrict
 
 // One pass per inner LG iteration over all P pairs (wl == null) or over the n pair
 // indices of a worklist (the near list of the step's near / far split).
-__global__ void __launch_bounds__(128, 5) k_partial_ndb(NdbArgs A, int64_t n, int* __restrict__ eng_count,
+__global__ void __launch_bounds__(128, 6) k_partial_ndb(NdbArgs A, int64_t n, int* __restrict__ eng_count,
                                                         const PlanView plan, const int* __restrict__ wl) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid = k < n;
@@ -1166,7 +1166,7 @@ __global__ void __launch_bounds__(256, 4) k_collision_terms(const int* __restric
         if (cloth_only && ids[k] >= n_cloth) keep = false;
         int64_t o = 4 * a + k;
         key[o] = keep ? free_index[ids[k]] : 0x7fffffff;
-        if (keep) stamp_out[o] = make_double4(tg[k].x, tg[k].y, tg[k].z, w[k]);  // others are never read
+        if (keep) stg256(stamp_out + o, tg[k].x, tg[k].y, tg[k].z, w[k]);  // others are never read
     }
 }
 

@@ -219,7 +219,7 @@ __global__ void k_gather_terms(const int* __restrict__ pick, const int* __restri
         const int4 id = idx[sel[o >> 2]];
         const int slot = o & 3;
         ids_out[k] = slot == 0 ? id.x : (slot == 1 ? id.y : (slot == 2 ? id.z : id.w));
-        const double4 st = stamp[o];
+        const double4 st = ldg256(stamp + o);
         w_out[k] = st.w;
         t_out[3 * k] = st.x;
         t_out[3 * k + 1] = st.y;
@@ -310,7 +310,7 @@ __global__ void k_stamp_delta(int nf, const int* __restrict__ seg_beg, const int
 __global__ void k_pack_stamps(const double* __restrict__ w, const double* __restrict__ t, int m,
                               double4* __restrict__ stamp) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < m) stamp[i] = make_double4(t[3 * i], t[3 * i + 1], t[3 * i + 2], w[i]);
+    if (i < m) stg256(stamp + i, t[3 * i], t[3 * i + 1], t[3 * i + 2], w[i]);
 }
 
 // stamp sort keys from cloth vertex ids: free row or sentinel (constraints.py:252-255)

@@ -216,7 +216,7 @@ __global__ void k_assemble_rhs(int nf, const int* __restrict__ free_ids, const d
             for (; k + 4 <= ke; k += 4) {
                 double4 st[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) st[u] = stamp[stamp_src != nullptr ? stamp_src[k + u] : k + u];
+                for (int u = 0; u < 4; ++u) st[u] = ldg256(stamp + (stamp_src != nullptr ? stamp_src[k + u] : k + u));
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const double w = st[u].w;
@@ -230,7 +230,7 @@ __global__ void k_assemble_rhs(int nf, const int* __restrict__ free_ids, const d
             // entry order (gather through the row sort) or plan order (stamp_src == null:
             // streamed); a row with side-list entries interleaves both lists by merge key
             const bool from_main = q >= qe || (k < ke && side.main_key[k] < side.key[q]);
-            const double4 st = from_main ? stamp[stamp_src != nullptr ? stamp_src[k] : k] : side.stamp[q];
+            const double4 st = ldg256(from_main ? stamp + (stamp_src != nullptr ? stamp_src[k] : k) : side.stamp + q);
             k += from_main ? 1 : 0;
             q += from_main ? 0 : 1;
             const double w = st.w;
@@ -979,7 +979,7 @@ __global__ void k_energy_grad(int n, const double* __restrict__ x, const double*
     }
     if (seg_beg != nullptr) {
         for (int k = seg_beg[fi]; k < seg_end[fi]; ++k) {
-            const double4 st = stamp[stamp_src[k]];
+            const double4 st = ldg256(stamp + stamp_src[k]);
             if (!(st.w > 0.0)) continue;  // plan entry outside the engaged set
             g = g + st.w * (xv - d3{st.x, st.y, st.z});
         }

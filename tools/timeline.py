@@ -23,7 +23,7 @@ if PAPER:
     sim.step()  # buffers of the 67-iteration regime sized once, outside the profile
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-    for _ in range(1 if PAPER else 2):
+    for _ in range(int(__import__("os").environ.get("TL_STEPS", "1")) if PAPER else 2):
         sim.step()
     torch.cuda.synchronize()
 prof.export_chrome_trace(f"gpurun_out/timeline{TAG}.json")
