@@ -238,7 +238,7 @@ enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_N
 // partial CCD near / far split margin, in units of d_hat (k_near_split)
 constexpr double kFarDelta = 0.05;
 enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_FLAG = 7, I_WLF = 8,
-       I_NEW = 9, I_NEAR = 10, I_COUNT = 12 };
+       I_NEW = 9, I_NEAR = 10, I_FARREST = 11, I_COUNT = 12 };
 
 const int kStages = 8;
 enum { T_WARM = 0, T_LOCAL, T_GLOBAL, T_SMOOTH, T_BROAD, T_PARTIAL, T_FULL, T_RF };
@@ -340,6 +340,7 @@ struct cs_scene {
     bool lazy_exit = std::getenv("CS_NO_LAZY_EXIT") == nullptr;  // read at scene creation
     bool far_pairs = std::getenv("CS_NO_FAR_PAIRS") == nullptr;  // partial CCD near / far split
     DBuf<double> vdn;  // per world vertex |candidate - anchor|
+    DBuf<int> far_rest;  // far pairs the displacement bound does not settle (k_far_gate)
     bool rows_from_delta = false;  // rows_act must be rebuilt from delta after the rhs
     bool plan_enabled = std::getenv("CS_NO_STAMP_PLAN") == nullptr;  // read at scene creation
     DBuf<unsigned long long> pkey, pkey2, nkey, nkey_s, skey_sd, skey_sd2;
@@ -1344,10 +1345,9 @@ struct cs_scene {
     // partial CCD near / far split of a freshly engaged set (k_near_split's argument)
     int near_split(PairBuf& pr) {
         pr.split_valid = false;
-        // (with a cached stamp plan the partial pass is bound by the plan pairs' fused
-        // stamp writes, and the split only adds its own passes: single-iteration outer
-        // loops only)
-        if (cfg.barrier_mode != CS_BARRIER_DBB && far_pairs && !(plan_enabled && last_loop_lg > 1)) {
+        // (every regime: with the light far gate the split also pays in multi-iteration
+        // outer loops with a cached stamp plan, whose pairs take the classifier path)
+        if (cfg.barrier_mode != CS_BARRIER_DBB && far_pairs) {
             CS_RET(pr.near_l.ensure(pr.P));
             cub::CountingInputIterator<int> it(0);
             const NearPair pred{pr.toi.p, pr.dist.p, (2.0 * cfg.d_hat + kFarDelta * cfg.d_hat) * (1.0 + 1e-6) + 1e-12};
@@ -2062,15 +2062,22 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
                                  0, nullptr, 1, nullptr};
                 if (cur->split_valid) {
                     // near list: the full classifier; far list (after it, reversed): gated on the
-                    // largest vertex displacement anchor -> candidate (k_partial_far)
+                    // largest vertex displacement anchor -> candidate (k_far_gate, then the rest through
+                    // the classifier: k_partial_ndb_dyn)
                     const long long nn = cur->n_near, nfar = cur->P - cur->n_near;
                     CS_RET(vdn.ensure(nw));
                     k_vertex_disp_norm<<<grid(nw), 256, 0, s>>>(anchor_w.p, xc_w.p, nw, vdn.p);
                     if (nn > 0)
                         k_partial_ndb<<<grid(nn, 128), 128, 0, s>>>(na, nn, d_iscal.p + I_ENG, plan, cur->near_l.p);
-                    if (nfar > 0)
-                        k_partial_far<<<std::max(1, std::min(grid(nfar, 128), 5 * sm_count)), 128, 0, s>>>(
-                            na, nfar, d_iscal.p + I_ENG, plan, cur->near_l.p + nn, cur->dist.p, vdn.p);
+                    if (nfar > 0) {
+                        CS_RET(far_rest.ensure(nfar));
+                        CS_TRY(cudaMemsetAsync(d_iscal.p + I_FARREST, 0, sizeof(int), s));
+                        k_far_gate<<<grid(nfar), 256, 0, s>>>(na, nfar, plan, cur->near_l.p + nn, cur->dist.p, vdn.p,
+                                                               far_rest.p, d_iscal.p + I_FARREST);
+                        k_partial_ndb_dyn<<<6 * sm_count, 128, 0, s>>>(na, d_iscal.p + I_FARREST, d_iscal.p + I_ENG,
+                                                                        plan, far_rest.p);
+                        ++launches;
+                    }
                     launches += 3;
                 } else {
                     k_partial_ndb<<<grid(cur->P, 128), 128, 0, s>>>(na, cur->P, d_iscal.p + I_ENG, plan, nullptr);

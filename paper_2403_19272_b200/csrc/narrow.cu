@@ -760,7 +760,7 @@ struct EngageOut {
 };
 __device__ __forceinline__ double ndb_weight(int life, double k, double base);
 
-__global__ void __launch_bounds__(128, 8) k_witness(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
+__global__ void __launch_bounds__(128, 10) k_witness(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
                           const double* __restrict__ x, int64_t P, double* __restrict__ bary,
                           double* __restrict__ dist, double* __restrict__ normal, double* __restrict__ p1_out,
                           double* __restrict__ p2_out, EngageOut eo) {
@@ -1043,34 +1043,56 @@ __global__ void __launch_bounds__(128, 6) k_partial_ndb(NdbArgs A, int64_t n, in
 // The far list of the split (NearPair): a far pair whose witness distance d exceeds
 // (2 d_hat + D1 + D2)(1 + 1e-6) + 1e-12, with D1, D2 the largest anchor -> candidate
 // displacements of its two sides' vertices (vdisp), is provably inactive and disengaged
-// (NearPair's argument): life 0, engaged 0, weight 0 without the classifier; the others
-// (and any far pair that has joined the stamp plan) run it.  Uniform grid-stride loop
-// (block_count inside).
-__global__ void __launch_bounds__(128, 5) k_partial_far(NdbArgs A, int64_t n, int* __restrict__ eng_count,
-                                                        const PlanView plan, const int* __restrict__ wl,
-                                                        const double* __restrict__ dist,
-                                                        const double* __restrict__ vdisp) {
+// (NearPair's argument): life 0, engaged 0, weight 0 without the classifier.  Two light
+// passes (one kernel with the classifier inlined ran the bound check at the
+// classifier's register budget and occupancy: 0.62 vs 0.36 ms on the skirt):
+// k_far_gate: the displacement bound alone (no classifier inlined, full occupancy for
+// a streaming pass); pairs it settles are written inactive and disengaged, the rest
+// (bound failed, or in the stamp plan) are appended to a worklist (any order: each
+// pair's result is its own, the counts are sums) that k_partial_ndb_dyn runs through
+// the full classifier, its length read on the device.
+__global__ void __launch_bounds__(256) k_far_gate(NdbArgs A, int64_t n, const PlanView plan,
+                                                  const int* __restrict__ wl, const double* __restrict__ dist,
+                                                  const double* __restrict__ vdisp, int* __restrict__ rest,
+                                                  int* __restrict__ n_rest) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool full = false;
+    int i = 0;
+    if (k < n) {
+        i = wl[k];
+        const int4 id = A.idx[i];
+        const bool vt = A.kind[i] == CS_VT;
+        const double v0 = vdisp[id.x], v1 = vdisp[id.y], v2 = vdisp[id.z], v3 = vdisp[id.w];
+        const double D1 = vt ? v0 : fmax(v0, v1), D2 = vt ? fmax(fmax(v1, v2), v3) : fmax(v2, v3);
+        const bool in_plan = plan.pair_u != nullptr && plan.pair_u[i] >= 0;
+        if (!in_plan && dist[i] > (2.0 * A.d_hat + D1 + D2) * (1.0 + 1e-6) + 1e-12) {
+            A.life[i] = 0;
+            A.engaged[i] = 0;
+            A.weight[i] = 0.0;
+        } else {
+            full = true;
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, full);
+    if (m) {
+        const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(n_rest, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (full) rest[base + __popc(m & ((1u << lane) - 1u))] = i;
+    }
+}
+
+__global__ void __launch_bounds__(128, 6) k_partial_ndb_dyn(NdbArgs A, const int* __restrict__ n_dev,
+                                                            int* __restrict__ eng_count, const PlanView plan,
+                                                            const int* __restrict__ wl) {
+    const int64_t n = *n_dev;
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = b0 + threadIdx.x;
         const bool valid = k < n;
         const int64_t i = valid ? (int64_t)wl[k] : 0;
         bool eng = false, fresh = false, alive = false;
-        if (valid) {
-            const int4 id = A.idx[i];
-            const bool vt = A.kind[i] == CS_VT;
-            const double v0 = vdisp[id.x], v1 = vdisp[id.y], v2 = vdisp[id.z], v3 = vdisp[id.w];
-            const double D1 = vt ? v0 : fmax(v0, v1), D2 = vt ? fmax(fmax(v1, v2), v3) : fmax(v2, v3);
-            // a pair in the stamp plan (it joined through an earlier full pass) keeps the full
-            // path: its fused stamps must be rewritten
-            const bool in_plan = plan.pair_u != nullptr && plan.pair_u[i] >= 0;
-            if (!in_plan && dist[i] > (2.0 * A.d_hat + D1 + D2) * (1.0 + 1e-6) + 1e-12) {
-                A.life[i] = 0;
-                A.engaged[i] = 0;
-                A.weight[i] = 0.0;
-            } else {
-                ndb_pair(A, plan, i, eng, fresh, alive);
-            }
-        }
+        if (valid) ndb_pair(A, plan, i, eng, fresh, alive);
         ndb_counts(plan, eng_count, A.live_count, i, eng, fresh, alive);
     }
 }
@@ -1081,7 +1103,7 @@ __global__ void __launch_bounds__(128, 5) k_partial_far(NdbArgs A, int64_t n, in
 // displacements D1 + D2 stay below delta, every sampled offset of a far pair keeps
 // |o_start| >= d > D1 + D2 >= |o_end - o_start| (so Q > 0) and its frozen-witness gap
 // at the candidate is >= d - D1 - D2 > 2 d_hat: the classifier finds it inactive and
-// disengaged (life 0, weight 0), as k_partial_far assumes.  Predicate for
+// disengaged (life 0, weight 0), as k_far_gate assumes.  Predicate for
 // cub::DevicePartition (near first in pair order, far after it in reverse order).
 struct NearPair {
     const double* __restrict__ toi;
@@ -1092,7 +1114,7 @@ struct NearPair {
     }
 };
 
-// |x1 - x0| per world vertex (k_partial_far's displacement bounds)
+// |x1 - x0| per world vertex (k_far_gate's displacement bounds)
 __global__ void k_vertex_disp_norm(const double* __restrict__ x0, const double* __restrict__ x1, int n,
                                    double* __restrict__ out) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
