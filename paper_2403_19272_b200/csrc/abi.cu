@@ -201,7 +201,7 @@ struct PairBuf {
     DBuf<double> toi, filt, bary, dist, normal, weight;
     DBuf<int> life;
     DBuf<uint8_t> engaged;
-    // near / far split for the partial CCD passes on this set (engage, k_near_split)
+    // near / far split for the partial CCD passes on this set (k_witness, EngageOut.split)
     DBuf<int> near_l;        // near pairs (pair order), then the far pairs (reversed)
     long long n_near = 0;    // read at the sync after engage (I_NEAR)
     bool split_valid = false;
@@ -235,7 +235,7 @@ struct PairBuf {
 // scalar slots (doubles) read back in one D2H copy
 enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_NORM1 = 5, S_NORM_F = 6,
        S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_MINBITS = 10, S_TOIEXIT = 11, S_COUNT = 16 };
-// partial CCD near / far split margin, in units of d_hat (k_near_split)
+// partial CCD near / far split margin, in units of d_hat (EngageOut.near_thresh)
 constexpr double kFarDelta = 0.05;
 enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_FLAG = 7, I_WLF = 8,
        I_NEW = 9, I_NEAR = 10, I_FARREST = 11, I_COUNT = 12 };
@@ -1317,15 +1317,31 @@ struct cs_scene {
             return engage(pr);
         }
         plan_valid = false;
+        pr.split_valid = false;
         CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
         if (pr.P == 0) return 0;
+        // the near / far split rides along (the far-pair classification on the toi and
+        // distance this pass has in registers)
+        EngageOut eo{pr.toi.p, pr.life.p, cfg.d_hat, cfg.ndb_k, cfg.ndb_base, pr.engaged.p, pr.weight.p,
+                     d_iscal.p + I_ENG, nullptr, nullptr, nullptr, 0.0};
+        if (far_pairs) {
+            CS_RET(pr.near_l.ensure(pr.P));
+            CS_TRY(cudaMemsetAsync(d_iscal.p + I_NEAR, 0, sizeof(int), s));
+            CS_TRY(cudaMemsetAsync(d_iscal.p + I_FARREST, 0, sizeof(int), s));
+            eo.split = pr.near_l.p;
+            eo.n_near = d_iscal.p + I_NEAR;
+            eo.n_far = d_iscal.p + I_FARREST;
+            eo.near_thresh = near_thresh();
+        }
         k_witness<<<grid(pr.P, 128), 128, 0, s>>>(pr.kind.p, pr.idx.p, xw, pr.P, pr.bary.p, pr.dist.p,
-                                                  pr.normal.p, nullptr, nullptr,
-                                                  EngageOut{pr.toi.p, pr.life.p, cfg.d_hat, cfg.ndb_k, cfg.ndb_base,
-                                                            pr.engaged.p, pr.weight.p, d_iscal.p + I_ENG});
+                                                  pr.normal.p, nullptr, nullptr, eo);
         ++launches;
-        return near_split(pr);
+        CS_CHECK_LAUNCH();
+        pr.split_valid = far_pairs;  // counts read at the caller's sync (I_NEAR)
+        return 0;
     }
+
+    double near_thresh() const { return (2.0 * cfg.d_hat + kFarDelta * cfg.d_hat) * (1.0 + 1e-6) + 1e-12; }
 
     // engaged set + weights after a site; count lands in I_ENG
     int engage(PairBuf& pr) {
@@ -1339,26 +1355,7 @@ struct cs_scene {
             k_engage_init<<<grid(pr.P), 256, 0, s>>>(pr.toi.p, pr.dist.p, pr.life.p, pr.P, cfg.d_hat, cfg.ndb_k,
                                                      cfg.ndb_base, pr.engaged.p, pr.weight.p, d_iscal.p + I_ENG);
         ++launches;
-        return near_split(pr);
-    }
-
-    // partial CCD near / far split of a freshly engaged set (k_near_split's argument)
-    int near_split(PairBuf& pr) {
-        pr.split_valid = false;
-        // (every regime: with the light far gate the split also pays in multi-iteration
-        // outer loops with a cached stamp plan, whose pairs take the classifier path)
-        if (cfg.barrier_mode != CS_BARRIER_DBB && far_pairs) {
-            CS_RET(pr.near_l.ensure(pr.P));
-            cub::CountingInputIterator<int> it(0);
-            const NearPair pred{pr.toi.p, pr.dist.p, (2.0 * cfg.d_hat + kFarDelta * cfg.d_hat) * (1.0 + 1e-6) + 1e-12};
-            size_t bytes = 0;
-            cub::DevicePartition::If(nullptr, bytes, it, pr.near_l.p, d_iscal.p + I_NEAR, (int)pr.P, pred, s);
-            CS_RET(cub_tmp.ensure(bytes));
-            CS_TRY(cub::DevicePartition::If(cub_tmp.p, bytes, it, pr.near_l.p, d_iscal.p + I_NEAR, (int)pr.P, pred,
-                                            s));
-            ++launches;
-            pr.split_valid = true;  // counts read at the caller's sync (I_NEAR)
-        }
+        pr.split_valid = false;  // DBB: no partial CCD classes, no split
         CS_CHECK_LAUNCH();
         return 0;
     }

@@ -757,7 +757,47 @@ struct EngageOut {
     uint8_t* __restrict__ engaged;
     double* __restrict__ weight;
     int* __restrict__ count;
+    // near / far split (the far-pair classification below k_far_gate, from the same toi and distance):
+    // near pairs fill split[0, n_near) from the front, far pairs split[n_near, P) from
+    // the back, block-aggregated (each block's pairs stay in pair order); null: no split
+    int* __restrict__ split;
+    int* __restrict__ n_near;
+    int* __restrict__ n_far;
+    double near_thresh;
 };
+
+// block-aggregated two-sided append (one atomic per block and side)
+__device__ __forceinline__ void block_split_append(bool valid, bool near, int64_t i, int64_t P,
+                                                   int* __restrict__ split, int* __restrict__ n_near,
+                                                   int* __restrict__ n_far) {
+    __shared__ int sh_pre[2][32];
+    __shared__ int sh_base[2];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    const unsigned mn = __ballot_sync(0xffffffffu, valid && near);
+    const unsigned mf = __ballot_sync(0xffffffffu, valid && !near);
+    __syncthreads();
+    if (lane == 0) {
+        sh_pre[0][w] = __popc(mn);
+        sh_pre[1][w] = __popc(mf);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        int tot = 0;
+        for (int k = 0; k < nw; ++k) {
+            const int c = sh_pre[threadIdx.x][k];
+            sh_pre[threadIdx.x][k] = tot;
+            tot += c;
+        }
+        sh_base[threadIdx.x] = tot ? atomicAdd(threadIdx.x == 0 ? n_near : n_far, tot) : 0;
+    }
+    __syncthreads();
+    if (valid) {
+        const int side = near ? 0 : 1;
+        const int pos = sh_base[side] + sh_pre[side][w] + __popc((near ? mn : mf) & ((1u << lane) - 1u));
+        if (near) split[pos] = (int)i;
+        else split[P - 1 - pos] = (int)i;
+    }
+}
 __device__ __forceinline__ double ndb_weight(int life, double k, double base);
 
 __global__ void __launch_bounds__(128, 10) k_witness(const int8_t* __restrict__ kind, const int4* __restrict__ idx,
@@ -765,7 +805,7 @@ __global__ void __launch_bounds__(128, 10) k_witness(const int8_t* __restrict__ 
                           double* __restrict__ dist, double* __restrict__ normal, double* __restrict__ p1_out,
                           double* __restrict__ p2_out, EngageOut eo) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    bool eng = false;
+    bool eng = false, near = false;
     if (i < P) {
     const int kd = kind[i];
     Corners a = gather4(x, idx[i]);
@@ -799,9 +839,11 @@ __global__ void __launch_bounds__(128, 10) k_witness(const int8_t* __restrict__ 
         eng = (t == t) || (d < 2.0 * eo.d_hat);
         eo.engaged[i] = eng;
         eo.weight[i] = eng ? ndb_weight(eo.life[i], eo.k_ndb, eo.base) : 0.0;
+        near = (t == t) || !(d > eo.near_thresh);
     }
     }
     if (eo.count != nullptr) block_count(eng, eo.count);
+    if (eo.split != nullptr) block_split_append(i < P, near, i, P, eo.split, eo.n_near, eo.n_far);
 }
 
 __device__ __forceinline__ double ndb_weight(int life, double k, double base) {
@@ -1040,10 +1082,10 @@ __global__ void __launch_bounds__(128, 6) k_partial_ndb(NdbArgs A, int64_t n, in
     ndb_counts(plan, eng_count, A.live_count, i, eng, fresh, alive);
 }
 
-// The far list of the split (NearPair): a far pair whose witness distance d exceeds
+// The far list of the split (EngageOut.split): a far pair whose witness distance d exceeds
 // (2 d_hat + D1 + D2)(1 + 1e-6) + 1e-12, with D1, D2 the largest anchor -> candidate
 // displacements of its two sides' vertices (vdisp), is provably inactive and disengaged
-// (NearPair's argument): life 0, engaged 0, weight 0 without the classifier.  Two light
+// (the split's argument, below): life 0, engaged 0, weight 0 without the classifier.  Two light
 // passes (one kernel with the classifier inlined ran the bound check at the
 // classifier's register budget and occupancy: 0.62 vs 0.36 ms on the skirt):
 // k_far_gate: the displacement bound alone (no classifier inlined, full occupancy for
@@ -1098,21 +1140,13 @@ __global__ void __launch_bounds__(128, 6) k_partial_ndb_dyn(NdbArgs A, const int
 }
 
 // Near / far split of a step's pair set at its engagement (anchor = the interval start
-// of every partial CCD on this set).  Far: not hit by the full CCD and witness distance
-// d > (2 d_hat + delta)(1 + 1e-6) + 1e-12.  While both sides' anchor -> candidate
-// displacements D1 + D2 stay below delta, every sampled offset of a far pair keeps
-// |o_start| >= d > D1 + D2 >= |o_end - o_start| (so Q > 0) and its frozen-witness gap
-// at the candidate is >= d - D1 - D2 > 2 d_hat: the classifier finds it inactive and
-// disengaged (life 0, weight 0), as k_far_gate assumes.  Predicate for
-// cub::DevicePartition (near first in pair order, far after it in reverse order).
-struct NearPair {
-    const double* __restrict__ toi;
-    const double* __restrict__ dist;
-    double thresh;  // (2 d_hat + delta)(1 + 1e-6) + 1e-12
-    __host__ __device__ __forceinline__ bool operator()(int i) const {
-        return toi[i] == toi[i] || !(dist[i] > thresh);
-    }
-};
+// of every partial CCD on this set), classified inside k_witness (EngageOut.split).
+// Far: not hit by the full CCD and witness distance d > (2 d_hat + delta)(1 + 1e-6) +
+// 1e-12.  While both sides' anchor -> candidate displacements D1 + D2 stay below
+// delta, every sampled offset of a far pair keeps |o_start| >= d > D1 + D2 >=
+// |o_end - o_start| (so Q > 0) and its frozen-witness gap at the candidate is >=
+// d - D1 - D2 > 2 d_hat: the classifier finds it inactive and disengaged (life 0,
+// weight 0), as k_far_gate assumes (which checks the per-pair D1 + D2, not delta).
 
 // |x1 - x0| per world vertex (k_far_gate's displacement bounds)
 __global__ void k_vertex_disp_norm(const double* __restrict__ x0, const double* __restrict__ x1, int n,

@@ -77,3 +77,9 @@ for g, a, b in gl[:2]:
     for e in sorted([e for e in ev if e.get("ph") == "X" and e.get("cat") in ("cuda_runtime", "cpu_op", "python_function")
                      and e["ts"] + e.get("dur", 0) >= a and e["ts"] <= b], key=lambda e: e["ts"])[:40]:
         print(f"    {e['ts'] - a:9.1f} +{e.get('dur', 0):8.1f}  {e.get('cat')}: {e['name'][:80]}")
+
+# per-launch durations of kernels named in TL_KERNELS (comma-separated substrings)
+import os  # noqa: E402
+for sub in filter(None, os.environ.get("TL_KERNELS", "").split(",")):
+    sel = [e for e in dev if sub in e["name"]]
+    print(f"{sub}: " + ", ".join(f"{e['dur']:.0f}us g{e.get('args', {}).get('grid', ['?'])[0]}" for e in sel))
