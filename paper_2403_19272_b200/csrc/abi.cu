@@ -340,7 +340,8 @@ struct cs_scene {
     bool lazy_exit = std::getenv("CS_NO_LAZY_EXIT") == nullptr;  // read at scene creation
     bool far_pairs = std::getenv("CS_NO_FAR_PAIRS") == nullptr;  // partial CCD near / far split
     DBuf<double> vdn;  // per world vertex |candidate - anchor|
-    DBuf<int> far_rest;  // far pairs the displacement bound does not settle (k_far_gate)
+    DBuf<int> far_rest;
+    DBuf<int> ktile;  // per-tile kept stamp-entry counts -> offsets (k_kept_tiles)  // far pairs the displacement bound does not settle (k_far_gate)
     bool rows_from_delta = false;  // rows_act must be rebuilt from delta after the rhs
     bool plan_enabled = std::getenv("CS_NO_STAMP_PLAN") == nullptr;  // read at scene creation
     DBuf<unsigned long long> pkey, pkey2, nkey, nkey_s, skey_sd, skey_sd2;
@@ -1446,24 +1447,22 @@ struct cs_scene {
                                                   nullptr, nullptr);
         ++launches;
         // entries on a free row (a third of them are not: obstacle / pinned endpoints,
-        // zero weight), compacted in order: indices, then their keys
-        bytes = 0;
-        cub::DeviceSelect::If(nullptr, bytes, it, ssrc.p, d_iscal.p + I_COUNT + 7, (int)m, RowKept{skey.p, nf}, s);
-        CS_RET(cub_tmp.ensure(bytes));
-        CS_TRY(cub::DeviceSelect::If(cub_tmp.p, bytes, it, ssrc.p, d_iscal.p + I_COUNT + 7, (int)m,
-                                     RowKept{skey.p, nf}, s));
-        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 7], d_iscal.p + I_COUNT + 7, sizeof(int), cudaMemcpyDeviceToHost,
-                               s));
+        // zero weight), compacted in order with their keys (tile counts, scan, write)
+        const long long ntile = (A + kKeptTile - 1) / kKeptTile;
+        CS_RET(ktile.ensure(ntile + 1));
+        CS_TRY(cudaMemsetAsync(ktile.p + ntile, 0, sizeof(int), s));
+        k_kept_tiles<<<(int)ntile, kKeptTile, 0, s>>>(skey.p, A, nf, ktile.p);
+        CS_RET(scan(ktile.p, ktile.p, (int)ntile + 1));
+        CS_TRY(cudaMemcpyAsync(&h_iscal[I_COUNT + 7], ktile.p + ntile, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CS_RET(skey_c.ensure(m));
+        k_kept_compact<<<(int)ntile, kKeptTile, 0, s>>>(skey.p, A, nf, ktile.p, ssrc.p, skey_c.p);
+        launches += 3;
         CS_TRY(hsync(__LINE__));
         const long long mc = h_iscal[I_COUNT + 7];
         static const bool trace_stamps = std::getenv("CS_TRACE_SITES") != nullptr;
         if (trace_stamps)
             std::fprintf(stderr, "[cs stamps] engaged %lld stamps %lld on free rows %lld\n", A, m, mc);
         if (mc == 0) return 0;
-        CS_RET(skey_c.ensure(mc));
-        k_gather_keys<<<std::max(1, std::min(grid(mc), 16 * sm_count)), 256, 0, s>>>(ssrc.p, d_iscal.p + I_COUNT + 7,
-                                                                                    skey.p, skey_c.p);
-        ++launches;
         // stable sort by free row keeps np.add.at's per-vertex order; only the bits a
         // row needs
         int bits = 1;

@@ -192,17 +192,46 @@ struct U64Less {
 };
 
 // compaction helpers for the per-stage collision-terms entry point
-// stable compaction of the stamp entries that land on a free row: indices from
-// DeviceSelect::If with this predicate, then their keys
-struct RowKept {
-    const int* __restrict__ key;
-    int nf;
-    __host__ __device__ __forceinline__ bool operator()(int i) const { return key[i] < nf; }
-};
-__global__ void k_gather_keys(const int* __restrict__ idx, const int* __restrict__ count,
-                              const int* __restrict__ key, int* __restrict__ out) {
-    const int n = count[0];
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = key[idx[j]];
+// Stable compaction of the stamp entries on a free row (key < nf) with their keys,
+// in entry order (replaces a flag select + key gather): tile counts over 256 pairs
+// (4 entries each) per block, an exclusive scan, then each block writes its kept
+// (entry, key) pairs at its offset.
+constexpr int kKeptTile = 256;
+__global__ void __launch_bounds__(kKeptTile) k_kept_tiles(const int* __restrict__ key, int64_t A, int nf,
+                                                         int* __restrict__ tile_count) {
+    using Reduce = cub::BlockReduce<int, kKeptTile>;
+    __shared__ typename Reduce::TempStorage tmp;
+    const int64_t a = (int64_t)blockIdx.x * kKeptTile + threadIdx.x;
+    int c = 0;
+    if (a < A) {
+        const int4 k = reinterpret_cast<const int4*>(key)[a];
+        c = (k.x < nf) + (k.y < nf) + (k.z < nf) + (k.w < nf);
+    }
+    const int t = Reduce(tmp).Sum(c);
+    if (threadIdx.x == 0) tile_count[blockIdx.x] = t;
+}
+__global__ void __launch_bounds__(kKeptTile) k_kept_compact(const int* __restrict__ key, int64_t A, int nf,
+                                                           const int* __restrict__ tile_off, int* __restrict__ src,
+                                                           int* __restrict__ key_out) {
+    using Scan = cub::BlockScan<int, kKeptTile>;
+    __shared__ typename Scan::TempStorage tmp;
+    const int64_t a = (int64_t)blockIdx.x * kKeptTile + threadIdx.x;
+    int4 k = make_int4(nf, nf, nf, nf);
+    if (a < A) k = reinterpret_cast<const int4*>(key)[a];
+    const int kk[4] = {k.x, k.y, k.z, k.w};
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c += kk[j] < nf;
+    int pos;
+    Scan(tmp).ExclusiveSum(c, pos);
+    pos += tile_off[blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (kk[j] < nf) {
+            src[pos] = (int)(4 * a + j);
+            key_out[pos] = kk[j];
+            ++pos;
+        }
 }
 
 __global__ void k_key_kept(const int* __restrict__ key, int m, int nf, uint8_t* __restrict__ flag) {

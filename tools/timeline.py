@@ -81,5 +81,6 @@ for g, a, b in gl[:2]:
 # per-launch durations of kernels named in TL_KERNELS (comma-separated substrings)
 import os  # noqa: E402
 for sub in filter(None, os.environ.get("TL_KERNELS", "").split(",")):
-    sel = [e for e in dev if sub in e["name"]]
-    print(f"{sub}: " + ", ".join(f"{e['dur']:.0f}us g{e.get('args', {}).get('grid', ['?'])[0]}" for e in sel))
+    sel = [(k, e) for k, e in enumerate(dev) if sub in e["name"]]
+    print(f"{sub}: " + ", ".join(f"{e['dur']:.0f}us g{e.get('args', {}).get('grid', ['?'])[0]} "
+                                 f"(after {dev[k - 1]['name'][:28] if k else '-'})" for k, e in sel))
