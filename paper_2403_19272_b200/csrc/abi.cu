@@ -279,7 +279,7 @@ struct cs_scene {
     PairBuf pa, pb;  // current and next pair sets
     PairBuf* cur = &pa;
     PairBuf* nxt = &pb;
-    DBuf<int> sel, skey, ssrc, skey_s, ssrc_s, seg_beg, seg_end, rowflag, rows_act, skey_c;
+    DBuf<int> sel, skey, ssrc, skey_s, ssrc_s, seg_beg, seg_end, rowflag, rows_act, skey_c;  // rowflag: stage APIs
     DBuf<double4> stamp;  // collision stamps: target xyz + weight
     DBuf<unsigned long long> hkeys;
     DBuf<int> hvals;
@@ -341,7 +341,8 @@ struct cs_scene {
     bool far_pairs = std::getenv("CS_NO_FAR_PAIRS") == nullptr;  // partial CCD near / far split
     DBuf<double> vdn;  // per world vertex |candidate - anchor|
     DBuf<int> far_rest;
-    DBuf<int> ktile;  // per-tile kept stamp-entry counts -> offsets (k_kept_tiles)  // far pairs the displacement bound does not settle (k_far_gate)
+    DBuf<int> ktile;  // per-tile kept stamp-entry counts -> offsets (k_kept_tiles)
+    DBuf<int> ftile;  // per-tile engaged-flag counts -> offsets (k_flag_tiles)  // far pairs the displacement bound does not settle (k_far_gate)
     bool rows_from_delta = false;  // rows_act must be rebuilt from delta after the rhs
     bool plan_enabled = std::getenv("CS_NO_STAMP_PLAN") == nullptr;  // read at scene creation
     DBuf<unsigned long long> pkey, pkey2, nkey, nkey_s, skey_sd, skey_sd2;
@@ -1434,14 +1435,19 @@ struct cs_scene {
         CS_RET(skey_s.ensure(m));
         CS_RET(ssrc_s.ensure(m));
         CS_RET(stamp.ensure(m));
-        CS_RET(rowflag.ensure(m));
         CS_RET(rows_act.ensure(m));
-        // compact engaged pair ids in pair order
+        // compact engaged pair ids in pair order (tile counts, scan, writes)
         size_t bytes = 0;
         cub::CountingInputIterator<int> it(0);
-        cub::DeviceSelect::Flagged(nullptr, bytes, it, pr.engaged.p, sel.p, d_iscal.p + I_BAD, (int)pr.P, s);
-        CS_RET(cub_tmp.ensure(bytes));
-        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, pr.engaged.p, sel.p, d_iscal.p + I_BAD, (int)pr.P, s));
+        {
+            const long long nt = (pr.P + kFlagTile - 1) / kFlagTile;
+            CS_RET(ftile.ensure(nt + 1));
+            CS_TRY(cudaMemsetAsync(ftile.p + nt, 0, sizeof(int), s));
+            k_flag_tiles<<<(int)nt, 256, 0, s>>>(pr.engaged.p, pr.P, ftile.p);
+            CS_RET(scan(ftile.p, ftile.p, (int)nt + 1));
+            k_flag_compact<<<(int)nt, 256, 0, s>>>(pr.engaged.p, pr.P, ftile.p, sel.p);
+            launches += 3;
+        }
         k_collision_terms<<<grid(A), 256, 0, s>>>(sel.p, A, pr.kind.p, pr.idx.p, xw, pr.bary.p, pr.normal.p,
                                                   pr.weight.p, cfg.d_hat, n, free_index.p, 0, skey.p, stamp.p,
                                                   nullptr, nullptr);
@@ -1472,14 +1478,15 @@ struct cs_scene {
         CS_RET(cub_tmp.ensure(bytes));
         CS_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, skey_c.p, skey_s.p, ssrc.p, ssrc_s.p, (int)mc, 0,
                                                bits, s));
-        CS_TRY(cudaMemsetAsync(rowflag.p, 0, sizeof(int) * mc, s));
-        k_mark_segments<<<grid(mc), 256, 0, s>>>(skey_s.p, (int)mc, nf, seg_beg.p, seg_end.p, rowflag.p);
+        k_mark_segments<<<grid(mc), 256, 0, s>>>(skey_s.p, (int)mc, nf, seg_beg.p, seg_end.p, nullptr);
         ++launches;
+        // distinct rows, ascending = the rows with a non-empty segment (a select over the
+        // nf rows instead of the mc sorted entries)
         bytes = 0;
-        cub::DeviceSelect::Flagged(nullptr, bytes, skey_s.p, rowflag.p, rows_act.p, d_iscal.p + I_ROWS, (int)mc, s);
+        cub::DeviceSelect::If(nullptr, bytes, it, rows_act.p, d_iscal.p + I_ROWS, nf, SegNonEmpty{seg_end.p}, s);
         CS_RET(cub_tmp.ensure(bytes));
-        CS_TRY(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, skey_s.p, rowflag.p, rows_act.p, d_iscal.p + I_ROWS,
-                                          (int)mc, s));
+        CS_TRY(cub::DeviceSelect::If(cub_tmp.p, bytes, it, rows_act.p, d_iscal.p + I_ROWS, nf, SegNonEmpty{seg_end.p},
+                                     s));
         CS_CHECK_LAUNCH();
         stamps_valid = true;
         n_stamp_rows = (int)std::min<long long>(m, nf);  // upper bound; exact count read on device

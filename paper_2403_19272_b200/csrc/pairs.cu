@@ -95,10 +95,50 @@ __global__ void k_mark_segments(const int* __restrict__ skey, int m, int nrows, 
     if (k >= nrows) return;
     if (j == 0 || skey[j - 1] != k) {
         seg_beg[k] = j;
-        rows_out_flag[j] = 1;
+        if (rows_out_flag) rows_out_flag[j] = 1;
     }
     if (j == m - 1 || skey[j + 1] != k) seg_end[k] = j + 1;
 }
+
+// Stable compaction of the indices of the set u8 flags (the engaged pairs, in pair
+// order): tiles of 1024 flags (256 threads x 4), tile counts, exclusive scan, writes.
+constexpr int kFlagTile = 1024;
+__device__ __forceinline__ uchar4 load_flags4(const uint8_t* __restrict__ f, int64_t i0, int64_t n) {
+    if (i0 + 4 <= n) return *reinterpret_cast<const uchar4*>(f + i0);
+    uchar4 v = make_uchar4(0, 0, 0, 0);
+    if (i0 < n) v.x = f[i0];
+    if (i0 + 1 < n) v.y = f[i0 + 1];
+    if (i0 + 2 < n) v.z = f[i0 + 2];
+    return v;
+}
+__global__ void __launch_bounds__(256) k_flag_tiles(const uint8_t* __restrict__ flags, int64_t n,
+                                                    int* __restrict__ tile_count) {
+    using Reduce = cub::BlockReduce<int, 256>;
+    __shared__ typename Reduce::TempStorage tmp;
+    const uchar4 v = load_flags4(flags, (int64_t)blockIdx.x * kFlagTile + 4 * threadIdx.x, n);
+    const int t = Reduce(tmp).Sum((v.x != 0) + (v.y != 0) + (v.z != 0) + (v.w != 0));
+    if (threadIdx.x == 0) tile_count[blockIdx.x] = t;
+}
+__global__ void __launch_bounds__(256) k_flag_compact(const uint8_t* __restrict__ flags, int64_t n,
+                                                      const int* __restrict__ tile_off, int* __restrict__ out) {
+    using Scan = cub::BlockScan<int, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    const int64_t i0 = (int64_t)blockIdx.x * kFlagTile + 4 * threadIdx.x;
+    const uchar4 v = load_flags4(flags, i0, n);
+    const bool f[4] = {v.x != 0, v.y != 0, v.z != 0, v.w != 0};
+    int pos;
+    Scan(tmp).ExclusiveSum(f[0] + f[1] + f[2] + f[3], pos);
+    pos += tile_off[blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (f[j]) out[pos++] = (int)(i0 + j);
+}
+
+// rows with a non-empty stamp segment (seg_end zeroed before k_mark_segments)
+struct SegNonEmpty {
+    const int* __restrict__ seg_end;
+    __host__ __device__ __forceinline__ bool operator()(int r) const { return seg_end[r] > 0; }
+};
 
 // ---- stamp plan (driver-cached row order of the collision stamps, reused across the
 // LG iterations of one pair set).  Plan entries are ordered by the merge key
