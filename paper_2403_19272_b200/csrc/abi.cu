@@ -342,6 +342,7 @@ struct cs_scene {
     DBuf<double> vdn;  // per world vertex |candidate - anchor|
     DBuf<int> far_rest;
     DBuf<int> ktile;  // per-tile kept stamp-entry counts -> offsets (k_kept_tiles)
+    long long live_known = -1;  // pairs with a nonzero life span after the last partial CCD (-1: unknown)
     DBuf<int> ftile;  // per-tile engaged-flag counts -> offsets (k_flag_tiles)  // far pairs the displacement bound does not settle (k_far_gate)
     bool rows_from_delta = false;  // rows_act must be rebuilt from delta after the rhs
     bool plan_enabled = std::getenv("CS_NO_STAMP_PLAN") == nullptr;  // read at scene creation
@@ -1369,12 +1370,16 @@ struct cs_scene {
         if (nw_.P == 0) return 0;
         CS_TRY(cudaMemsetAsync(nw_.life.p, 0, sizeof(int) * nw_.P, s));
         if (old.P == 0) return 0;
-        CS_TRY(cudaMemsetAsync(d_iscal.p + I_LIVE, 0, sizeof(int), s));
-        k_count_nonzero<<<grid(old.P), 256, 0, s>>>(old.life.p, old.P, d_iscal.p + I_LIVE);
-        ++launches;
-        CS_TRY(cudaMemcpyAsync(&h_iscal[I_LIVE], d_iscal.p + I_LIVE, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CS_TRY(hsync(__LINE__));
-        const long long live = h_iscal[I_LIVE];
+        long long live = live_known;
+        if (live < 0) {  // not counted by the last partial CCD pass on this set
+            CS_TRY(cudaMemsetAsync(d_iscal.p + I_LIVE, 0, sizeof(int), s));
+            k_count_nonzero<<<grid(old.P), 256, 0, s>>>(old.life.p, old.P, d_iscal.p + I_LIVE);
+            ++launches;
+            CS_TRY(cudaMemcpyAsync(&h_iscal[I_LIVE], d_iscal.p + I_LIVE, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CS_TRY(hsync(__LINE__));
+            live = h_iscal[I_LIVE];
+        }
+        live_known = -1;
         if (live == 0) return 0;
         unsigned long long cap = 1024;
         while (cap < 2ull * (unsigned long long)live) cap <<= 1;
@@ -1908,6 +1913,7 @@ void cs_scene::release() {
 int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_report* rep) {
     launches = 0;
     n_syncs = 0;
+    live_known = -1;
     const long long plan_reuses0 = plan_reuses;
     ev_used = 0;
     spans.clear();
@@ -2052,6 +2058,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             stage(T_PARTIAL);
             CS_TRY(cudaMemsetAsync(d_iscal.p + I_ENG, 0, sizeof(int), s));
             CS_TRY(cudaMemsetAsync(d_iscal.p + I_NEW, 0, sizeof(int), s));
+            CS_TRY(cudaMemsetAsync(d_iscal.p + I_LIVE, 0, sizeof(int), s));  // the carry's table size
             // collect pairs joining the stamp plan; write the plan's next stamps (fused terms)
             const bool track = plan_valid && plan_pr == cur;
             PlanView plan{};
@@ -2062,7 +2069,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             if (cur->P) {
                 const NdbArgs na{cur->kind.p, cur->idx.p, anchor_w.p, xc_w.p, pat, cur->bary.p, cur->normal.p,
                                  cfg.d_hat, cfg.ndb_k, cfg.ndb_base, cur->life.p, cur->weight.p, cur->engaged.p,
-                                 0, nullptr, 1, nullptr};
+                                 0, nullptr, 1, d_iscal.p + I_LIVE};
                 if (cur->split_valid) {
                     // near list: the full classifier; far list (after it, reversed): gated on the
                     // largest vertex displacement anchor -> candidate (k_far_gate, then the rest through
@@ -2093,6 +2100,7 @@ int cs_scene::step(const double* pin_next_h, const double* obs_next_h, cs_step_r
             dx_last = h_scal[S_SQ] / std::max(std::sqrt(3.0 * nf), 1.0);
             A = h_iscal[I_ENG];
             plan_new = h_iscal[I_NEW];
+            live_known = cur->P ? h_iscal[I_LIVE] : -1;
 
             if (cfg.iteration_cap && lg >= cfg.iteration_cap) {
                 cap_hit = true;
