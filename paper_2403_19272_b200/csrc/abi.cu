@@ -235,8 +235,10 @@ struct PairBuf {
 // scalar slots (doubles) read back in one D2H copy
 enum { S_SQ = 0, S_CLAMP_MIN = 1, S_CLAMP = 2, S_CLAMP_BAD = 3, S_NORM0 = 4, S_NORM1 = 5, S_NORM_F = 6,
        S_RES = 7, S_DFNORM = 8, S_DFSCALE = 9, S_MINBITS = 10, S_TOIEXIT = 11, S_COUNT = 16 };
-// partial CCD near / far split margin, in units of d_hat (EngageOut.near_thresh)
-constexpr double kFarDelta = 0.05;
+// partial CCD near / far split margin, in units of d_hat (EngageOut.near_thresh; the
+// far gate's per-pair displacement bound is what makes a far pair exact, this only
+// sets which list a pair starts in: 0.05 and 0.25 were slower than 0)
+constexpr double kFarDelta = 0.0;
 enum { I_ENG = 0, I_BAD = 1, I_ROWS = 2, I_VT = 3, I_EE = 4, I_FALLBACK = 5, I_LIVE = 6, I_FLAG = 7, I_WLF = 8,
        I_NEW = 9, I_NEAR = 10, I_FARREST = 11, I_COUNT = 12 };
 

@@ -1142,11 +1142,14 @@ __global__ void __launch_bounds__(128, 6) k_partial_ndb_dyn(NdbArgs A, const int
 // Near / far split of a step's pair set at its engagement (anchor = the interval start
 // of every partial CCD on this set), classified inside k_witness (EngageOut.split).
 // Far: not hit by the full CCD and witness distance d > (2 d_hat + delta)(1 + 1e-6) +
-// 1e-12.  While both sides' anchor -> candidate displacements D1 + D2 stay below
-// delta, every sampled offset of a far pair keeps |o_start| >= d > D1 + D2 >=
-// |o_end - o_start| (so Q > 0) and its frozen-witness gap at the candidate is >=
-// d - D1 - D2 > 2 d_hat: the classifier finds it inactive and disengaged (life 0,
-// weight 0), as k_far_gate assumes (which checks the per-pair D1 + D2, not delta).
+// 1e-12 (delta = kFarDelta d_hat, 0: a larger margin only moved pairs from the cheap
+// gate into the classifier, measured).  With D1, D2 the largest anchor -> candidate
+// displacements of the two sides' vertices, a far pair with d > 2 d_hat + D1 + D2
+// keeps every sampled offset at |o_start| >= d > D1 + D2 >= |o_end - o_start| (so
+// Q > 0) and its frozen-witness gap at the candidate at >= d - D1 - D2 > 2 d_hat: the
+// classifier finds it inactive and disengaged (life 0, weight 0), which is what
+// k_far_gate writes for it (with a relative slack on the bound); the others run the
+// classifier.
 
 // |x1 - x0| per world vertex (k_far_gate's displacement bounds)
 __global__ void k_vertex_disp_norm(const double* __restrict__ x0, const double* __restrict__ x1, int n,
