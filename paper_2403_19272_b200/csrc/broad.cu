@@ -674,10 +674,11 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_vt(EntryTable V, Entr
                     vt_index(k, mt, inv_mt, i, j);
                     const int zi = S.vzs[i], zj = S.tzs[j];
                     const int v = S.vprim[i];
-                    hit = ((zi | zj) & 7) == 7 && !(zi & zj & 8) && S.vcode[i] == S.tcode[j] && v != S.ta[j] &&
-                          v != S.tb[j] && v != S.tc[j] && S.vlo[0][i] <= S.thi[0][j] && S.tlo[0][j] <= S.vhi[0][i] &&
-                          S.vlo[1][i] <= S.thi[1][j] && S.tlo[1][j] <= S.vhi[1][i] && S.vlo[2][i] <= S.thi[2][j] &&
-                          S.tlo[2][j] <= S.vhi[2][i];
+                    hit = ((zi | zj) & 7) == 7 && !(zi & zj & 8) && S.vcode[i] == S.tcode[j];
+                    hit = hit && ((v != S.ta[j]) & (v != S.tb[j]) & (v != S.tc[j]) & (S.vlo[0][i] <= S.thi[0][j]) &
+                                  (S.tlo[0][j] <= S.vhi[0][i]) & (S.vlo[1][i] <= S.thi[1][j]) &
+                                  (S.tlo[1][j] <= S.vhi[1][i]) & (S.vlo[2][i] <= S.thi[2][j]) &
+                                  (S.tlo[2][j] <= S.vhi[2][i]));
                 }
                 const unsigned m = warp_hits<PASS>(hit, masks, it);
                 if (PASS == 1 && ((m >> lane) & 1u)) {
@@ -800,10 +801,12 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_ee(EntryTable E, cons
                     int i, j;
                     rr_index(k, m, inv_m, i, j);
                     const int zi = S.zs[i], zj = S.zs[j];
-                    hit = ((zi | zj) & 7) == 7 && !(zi & zj & 8) && S.code[i] == S.code[j] && S.a[i] != S.a[j] &&
-                          S.a[i] != S.b[j] && S.b[i] != S.a[j] && S.b[i] != S.b[j] && S.lo[0][i] <= S.hi[0][j] &&
-                          S.lo[0][j] <= S.hi[0][i] && S.lo[1][i] <= S.hi[1][j] && S.lo[1][j] <= S.hi[1][i] &&
-                          S.lo[2][i] <= S.hi[2][j] && S.lo[2][j] <= S.hi[2][i];
+                    // the selective class / cell tests short-circuit; the adjacency and box
+                    // tests after them are evaluated branch-free (fewer divergent branches)
+                    hit = ((zi | zj) & 7) == 7 && !(zi & zj & 8) && S.code[i] == S.code[j];
+                    hit = hit && ((S.a[i] != S.a[j]) & (S.a[i] != S.b[j]) & (S.b[i] != S.a[j]) & (S.b[i] != S.b[j]) &
+                                  (S.lo[0][i] <= S.hi[0][j]) & (S.lo[0][j] <= S.hi[0][i]) & (S.lo[1][i] <= S.hi[1][j]) &
+                                  (S.lo[1][j] <= S.hi[1][i]) & (S.lo[2][i] <= S.hi[2][j]) & (S.lo[2][j] <= S.hi[2][i]));
                 }
                 const unsigned msk = warp_hits<PASS>(hit, masks, it);
                 if (PASS == 1 && ((msk >> lane) & 1u)) {
