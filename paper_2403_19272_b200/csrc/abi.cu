@@ -1370,8 +1370,12 @@ struct cs_scene {
     // extra 4-byte read-back sizes it; nothing to do when no pair is alive).
     int carry(PairBuf& old, PairBuf& nw_) {
         if (nw_.P == 0) return 0;
-        CS_TRY(cudaMemsetAsync(nw_.life.p, 0, sizeof(int) * nw_.P, s));
-        if (old.P == 0) return 0;
+        // life spans of the new set: zero unless the lookup below writes every one
+        const auto zero_new = [&]() -> int {
+            CS_TRY(cudaMemsetAsync(nw_.life.p, 0, sizeof(int) * nw_.P, s));
+            return 0;
+        };
+        if (old.P == 0) return zero_new();
         long long live = live_known;
         if (live < 0) {  // not counted by the last partial CCD pass on this set
             CS_TRY(cudaMemsetAsync(d_iscal.p + I_LIVE, 0, sizeof(int), s));
@@ -1382,14 +1386,14 @@ struct cs_scene {
             live = h_iscal[I_LIVE];
         }
         live_known = -1;
-        if (live == 0) return 0;
+        if (live == 0) return zero_new();
         unsigned long long cap = 1024;
         while (cap < 2ull * (unsigned long long)live) cap <<= 1;
         CS_RET(hkeys.ensure(cap));
         CS_RET(hvals.ensure(cap));
         k_fill_u64<<<grid(cap), 256, 0, s>>>(hkeys.p, cap, CS_EMPTY_KEY);
         k_hash_insert<<<grid(old.P), 256, 0, s>>>(old.keys.p, old.life.p, old.P, hkeys.p, hvals.p, cap - 1);
-        k_hash_lookup<<<grid(nw_.P), 256, 0, s>>>(nw_.keys.p, nw_.P, hkeys.p, hvals.p, cap - 1, nw_.life.p);
+        k_hash_lookup<<<grid(nw_.P), 256, 0, s>>>(nw_.keys.p, nw_.P, hkeys.p, hvals.p, cap - 1, nw_.life.p);  // all P
         launches += 3;
         CS_CHECK_LAUNCH();
         return 0;
